@@ -1,0 +1,727 @@
+// capi.cu -- the extern "C" boundary (include/slq_b200.h).
+//
+// Each entry point marshals host buffers, runs the device kernels on the
+// context stream and maps slq::Error (thrown by the kernels' host code) to an
+// slq_status plus a thread-local message, mirroring the reference's exception
+// types (errors.hpp:9-76).
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "lsqr.cuh"
+#include "qr.cuh"
+#include "sketch.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return SLQ_OK;
+    } catch (const slq::Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return SLQ_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SLQ_CUDA;
+    }
+}
+
+void need(bool cond, int code, const char* what) {
+    if (!cond) slq::fail(code, what);
+}
+
+// ------------------------------------------------------------ kernels
+
+// column-major staging (rows x n, ld = rows_cap) -> row-major A rows [r0, r0+rows)
+__global__ void colmajor_to_rows_kernel(const double* src, int64_t rows, int64_t rows_cap, int64_t n,
+                                        const double* bsrc, double* A, int64_t ld) {
+    __shared__ double tile[32][33];
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    for (int k = ty; k < 32; k += 8) {
+        const int64_t c = c0 + k, r = r0 + tx;
+        double v = 0.0;
+        if (r < rows) {
+            if (c < n) v = src[c * rows_cap + r];
+            else if (c == n && bsrc) v = bsrc[r];
+        }
+        tile[k][tx] = v;
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+        const int64_t r = r0 + k, c = c0 + tx;
+        if (r < rows && c < ld) A[r * ld + c] = tile[tx][k];
+    }
+}
+
+__global__ void set_column_kernel(double* A, int64_t m, int64_t ld, int64_t col, const double* v) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < m) A[i * ld + col] = v ? v[i] : 0.0;
+}
+
+__global__ void transpose_square_kernel(const double* M, int64_t n, double* Mt) {
+    __shared__ double tile[32][33];
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32, r0 = static_cast<int64_t>(blockIdx.y) * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int k = ty; k < 32; k += 8)
+        if (c0 + k < n && r0 + tx < n) tile[k][tx] = M[(c0 + k) * n + r0 + tx];
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8)
+        if (r0 + k < n && c0 + tx < n) Mt[(r0 + k) * n + c0 + tx] = tile[tx][k];
+}
+
+// y_j = Q(:, j)^T v, warp per column (Q column-major d x n)
+__global__ void gemv_t_kernel(const double* Q, int64_t d, int64_t n, const double* v, double* y) {
+    const int lane = threadIdx.x & 31;
+    const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (j >= n) return;
+    double s = 0.0;
+    for (int64_t i = lane; i < d; i += 32) s += Q[j * d + i] * v[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) y[j] = s;
+}
+
+__global__ void csc_to_compact_kernel(const int64_t* rows, const double* vals, int64_t nnz, uint32_t* out) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e < nnz) out[e] = static_cast<uint32_t>(rows[e]) | (vals[e] < 0.0 ? 0x80000000u : 0u);
+}
+
+
+
+void transpose_square(slq_ctx* ctx, const double* M, int64_t n, double* Mt) {
+    dim3 g(static_cast<unsigned>(slq::ceil_div(n, 32)), static_cast<unsigned>(slq::ceil_div(n, 32)));
+    transpose_square_kernel<<<g, dim3(32, 8), 0, ctx->stream>>>(M, n, Mt);
+    SLQ_LAUNCH_CHECK(ctx);
+}
+
+// Host column-major block (m x n, lda) + optional b -> device layout.
+void upload_dense(slq_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, const double* b, double* dst,
+                  int64_t ld) {
+    slq::Workspace& ws = ctx->ws;
+    const int64_t rows_cap = std::max<int64_t>(32, std::min<int64_t>(m, (int64_t(256) << 20) / (8 * std::max<int64_t>(n + 1, 1))));
+    double* stg[2];
+    for (int s = 0; s < 2; ++s) stg[s] = static_cast<double*>(ws.staging[s].ensure(sizeof(double) * rows_cap * (n + 1)));
+    cudaStream_t cs;
+    SLQ_CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaEvent_t copied[2], done[2];
+    for (int s = 0; s < 2; ++s) {
+        SLQ_CUDA_CHECK(cudaEventCreateWithFlags(&copied[s], cudaEventDisableTiming));
+        SLQ_CUDA_CHECK(cudaEventCreateWithFlags(&done[s], cudaEventDisableTiming));
+        SLQ_CUDA_CHECK(cudaEventRecord(done[s], ctx->stream));
+    }
+    int64_t k = 0;
+    for (int64_t r0 = 0; r0 < m; r0 += rows_cap, ++k) {
+        const int s = static_cast<int>(k & 1);
+        const int64_t rows = std::min(rows_cap, m - r0);
+        SLQ_CUDA_CHECK(cudaStreamWaitEvent(cs, done[s], 0));
+        if (n > 0)
+            SLQ_CUDA_CHECK(cudaMemcpy2DAsync(stg[s], sizeof(double) * rows_cap, A + r0, sizeof(double) * lda,
+                                             sizeof(double) * rows, n, cudaMemcpyHostToDevice, cs));
+        if (b)
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(stg[s] + n * rows_cap, b + r0, sizeof(double) * rows,
+                                           cudaMemcpyHostToDevice, cs));
+        SLQ_CUDA_CHECK(cudaEventRecord(copied[s], cs));
+        SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, copied[s], 0));
+        dim3 g(static_cast<unsigned>(slq::ceil_div(ld, 32)), static_cast<unsigned>(slq::ceil_div(rows, 32)));
+        colmajor_to_rows_kernel<<<g, dim3(32, 8), 0, ctx->stream>>>(stg[s], rows, rows_cap, n,
+                                                                   b ? stg[s] + n * rows_cap : nullptr,
+                                                                   dst + r0 * ld, ld);
+        SLQ_LAUNCH_CHECK(ctx);
+        SLQ_CUDA_CHECK(cudaEventRecord(done[s], ctx->stream));
+    }
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(cs));
+    for (int s = 0; s < 2; ++s) {
+        cudaEventDestroy(copied[s]);
+        cudaEventDestroy(done[s]);
+    }
+    cudaStreamDestroy(cs);
+}
+
+struct Timer {
+    cudaEvent_t e;
+    explicit Timer(cudaStream_t s) {
+        SLQ_CUDA_CHECK(cudaEventCreate(&e));
+        SLQ_CUDA_CHECK(cudaEventRecord(e, s));
+    }
+    ~Timer() { cudaEventDestroy(e); }
+    double since(const Timer& o) const {
+        float ms = 0.f;
+        SLQ_CUDA_CHECK(cudaEventSynchronize(e));
+        SLQ_CUDA_CHECK(cudaEventElapsedTime(&ms, o.e, e));
+        return ms * 1e-3;
+    }
+};
+
+// Device buffers of the preconditioner: [M | Mt | R | x0 | qtb | status]
+struct PrecondBufs {
+    double *M, *Mt, *R, *x0, *qtb, *status;
+};
+
+PrecondBufs precond_bufs(slq_ctx* ctx, int64_t n) {
+    double* base = static_cast<double*>(ctx->ws.mats.ensure(sizeof(double) * (3 * n * n + 2 * n + 8)));
+    return {base, base + n * n, base + 2 * n * n, base + 3 * n * n, base + 3 * n * n + n, base + 3 * n * n + 2 * n};
+}
+
+// QR of Yaug (d x (n+1) incl. Sb) -> M, Mt, x0 on the device; times in t[3].
+void build_precond_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, bool with_sb, double* Q,
+                       const PrecondBufs& P, double* t) {
+    Timer t0(ctx->stream);
+    slq::qr_factor_dev(ctx, Yaug, d, n, with_sb ? n + 1 : n, d, P.R, with_sb ? P.qtb : nullptr, Q, nullptr);
+    Timer t1(ctx->stream);
+    slq::tri_inverse_dev(ctx, P.R, n, P.M, P.Mt);
+    Timer t2(ctx->stream);
+    if (with_sb) slq::trmv_upper_dev(ctx, P.Mt, n, P.qtb, P.x0);
+    Timer t3(ctx->stream);
+    if (t) {
+        t[0] = t1.since(t0);
+        t[1] = t2.since(t1);
+        t[2] = t3.since(t2);
+    }
+}
+
+void fill_report(slq_report* r, const slq::LsqrOut& o) {
+    if (!r) return;
+    std::memset(r, 0, sizeof(*r));
+    r->iterations = o.iterations;
+    r->termination = o.termination;
+    r->sync_count = o.allreduces;
+    r->broadcasts = 0;
+    r->init_reductions = o.init_allreduces;
+    r->init_broadcasts = 0;
+    r->wall_time = o.seconds;
+    r->n_estimate = o.n_estimate;
+    r->n_err = o.n_err;
+    r->n_true = o.n_true;
+    r->backward_error = o.backward_error;
+}
+
+int run_solve(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed, const slq_solve_opts* opts_in,
+              double* x_out, slq_report* report, slq_phase_times* times, double* est) {
+    return guarded([&] {
+        need(ctx && A, SLQ_INVALID_ARG, "solve: null handle");
+        slq_solve_opts opts;
+        if (opts_in) opts = *opts_in;
+        else slq_solve_opts_default(&opts);
+        const int64_t n = A->n;
+        need(n >= 1, SLQ_INVALID_DIMS, "solve: n < 1");
+        need(d > n, SLQ_INVALID_DIMS, "SketchParams: need n < d <= m");
+        need(zeta >= 1 && zeta <= d, SLQ_INVALID_SPARSITY, "SketchParams: need 1 <= zeta <= d");
+        const int64_t launches0 = ctx->launches, nccl0 = ctx->nccl_calls;
+        slq::Workspace& ws = ctx->ws;
+        double* Yaug = static_cast<double*>(ws.yaug.ensure(sizeof(double) * d * (n + 1)));
+        const int64_t m = A->m;
+        uint32_t* compact = static_cast<uint32_t*>(ws.compact.ensure(sizeof(uint32_t) * std::max<int64_t>(1, m * zeta)));
+        int64_t* work = zeta > 32 ? static_cast<int64_t*>(ws.tmp.ensure(sizeof(int64_t) * m * zeta)) : nullptr;
+
+        Timer t0(ctx->stream);
+        slq::generate_sparse_sign_dev(ctx, d, zeta, seed, A->row_begin, m, compact, work, nullptr, nullptr, nullptr);
+        Timer t1(ctx->stream);
+        slq::sketch_apply_compact_dev(ctx, A, d, compact, nullptr, zeta, 1.0 / std::sqrt(static_cast<double>(zeta)),
+                                      false, Yaug);
+        Timer t2(ctx->stream);
+        slq::reduce_sum_root(ctx, Yaug, d * (n + 1));
+        Timer t3(ctx->stream);
+        PrecondBufs P = precond_bufs(ctx, n);
+        double tq[3] = {0, 0, 0};
+        if (ctx->rank == 0) {
+            double st = 0.0;
+            try {
+                build_precond_dev(ctx, Yaug, d, n, true, nullptr, P, tq);
+            } catch (const slq::Error& e) {
+                if (!ctx->comm) throw;
+                st = e.code;
+                g_last_error = e.what();
+            }
+            if (ctx->comm) {
+                SLQ_CUDA_CHECK(cudaMemcpyAsync(P.status, &st, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+                SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            }
+        }
+        Timer t4(ctx->stream);
+        if (ctx->comm) {
+            // status first so no rank waits on a broadcast that will never come
+            slq::broadcast_root(ctx, P.status, 1);
+            double st = 0.0;
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(&st, P.status, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+            SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            if (st != 0.0) slq::fail(static_cast<int>(st), ctx->rank == 0 ? g_last_error : "preconditioner build failed on rank 0");
+            slq::broadcast_root(ctx, P.M, n * n);
+            slq::broadcast_root(ctx, P.Mt, n * n);
+            slq::broadcast_root(ctx, P.x0, n);
+        }
+        Timer t5(ctx->stream);
+        double* x = static_cast<double*>(ws.qr_w.ensure(sizeof(double) * (n + 8)));
+        slq::LsqrOut lo;
+        slq::lsqr_dev(ctx, A, nullptr, P.M, P.Mt, P.x0, x, opts, est, nullptr, nullptr, lo);
+        Timer t6(ctx->stream);
+        if (opts.backward_tol > 0.0 || opts.a_norm_est > 0.0)
+            lo.backward_error = slq::backward_error_dev(ctx, A, x, opts.a_norm_est > 0.0 ? opts.a_norm_est : 1.0);
+        if (x_out) SLQ_CUDA_CHECK(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        fill_report(report, lo);
+        if (times) {
+            times->generate = t1.since(t0);
+            times->apply = t2.since(t1);
+            times->reduce = t3.since(t2);
+            times->qr = tq[0];
+            times->inverse = tq[1];
+            times->x0 = tq[2] + t5.since(t4);
+            times->lsqr = t6.since(t5);
+            times->total = t6.since(t0);
+            times->lsqr_per_iteration = lo.iterations > 0 ? lo.seconds / static_cast<double>(lo.iterations) : 0.0;
+            times->nccl_calls = ctx->nccl_calls - nccl0;
+            times->kernel_launches = ctx->launches - launches0;
+        }
+    });
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* slq_last_error(void) { return g_last_error.c_str(); }
+const char* slq_version(void) { return "slq_b200 0.1 (sm_100a)"; }
+
+void slq_solve_opts_default(slq_solve_opts* o) {
+    std::memset(o, 0, sizeof(*o));
+    o->eps = 1e-10;  // lsqr.hpp:15
+    o->maxit = 100;  // lsqr.hpp:16
+}
+
+int slq_ctx_create(int device, slq_ctx** out) {
+    return guarded([&] {
+        need(out != nullptr, SLQ_INVALID_ARG, "ctx_create: null out");
+        int ndev = 0;
+        SLQ_CUDA_CHECK(cudaGetDeviceCount(&ndev));
+        need(device >= 0 && device < ndev, SLQ_INVALID_ARG, "ctx_create: bad device");
+        SLQ_CUDA_CHECK(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        SLQ_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+        need(prop.major >= 10, SLQ_UNSUPPORTED, "ctx_create: needs an sm_100 (Blackwell) GPU");
+        auto* c = new slq_ctx();
+        c->device = device;
+        c->num_sms = prop.multiProcessorCount;
+        SLQ_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+        *out = c;
+    });
+}
+
+int slq_ctx_destroy(slq_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        slq::comm_destroy(ctx);
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int slq_ctx_set_stream(slq_ctx* ctx, void* s) {
+    return guarded([&] {
+        need(ctx != nullptr, SLQ_INVALID_ARG, "null ctx");
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        ctx->stream = static_cast<cudaStream_t>(s);
+        ctx->own_stream = false;
+    });
+}
+
+int slq_ctx_synchronize(slq_ctx* ctx) {
+    return guarded([&] { SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int64_t slq_ctx_kernel_launches(const slq_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int slq_comm_unique_id(unsigned char id_out[128]) {
+    return guarded([&] { slq::comm_unique_id(id_out); });
+}
+
+int slq_ctx_init_comm(slq_ctx* ctx, const unsigned char id[128], int rank, int nranks) {
+    return guarded([&] { slq::comm_init(ctx, id, rank, nranks); });
+}
+
+int slq_partition_rows(int64_t m, int p, int64_t* boundaries) {
+    return guarded([&] {
+        // distsim.hpp:31-42
+        need(p >= 1 && static_cast<int64_t>(p) <= m, SLQ_INVALID_DIMS, "partition_rows: need 1 <= p <= m");
+        const int64_t stride = m / p;
+        for (int k = 0; k < p; ++k) boundaries[k] = stride * k;
+        boundaries[p] = m;
+    });
+}
+
+int slq_generate_sparse_sign(slq_ctx* ctx, int64_t d, int64_t col_begin, int64_t ncols, int64_t zeta, uint64_t seed,
+                             int64_t* row_indices, double* values, int64_t* col_pointers,
+                             slq_rejection_stats* stats) {
+    return guarded([&] {
+        need(ctx != nullptr, SLQ_INVALID_ARG, "null ctx");
+        if (zeta > d || zeta < 1) slq::fail(SLQ_INVALID_SPARSITY, "generate_sparse_sign: need 1 <= zeta <= d");
+        need(ncols >= 0 && col_begin >= 0, SLQ_INVALID_DIMS, "generate_sparse_sign: bad column window");
+        SLQ_CUDA_CHECK(cudaSetDevice(ctx->device));
+        const int64_t nnz = ncols * zeta;
+        slq::DevBuf rows, vals, cp, st;
+        int64_t* drows = static_cast<int64_t*>(rows.ensure(sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
+        double* dvals = static_cast<double*>(vals.ensure(sizeof(double) * std::max<int64_t>(nnz, 1)));
+        int64_t* dcp = static_cast<int64_t*>(cp.ensure(sizeof(int64_t) * (ncols + 1)));
+        unsigned long long* dst = static_cast<unsigned long long*>(st.ensure(2 * sizeof(unsigned long long)));
+        SLQ_CUDA_CHECK(cudaMemsetAsync(dst, 0, 2 * sizeof(unsigned long long), ctx->stream));
+        slq::generate_sparse_sign_dev(ctx, d, zeta, seed, col_begin, ncols, nullptr, drows, dvals, dcp, dst);
+        if (row_indices) SLQ_CUDA_CHECK(cudaMemcpyAsync(row_indices, drows, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost, ctx->stream));
+        if (values) SLQ_CUDA_CHECK(cudaMemcpyAsync(values, dvals, sizeof(double) * nnz, cudaMemcpyDeviceToHost, ctx->stream));
+        if (col_pointers) SLQ_CUDA_CHECK(cudaMemcpyAsync(col_pointers, dcp, sizeof(int64_t) * (ncols + 1), cudaMemcpyDeviceToHost, ctx->stream));
+        unsigned long long hs[2] = {0, 0};
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(hs, dst, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (stats) {
+            stats->columns_resampled += static_cast<int64_t>(hs[0]);
+            stats->resample_rounds += static_cast<int64_t>(hs[1]);
+        }
+    });
+}
+
+int slq_rejection_sample_columns(slq_ctx* ctx, int64_t d, int64_t m, int64_t zeta, uint64_t seed, int64_t* out,
+                                 slq_rejection_stats* stats) {
+    return guarded([&] {
+        need(ctx != nullptr, SLQ_INVALID_ARG, "null ctx");
+        if (zeta > d || zeta < 1) slq::fail(SLQ_INVALID_SPARSITY, "rejection_sample_columns: need 1 <= zeta <= d");
+        SLQ_CUDA_CHECK(cudaSetDevice(ctx->device));
+        const int64_t nnz = m * zeta;
+        slq::DevBuf rows, st;
+        int64_t* drows = static_cast<int64_t*>(rows.ensure(sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
+        unsigned long long* dst = static_cast<unsigned long long*>(st.ensure(2 * sizeof(unsigned long long)));
+        SLQ_CUDA_CHECK(cudaMemsetAsync(dst, 0, 2 * sizeof(unsigned long long), ctx->stream));
+        // sketch.hpp:105-124 draws column j from substream 2j: identical to the
+        // index part of sparse_sign_block with col_begin = 0.
+        slq::generate_sparse_sign_dev(ctx, d, zeta, seed, 0, m, nullptr, drows, nullptr, nullptr, dst);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(out, drows, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost, ctx->stream));
+        unsigned long long hs[2] = {0, 0};
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(hs, dst, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (stats) {
+            stats->columns_resampled += static_cast<int64_t>(hs[0]);
+            stats->resample_rounds += static_cast<int64_t>(hs[1]);
+        }
+    });
+}
+
+int slq_dense_upload(slq_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                     int64_t row_begin, slq_dense** out) {
+    return guarded([&] {
+        need(ctx && out, SLQ_INVALID_ARG, "dense_upload: null argument");
+        need(m >= 0 && n >= 0 && lda >= m && row_begin >= 0, SLQ_INVALID_DIMS, "dense_upload: bad shape");
+        need(A != nullptr || m * n == 0, SLQ_INVALID_ARG, "dense_upload: null A");
+        SLQ_CUDA_CHECK(cudaSetDevice(ctx->device));
+        auto* h = new slq_dense();
+        h->ctx = ctx;
+        h->m = m;
+        h->n = n;
+        h->ld = slq::dense_ld(n);
+        h->row_begin = row_begin;
+        h->owned = true;
+        h->has_b = b != nullptr;
+        cudaError_t e = cudaMalloc(&h->A, sizeof(double) * std::max<int64_t>(1, m * h->ld));
+        if (e != cudaSuccess) {
+            delete h;
+            SLQ_CUDA_CHECK(e);
+        }
+        if (m > 0) upload_dense(ctx, A, m, n, lda, b, h->A, h->ld);
+        *out = h;
+    });
+}
+
+int slq_dense_create(slq_ctx* ctx, int64_t m, int64_t n, int64_t row_begin, slq_dense** out, double** dev_ptr,
+                     int64_t* ld) {
+    return guarded([&] {
+        need(ctx && out, SLQ_INVALID_ARG, "dense_create: null argument");
+        need(m >= 0 && n >= 0 && row_begin >= 0, SLQ_INVALID_DIMS, "dense_create: bad shape");
+        SLQ_CUDA_CHECK(cudaSetDevice(ctx->device));
+        auto* h = new slq_dense();
+        h->ctx = ctx;
+        h->m = m;
+        h->n = n;
+        h->ld = slq::dense_ld(n);
+        h->row_begin = row_begin;
+        h->owned = true;
+        cudaError_t e = cudaMalloc(&h->A, sizeof(double) * std::max<int64_t>(1, m * h->ld));
+        if (e != cudaSuccess) {
+            delete h;
+            SLQ_CUDA_CHECK(e);
+        }
+        SLQ_CUDA_CHECK(cudaMemsetAsync(h->A, 0, sizeof(double) * m * h->ld, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        *out = h;
+        if (dev_ptr) *dev_ptr = h->A;
+        if (ld) *ld = h->ld;
+    });
+}
+
+int slq_dense_wrap(slq_ctx* ctx, double* dev_ptr, int64_t m, int64_t n, int64_t ld, int64_t row_begin,
+                   slq_dense** out) {
+    return guarded([&] {
+        need(ctx && out && (dev_ptr || m == 0), SLQ_INVALID_ARG, "dense_wrap: null argument");
+        need(ld >= n + 1 && ld % 4 == 0, SLQ_INVALID_DIMS, "dense_wrap: ld must be >= n+1 and a multiple of 4");
+        need((reinterpret_cast<uintptr_t>(dev_ptr) & 31) == 0, SLQ_INVALID_ARG, "dense_wrap: pointer not 32-byte aligned");
+        auto* h = new slq_dense();
+        h->ctx = ctx;
+        h->A = dev_ptr;
+        h->m = m;
+        h->n = n;
+        h->ld = ld;
+        h->row_begin = row_begin;
+        h->owned = false;
+        h->has_b = true;
+        *out = h;
+    });
+}
+
+int slq_dense_set_rhs(slq_dense* A, const double* b) {
+    return guarded([&] {
+        need(A != nullptr, SLQ_INVALID_ARG, "null matrix");
+        slq_ctx* ctx = A->ctx;
+        slq::DevBuf tmp;
+        double* db = nullptr;
+        if (b) {
+            db = static_cast<double*>(tmp.ensure(sizeof(double) * std::max<int64_t>(1, A->m)));
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(db, b, sizeof(double) * A->m, cudaMemcpyHostToDevice, ctx->stream));
+        }
+        if (A->m > 0) {
+            set_column_kernel<<<static_cast<unsigned>(slq::ceil_div(A->m, 256)), 256, 0, ctx->stream>>>(A->A, A->m, A->ld,
+                                                                                                    A->n, db);
+            SLQ_LAUNCH_CHECK(ctx);
+        }
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        A->has_b = b != nullptr;
+    });
+}
+
+int slq_dense_free(slq_dense* A) {
+    return guarded([&] {
+        if (!A) return;
+        if (A->owned && A->A) {
+            cudaStreamSynchronize(A->ctx->stream);
+            cudaFree(A->A);
+        }
+        delete A;
+    });
+}
+
+int64_t slq_dense_ld(const slq_dense* A) { return A ? A->ld : 0; }
+
+int slq_sketch_apply(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed, int exact, double* Y,
+                     double* Sb) {
+    return guarded([&] {
+        need(ctx && A, SLQ_INVALID_ARG, "sketch_apply: null handle");
+        if (zeta > d || zeta < 1) slq::fail(SLQ_INVALID_SPARSITY, "apply: need 1 <= zeta <= d");
+        const int64_t n = A->n;
+        double* Yaug = static_cast<double*>(ctx->ws.yaug.ensure(sizeof(double) * d * (n + 1)));
+        slq::sketch_apply_dev(ctx, A, d, zeta, seed, exact != 0, Yaug);
+        slq::allreduce_sum(ctx, Yaug, d * (n + 1));  // distsim.hpp:383-396: every caller gets the total
+        if (Y) SLQ_CUDA_CHECK(cudaMemcpyAsync(Y, Yaug, sizeof(double) * d * n, cudaMemcpyDeviceToHost, ctx->stream));
+        if (Sb) SLQ_CUDA_CHECK(cudaMemcpyAsync(Sb, Yaug + d * n, sizeof(double) * d, cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int slq_spmm_csc_dense(slq_ctx* ctx, int64_t d, int64_t m, const int64_t* row_indices, const double* values,
+                       const int64_t* col_pointers, const double* A, int64_t n, int64_t lda, double* Y) {
+    return guarded([&] {
+        need(ctx && col_pointers && Y, SLQ_INVALID_ARG, "spmm: null argument");
+        need(lda >= m, SLQ_INVALID_DIMS, "spmm: lda < m");
+        const int64_t nnz = col_pointers[m];
+        need(col_pointers[0] == 0 && nnz >= 0, SLQ_INVALID_ARG, "spmm: bad col_pointers");
+        double val = 0.0;
+        for (int64_t e = 0; e < nnz; ++e) {
+            const double a = std::fabs(values[e]);
+            if (e == 0) val = a;
+            else if (a != val) slq::fail(SLQ_UNSUPPORTED, "spmm: device path needs +-v sketch values");
+            if (row_indices[e] < 0 || row_indices[e] >= d) slq::fail(SLQ_INVALID_ARG, "spmm: row index out of range");
+        }
+        slq_dense* Ad = nullptr;
+        int st = slq_dense_upload(ctx, A, m, n, lda, nullptr, 0, &Ad);
+        if (st != SLQ_OK) slq::fail(st, g_last_error);
+        struct Free {
+            slq_dense* p;
+            ~Free() { slq_dense_free(p); }
+        } fr{Ad};
+        slq::DevBuf drows, dvals, dcp, dcomp, dY;
+        int64_t* r = static_cast<int64_t*>(drows.ensure(sizeof(int64_t) * std::max<int64_t>(1, nnz)));
+        double* v = static_cast<double*>(dvals.ensure(sizeof(double) * std::max<int64_t>(1, nnz)));
+        int64_t* cp = static_cast<int64_t*>(dcp.ensure(sizeof(int64_t) * (m + 1)));
+        uint32_t* comp = static_cast<uint32_t*>(dcomp.ensure(sizeof(uint32_t) * std::max<int64_t>(1, nnz)));
+        double* Yd = static_cast<double*>(dY.ensure(sizeof(double) * d * (n + 1)));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(r, row_indices, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(v, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(cp, col_pointers, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, ctx->stream));
+        if (nnz > 0) {
+            csc_to_compact_kernel<<<static_cast<unsigned>(slq::ceil_div(nnz, 256)), 256, 0, ctx->stream>>>(r, v, nnz, comp);
+            SLQ_LAUNCH_CHECK(ctx);
+        }
+        int64_t zmax = 1;
+        for (int64_t j = 0; j < m; ++j) zmax = std::max(zmax, col_pointers[j + 1] - col_pointers[j]);
+        slq::sketch_apply_compact_dev(ctx, Ad, d, comp, cp, zmax, val, true, Yd);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(Y, Yd, sizeof(double) * d * n, cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int slq_householder_qr(slq_ctx* ctx, const double* Y, int64_t d, int64_t n, int64_t ldy, double* Q, double* R) {
+    return guarded([&] {
+        need(ctx && Y && R, SLQ_INVALID_ARG, "householder_qr: null argument");
+        if (d < n) slq::fail(SLQ_DIMENSION_MISMATCH, "householder_qr: need rows >= cols");
+        need(ldy >= d, SLQ_INVALID_DIMS, "householder_qr: ldy < d");
+        slq::DevBuf dY, dQ, dR;
+        double* y = static_cast<double*>(dY.ensure(sizeof(double) * std::max<int64_t>(1, d * n)));
+        SLQ_CUDA_CHECK(cudaMemcpy2DAsync(y, sizeof(double) * d, Y, sizeof(double) * ldy, sizeof(double) * d, n,
+                                         cudaMemcpyHostToDevice, ctx->stream));
+        double* r = static_cast<double*>(dR.ensure(sizeof(double) * std::max<int64_t>(1, n * n)));
+        double* q = Q ? static_cast<double*>(dQ.ensure(sizeof(double) * std::max<int64_t>(1, d * n))) : nullptr;
+        slq::qr_factor_dev(ctx, y, d, n, n, d, r, nullptr, q, nullptr);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(R, r, sizeof(double) * n * n, cudaMemcpyDeviceToHost, ctx->stream));
+        if (Q) SLQ_CUDA_CHECK(cudaMemcpyAsync(Q, q, sizeof(double) * d * n, cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int slq_tri_inverse(slq_ctx* ctx, const double* R, int64_t n, double* M) {
+    return guarded([&] {
+        need(ctx && R && M, SLQ_INVALID_ARG, "tri_inverse: null argument");
+        slq::DevBuf dR, dM;
+        double* r = static_cast<double*>(dR.ensure(sizeof(double) * std::max<int64_t>(1, n * n)));
+        double* mm = static_cast<double*>(dM.ensure(sizeof(double) * std::max<int64_t>(1, n * n)));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(r, R, sizeof(double) * n * n, cudaMemcpyHostToDevice, ctx->stream));
+        slq::tri_inverse_dev(ctx, r, n, mm, nullptr);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(M, mm, sizeof(double) * n * n, cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int slq_build_preconditioner(slq_ctx* ctx, const double* Y, int64_t d, int64_t n, int64_t ldy, const double* Sb,
+                             double* M, double* Q, double* x0, double* build_time) {
+    return guarded([&] {
+        need(ctx && Y && M, SLQ_INVALID_ARG, "build_preconditioner: null argument");
+        if (d < n) slq::fail(SLQ_DIMENSION_MISMATCH, "householder_qr: need rows >= cols");
+        need(ldy >= d, SLQ_INVALID_DIMS, "build_preconditioner: ldy < d");
+        const bool with_sb = Sb != nullptr;
+        double* Yaug = static_cast<double*>(ctx->ws.yaug.ensure(sizeof(double) * d * (n + 1)));
+        SLQ_CUDA_CHECK(cudaMemcpy2DAsync(Yaug, sizeof(double) * d, Y, sizeof(double) * ldy, sizeof(double) * d, n,
+                                         cudaMemcpyHostToDevice, ctx->stream));
+        if (with_sb)
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(Yaug + d * n, Sb, sizeof(double) * d, cudaMemcpyHostToDevice, ctx->stream));
+        slq::DevBuf dQ;
+        double* q = Q ? static_cast<double*>(dQ.ensure(sizeof(double) * std::max<int64_t>(1, d * n))) : nullptr;
+        PrecondBufs P = precond_bufs(ctx, n);
+        double t[3] = {0, 0, 0};
+        build_precond_dev(ctx, Yaug, d, n, with_sb, q, P, t);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(M, P.M, sizeof(double) * n * n, cudaMemcpyDeviceToHost, ctx->stream));
+        if (Q) SLQ_CUDA_CHECK(cudaMemcpyAsync(Q, q, sizeof(double) * d * n, cudaMemcpyDeviceToHost, ctx->stream));
+        if (x0 && with_sb) SLQ_CUDA_CHECK(cudaMemcpyAsync(x0, P.x0, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (build_time) *build_time = t[0] + t[1];
+    });
+}
+
+int slq_initial_guess(slq_ctx* ctx, const double* M, const double* Q, int64_t d, int64_t n, const double* Sb,
+                      double* x0) {
+    return guarded([&] {
+        need(ctx && M && Q && Sb && x0, SLQ_INVALID_ARG, "initial_guess: null argument");
+        slq::DevBuf dM, dQ, dv, dt;
+        double* mm = static_cast<double*>(dM.ensure(sizeof(double) * std::max<int64_t>(1, 2 * n * n)));
+        double* q = static_cast<double*>(dQ.ensure(sizeof(double) * std::max<int64_t>(1, d * n)));
+        double* v = static_cast<double*>(dv.ensure(sizeof(double) * std::max<int64_t>(1, d)));
+        double* t = static_cast<double*>(dt.ensure(sizeof(double) * std::max<int64_t>(1, 2 * n)));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(mm, M, sizeof(double) * n * n, cudaMemcpyHostToDevice, ctx->stream));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(q, Q, sizeof(double) * d * n, cudaMemcpyHostToDevice, ctx->stream));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(v, Sb, sizeof(double) * d, cudaMemcpyHostToDevice, ctx->stream));
+        if (n > 0) {
+            gemv_t_kernel<<<static_cast<unsigned>(slq::ceil_div(n * 32, 256)), 256, 0, ctx->stream>>>(q, d, n, v, t);
+            SLQ_LAUNCH_CHECK(ctx);
+            transpose_square(ctx, mm, n, mm + n * n);
+            slq::trmv_upper_dev(ctx, mm + n * n, n, t, t + n);
+        }
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(x0, t + n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int slq_tri_upper_matvec(slq_ctx* ctx, const double* R, int64_t n, const double* x, double* y, int trans) {
+    return guarded([&] {
+        need(ctx && R && x && y, SLQ_INVALID_ARG, "tri_upper_matvec: null argument");
+        slq::DevBuf dR, dv;
+        double* r = static_cast<double*>(dR.ensure(sizeof(double) * std::max<int64_t>(1, 2 * n * n)));
+        double* v = static_cast<double*>(dv.ensure(sizeof(double) * std::max<int64_t>(1, 2 * n)));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(r, R, sizeof(double) * n * n, cudaMemcpyHostToDevice, ctx->stream));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(v, x, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        if (n > 0) {
+            if (trans) {
+                slq::trmv_upper_trans_dev(ctx, r, n, v, v + n);
+            } else {
+                transpose_square(ctx, r, n, r + n * n);
+                slq::trmv_upper_dev(ctx, r + n * n, n, v, v + n);
+            }
+        }
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(y, v + n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int slq_lsqr(slq_ctx* ctx, const slq_dense* A, const double* M, const double* b, const double* x0,
+             const slq_solve_opts* opts_in, double* x_out, slq_report* report, double* residual_estimate,
+             double* iterates_error, double* residual_true) {
+    return guarded([&] {
+        need(ctx && A && M && x0 && x_out, SLQ_INVALID_ARG, "lsqr: null argument");
+        need(b != nullptr || A->has_b, SLQ_INVALID_ARG, "lsqr: no right-hand side");
+        slq_solve_opts opts;
+        if (opts_in) opts = *opts_in;
+        else slq_solve_opts_default(&opts);
+        const int64_t n = A->n, m = A->m;
+        PrecondBufs P = precond_bufs(ctx, n);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(P.M, M, sizeof(double) * n * n, cudaMemcpyHostToDevice, ctx->stream));
+        transpose_square(ctx, P.M, n, P.Mt);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(P.x0, x0, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        slq::DevBuf db, dx;
+        double* bd = nullptr;
+        if (b) {
+            bd = static_cast<double*>(db.ensure(sizeof(double) * std::max<int64_t>(1, m)));
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(bd, b, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream));
+        }
+        double* x = static_cast<double*>(dx.ensure(sizeof(double) * (n + 8)));
+        slq::LsqrOut lo;
+        const auto h0 = std::chrono::steady_clock::now();
+        slq::lsqr_dev(ctx, A, bd, P.M, P.Mt, P.x0, x, opts, residual_estimate, iterates_error, residual_true, lo);
+        SLQ_CUDA_CHECK(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        lo.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
+        fill_report(report, lo);
+    });
+}
+
+int slq_solve(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed, const slq_solve_opts* opts,
+              double* x_out, slq_report* report, slq_phase_times* times, double* residual_estimate) {
+    return run_solve(ctx, A, d, zeta, seed, opts, x_out, report, times, residual_estimate);
+}
+
+int slq_solve_host(slq_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
+                   int64_t row_begin, int64_t d, int64_t zeta, uint64_t seed, const slq_solve_opts* opts,
+                   double* x_out, slq_report* report, slq_phase_times* times, double* residual_estimate) {
+    slq_dense* Ad = nullptr;
+    int st = slq_dense_upload(ctx, A, m, n, lda, b, row_begin, &Ad);
+    if (st != SLQ_OK) return st;
+    st = run_solve(ctx, Ad, d, zeta, seed, opts, x_out, report, times, residual_estimate);
+    std::string keep = g_last_error;
+    slq_dense_free(Ad);
+    g_last_error = keep;
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,114 @@
+// common.cuh -- shared host/device plumbing for the sm_100a solver library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "slq_b200.h"
+
+namespace slq {
+
+// Exception carrying an slq_status; converted to a return code at the C-ABI.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& what) : std::runtime_error(what), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& what) { throw Error(code, what); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        std::string msg = std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                          std::to_string(line) + ")";
+        fail(e == cudaErrorMemoryAllocation ? SLQ_OOM : SLQ_CUDA, msg);
+    }
+}
+#define SLQ_CUDA_CHECK(x) ::slq::cuda_check((x), #x, __FILE__, __LINE__)
+#define SLQ_LAUNCH_CHECK(ctx)                                        \
+    do {                                                             \
+        ::slq::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
+        (ctx)->launches++;                                           \
+    } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// Device buffer with RAII; grow-only reuse via ensure().
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void* ensure(size_t b) {
+        if (b <= bytes && p) return p;
+        release();
+        if (b == 0) b = 16;
+        SLQ_CUDA_CHECK(cudaMalloc(&p, b));
+        bytes = b;
+        return p;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+// Per-context scratch, grow-only (sizes at C3 in DESIGN.md).
+struct Workspace {
+    DevBuf compact;      // sketch entries, u32 (row | neg << 31), column order
+    DevBuf chunk_ptr;    // per-chunk row pointers (u16)
+    DevBuf chunk_ent;    // per-chunk sorted entries (u16: k_local << 1 | neg)
+    DevBuf ypart;        // sketch partials [nsplit][ld][d]
+    DevBuf yaug;         // Y_aug = [S A | S b], d x (n+1) column-major
+    DevBuf flags;        // small device counters / error flags
+    DevBuf staging[2];   // upload staging
+    DevBuf qr_t, qr_w, qr_q, qr_misc;
+    DevBuf lsqr_vec, lsqr_part, lsqr_state, lsqr_u;
+    DevBuf mats;         // M, Mt
+    DevBuf tmp;
+};
+
+}  // namespace slq
+
+// Opaque handles of the C-ABI (defined here so every translation unit agrees).
+struct slq_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int num_sms = 148;
+    int64_t launches = 0;
+    slq::Workspace ws;
+    // multi-GPU (NCCL communicator stored as void* to keep nccl.h local to comm.cu)
+    void* comm = nullptr;
+    int rank = 0;
+    int nranks = 1;
+    int64_t nccl_calls = 0;
+};
+
+struct slq_dense {
+    slq_ctx* ctx = nullptr;
+    double* A = nullptr;  // row-major, element (i, j) at A[i*ld + j]; column n holds b
+    int64_t m = 0;        // rows of this block
+    int64_t n = 0;
+    int64_t ld = 0;
+    int64_t row_begin = 0;  // global id of row 0 (sketch column key)
+    bool owned = false;
+    bool has_b = false;
+};
+
+namespace slq {
+
+// Row stride of the device layout: [A | b | zero pad], 32-byte aligned rows.
+inline int64_t dense_ld(int64_t n) { return round_up(n + 1, 4); }
+
+}  // namespace slq

@@ -1,0 +1,769 @@
+// lsqr.cu -- K4/K5: preconditioned LSQR with one pass over A per iteration.
+//
+// Replaces lsqr.hpp:50-168 (detail::lsqr_impl) over the serial operator
+// (operators.hpp:15-51) and the row-partitioned DistOperator
+// (distsim.hpp:413-450), using the one-sync algebra of lsqr.hpp:120-127:
+//
+//   K4 fused_pass  : one HBM pass over A per iteration.  Each row tile of A
+//                    (TMA bulk copy into a 3-stage smem ring, mbarrier
+//                    full/empty pipeline, one producer warp) is used twice
+//                    from shared memory: u_hat_i = A_i p + c u_i (warp dot +
+//                    shuffle reduce), then z += A_i^T u_hat_i (register
+//                    accumulators), plus ||u_hat||^2.  u is never rescaled
+//                    in memory: u_true = su * u_hat is carried as a scalar
+//                    and folded into the next pass's coefficient c.
+//   reduce         : per-CTA partials -> [A^T u_hat | ||u_hat||^2] (fixed order);
+//                    multi-GPU: ONE ncclAllReduce of n+1 doubles here.
+//   mtz            : v_hat = M^T z - beta v (warp per column of M), ||v_hat||^2,
+//                    and in its last CTA the whole scalar recurrence (Givens
+//                    rotation, breakdown tests, stopping rule lsqr.hpp:163).
+//   mv_update      : v = v_hat / alpha, p = M v (warp per row of M^T), x += (phi/rho) w,
+//                    w = p - (theta/rho) w.  p is the next pass's M v, so M v is
+//                    applied once per iteration (the reference applies it twice,
+//                    lsqr.hpp:115 and :156).
+// The iteration is captured in a CUDA graph (8 iterations per launch); a
+// device-side done flag turns the tail of the last graph into no-ops.
+#include <cmath>
+#include <vector>
+
+#include "lsqr.cuh"
+
+namespace slq {
+
+namespace {
+
+enum Mode : int { kModeSkip = 0, kModeInit = 1, kModeIter = 2, kModeFinal = 3 };
+
+struct LsqrState {
+    double alpha, rho_bar, phi_bar, beta1;
+    double c_next;   // coefficient of the next fused pass
+    double coef_x;   // phi / rho
+    double coef_w;   // -theta / rho
+    double eps;
+    int64_t t;       // current iteration (1-based); 0 during init
+    int64_t maxit;
+    int64_t iters;
+    int done;
+    int term;
+    int mode;
+    int pad;
+    unsigned counter_mtz;
+    unsigned counter_mv;
+};
+
+// ------------------------------------------------------------ PTX helpers
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned a = smem_u32(bar);
+    unsigned ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// --------------------------------------------------------------- K4 pass
+
+constexpr int kConsumerWarps = 7;  // + 1 producer warp = 256 threads (255-register budget)
+constexpr int kPassThreads = (kConsumerWarps + 1) * 32;
+
+struct PassArgs {
+    const double* A;
+    int64_t ld, m, n;
+    const double* p;       // n
+    const double* u_in;    // m, or nullptr -> column n of A (b)
+    double* u_out;         // m, or nullptr
+    const double* coef;    // device scalar c, or nullptr -> c_fixed
+    double c_fixed;
+    double* part;          // [grid][n+1]
+    int want_z;
+    const int* skip;       // nonzero -> no-op
+    int R, S;              // rows per tile, stages
+};
+
+template <int NP, bool P_SMEM>
+__global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (a.skip && *a.skip) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t ld = a.ld;
+    const size_t stage_elems = static_cast<size_t>(a.R) * ld;
+    double* stages = reinterpret_cast<double*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.S * stage_elems * sizeof(double));
+    uint64_t* empty = full + a.S;
+    double* p_s = reinterpret_cast<double*>(empty + a.S);  // [ld] when P_SMEM
+
+    const int64_t ntiles = (a.m + a.R - 1) / a.R;
+    const int64_t t0 = blockIdx.x * ntiles / gridDim.x;
+    const int64_t t1 = (blockIdx.x + 1) * ntiles / gridDim.x;
+    const int64_t nt = t1 - t0;
+
+    if (tid == 0) {
+        for (int s = 0; s < a.S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (P_SMEM)
+        for (int64_t j = tid; j < ld; j += kPassThreads) p_s[j] = (j < a.n) ? a.p[j] : 0.0;
+    __syncthreads();
+
+    double z[2 * NP];
+#pragma unroll
+    for (int q = 0; q < 2 * NP; ++q) z[q] = 0.0;
+    double ssq = 0.0;
+    if (warp == kConsumerWarps) {
+        // ---------------- producer: one elected lane streams row tiles
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            for (int64_t k = 0; k < nt; ++k) {
+                const int s = static_cast<int>(k % a.S);
+                const int64_t r = k / a.S;
+                if (r > 0) mbar_wait(&empty[s], static_cast<unsigned>((r - 1) & 1));
+                const int64_t row0 = (t0 + k) * a.R;
+                const int64_t rows = min(static_cast<int64_t>(a.R), a.m - row0);
+                const unsigned bytes = static_cast<unsigned>(rows * ld * sizeof(double));
+                mbar_expect_tx(&full[s], bytes);
+                bulk_g2s(stages + s * stage_elems, a.A + row0 * ld, bytes, &full[s], pol);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- consumers
+        double pr[P_SMEM ? 1 : 2 * NP];
+        if (!P_SMEM) {
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                const int64_t j = 2 * lane + 64 * q;
+                pr[2 * q] = (j < a.n) ? a.p[j] : 0.0;
+                pr[2 * q + 1] = (j + 1 < a.n) ? a.p[j + 1] : 0.0;
+            }
+        }
+        const double c = a.coef ? *a.coef : a.c_fixed;
+        for (int64_t k = 0; k < nt; ++k) {
+            const int s = static_cast<int>(k % a.S);
+            mbar_wait(&full[s], static_cast<unsigned>((k / a.S) & 1));
+            const double* tile = stages + s * stage_elems;
+            const int64_t row0 = (t0 + k) * a.R;
+            const int rows = static_cast<int>(min(static_cast<int64_t>(a.R), a.m - row0));
+            // rows of this tile owned by this warp: (k*R + i) % 8 == warp
+            int i = static_cast<int>(((warp - (k * a.R) % kConsumerWarps) + kConsumerWarps) % kConsumerWarps);
+            for (; i < rows; i += kConsumerWarps) {
+                const double* row = tile + static_cast<int64_t>(i) * ld;
+                const double u = a.u_in ? a.u_in[row0 + i] : row[a.n];
+                double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+                for (int q = 0; q < NP; ++q) {
+                    const int64_t j = 2 * lane + 64 * q;
+                    if (j < ld) {
+                        const double2 v = *reinterpret_cast<const double2*>(row + j);
+                        const double p0 = P_SMEM ? p_s[j] : pr[2 * q];
+                        const double p1 = P_SMEM ? p_s[j + 1] : pr[2 * q + 1];
+                        acc0 = fma(v.x, p0, acc0);
+                        acc1 = fma(v.y, p1, acc1);
+                    }
+                }
+                const double y = warp_sum(acc0 + acc1);
+                const double uh = __dadd_rn(y, __dmul_rn(c, u));
+                if (lane == 0 && a.u_out) a.u_out[row0 + i] = uh;
+                ssq = fma(uh, uh, ssq);
+                if (a.want_z) {
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) {
+                        const int64_t j = 2 * lane + 64 * q;
+                        if (j < ld) {
+                            const double2 v = *reinterpret_cast<const double2*>(row + j);
+                            z[2 * q] = fma(v.x, uh, z[2 * q]);
+                            z[2 * q + 1] = fma(v.y, uh, z[2 * q + 1]);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+    }
+    // park accumulators for the block reduction: stage memory is free once
+    // every tile has been consumed
+    __syncthreads();
+    if (warp < kConsumerWarps) {
+        double* red = stages;  // [8][ld] + [8] ssq
+        if (a.want_z) {
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                const int64_t j = 2 * lane + 64 * q;
+                if (j < ld) {
+                    red[warp * ld + j] = z[2 * q];
+                    red[warp * ld + j + 1] = z[2 * q + 1];
+                }
+            }
+        }
+        if (lane == 0) red[kConsumerWarps * ld + warp] = ssq;
+    }
+    __syncthreads();
+    double* red = stages;
+    double* outp = a.part + static_cast<int64_t>(blockIdx.x) * (a.n + 1);
+    if (a.want_z) {
+        for (int64_t j = tid; j < a.n; j += kPassThreads) {
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < kConsumerWarps; ++w) s += red[w * ld + j];
+            outp[j] = s;
+        }
+    }
+    if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kConsumerWarps; ++w) s += red[kConsumerWarps * ld + w];
+        outp[a.n] = s;
+    }
+}
+
+// partials [G][n+1] -> out[n+1], fixed order
+__global__ void reduce_partials_kernel(const double* part, int G, int64_t n1, double* out, const int* skip) {
+    if (skip && *skip) return;
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n1) return;
+    double s = 0.0;
+    for (int g = 0; g < G; ++g) s += part[static_cast<int64_t>(g) * n1 + j];
+    out[j] = s;
+}
+
+// --------------------------------------------------------------- K5 mtz
+
+struct MtzArgs {
+    const double* M;   // column-major n x n upper
+    int64_t n;
+    const double* zt;  // [n+1]: A^T u_hat | ||u_hat||^2
+    const double* v;
+    double* vhat;
+    double* part2;     // [gridDim]
+    LsqrState* st;
+    double* est_hist;
+    int init;
+};
+
+__device__ void scalar_step(const MtzArgs& a, double beta, double alpha_next) {
+    LsqrState& st = *a.st;
+    if (a.init) {
+        st.beta1 = beta;
+        st.t = 1;
+        if (beta == 0.0 || alpha_next == 0.0) {
+            // lsqr.hpp:73-76 / :86-89: x0 already optimal
+            st.done = 1;
+            st.term = SLQ_TERM_TOLERANCE;
+            st.iters = 0;
+            st.mode = kModeSkip;
+            return;
+        }
+        st.alpha = alpha_next;
+        st.rho_bar = alpha_next;
+        st.phi_bar = beta;
+        st.c_next = -alpha_next * (-1.0 / beta);
+        st.mode = kModeInit;
+        if (st.maxit <= 0) {
+            st.done = 1;
+            st.term = SLQ_TERM_MAXITER;
+            st.iters = 0;
+        }
+        return;
+    }
+    const int64_t t = st.t;
+    auto final_rotation = [&](double beta_term) {  // lsqr.hpp:101-111
+        const double rho = hypot(st.rho_bar, beta_term);
+        const double c = st.rho_bar / rho;
+        const double s = beta_term / rho;
+        const double phi = c * st.phi_bar;
+        st.phi_bar = s * st.phi_bar;
+        st.coef_x = phi / rho;
+        a.est_hist[t - 1] = st.phi_bar;
+        st.done = 1;
+        st.term = SLQ_TERM_BREAKDOWN;
+        st.iters = t;
+        st.mode = kModeFinal;
+    };
+    if (beta < 1e-300) {
+        final_rotation(0.0);
+        return;
+    }
+    if (alpha_next < 1e-300) {
+        final_rotation(beta);
+        return;
+    }
+    // lsqr.hpp:147-153
+    const double rho = hypot(st.rho_bar, beta);
+    const double c = st.rho_bar / rho;
+    const double s = beta / rho;
+    const double theta = s * alpha_next;
+    st.rho_bar = -c * alpha_next;
+    const double phi = c * st.phi_bar;
+    st.phi_bar = s * st.phi_bar;
+    st.coef_x = phi / rho;
+    st.coef_w = -theta / rho;
+    st.alpha = alpha_next;
+    st.c_next = -alpha_next * (1.0 / beta);
+    a.est_hist[t - 1] = st.phi_bar;
+    st.mode = kModeIter;
+    if (st.phi_bar <= st.eps * st.beta1) {  // lsqr.hpp:163
+        st.done = 1;
+        st.term = SLQ_TERM_TOLERANCE;
+        st.iters = t;
+    } else if (t >= st.maxit) {
+        st.done = 1;
+        st.term = SLQ_TERM_MAXITER;
+        st.iters = st.maxit;
+    }
+    st.t = t + 1;
+}
+
+__global__ void __launch_bounds__(256) mtz_kernel(MtzArgs a) {
+    __shared__ double wsum[8];
+    __shared__ bool last;
+    if (a.st->done) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    const double beta = sqrt(a.zt[a.n]);
+    const double zs = a.init ? (-1.0 / beta) : (1.0 / beta);
+    double vh = 0.0;
+    if (j < a.n) {
+        const double* col = a.M + j * a.n;
+        double s = 0.0;
+        for (int64_t i = lane; i <= j; i += 32) s = fma(col[i], a.zt[i] * zs, s);
+        s = warp_sum(s);
+        vh = a.init ? s : __dadd_rn(s, __dmul_rn(-beta, a.v[j]));  // lsqr.hpp:137
+        if (lane == 0) a.vhat[j] = vh;
+    }
+    if (lane == 0) wsum[warp] = vh * vh;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += wsum[w];
+        a.part2[blockIdx.x] = s;
+        __threadfence();
+        last = atomicAdd(&a.st->counter_mtz, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double s = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) s += static_cast<volatile double*>(a.part2)[b];
+        a.st->counter_mtz = 0;
+        scalar_step(a, beta, sqrt(s));
+    }
+}
+
+// --------------------------------------------------------- K5 mv_update
+
+struct MvArgs {
+    const double* Mt;  // row-major copy of M
+    int64_t n;
+    const double* vhat;
+    double* v;
+    double* p;
+    double* w;
+    double* x;
+    LsqrState* st;
+};
+
+__global__ void __launch_bounds__(256) mv_update_kernel(MvArgs a) {
+    __shared__ bool last;
+    const int mode = a.st->mode;
+    if (mode == kModeSkip) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    if (i < a.n) {
+        if (mode == kModeFinal) {
+            if (lane == 0) a.x[i] = __dadd_rn(a.x[i], __dmul_rn(a.st->coef_x, a.w[i]));
+        } else {
+            const double inv_alpha = 1.0 / a.st->alpha;  // lsqr.hpp:141 scal(1/alpha, v_hat)
+            const double* row = a.Mt + i * a.n;
+            double s = 0.0;
+            for (int64_t j = i + lane; j < a.n; j += 32) s = fma(row[j], a.vhat[j] * inv_alpha, s);
+            s = warp_sum(s);
+            if (lane == 0) {
+                a.v[i] = a.vhat[i] * inv_alpha;
+                a.p[i] = s;
+                if (mode == kModeInit) {
+                    a.w[i] = s;  // lsqr.hpp:92
+                } else {
+                    const double wi = a.w[i];
+                    a.x[i] = __dadd_rn(a.x[i], __dmul_rn(a.st->coef_x, wi));  // lsqr.hpp:155
+                    a.w[i] = __dadd_rn(s, __dmul_rn(a.st->coef_w, wi));       // lsqr.hpp:156-158
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&a.st->counter_mv, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        a.st->counter_mv = 0;
+        if (a.st->done) a.st->mode = kModeSkip;
+    }
+}
+
+__global__ void sum_strided_kernel(const double* p, int G, int64_t stride, double* out) {
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int g = 0; g < G; ++g) s += p[g * stride];
+        *out = s;
+    }
+}
+
+// ||q||^2 partial helpers for instrumentation
+__global__ void sub_kernel(const double* a, const double* b, double* out, int64_t n) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = a[i] + (-1.0) * b[i];  // axpy(-1, x, diff), lsqr.hpp:30
+}
+
+__global__ void sqrt_to_kernel(const double* ssq, double* out) {
+    if (threadIdx.x == 0) *out = sqrt(*ssq);
+}
+
+__global__ void norm_scaled_kernel(const double* u, int64_t m, const double* scale_src, int which,
+                                   double* out_ssq) {
+    // single-block ||u * s||^2 (debug hook only)
+    __shared__ double red[32];
+    const double s = (which == 0) ? 1.0 / sqrt(scale_src[0]) : 1.0;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const double v = u[i] * s;
+        acc += v * v;
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+        *out_ssq = t;
+    }
+}
+
+// ---------------------------------------------------------------- host
+
+struct PassPlan {
+    int NP;
+    bool p_smem;
+    int R, S;
+    size_t smem;
+    int grid;
+};
+
+PassPlan plan_pass(slq_ctx* ctx, const slq_dense* A) {
+    PassPlan pp{};
+    const int64_t ld = A->ld;
+    if (ld > 2048) fail(SLQ_UNSUPPORTED, "lsqr: n > 2046 not supported by the fused pass");
+    pp.NP = 1;
+    while (64 * pp.NP < ld) pp.NP <<= 1;
+    pp.p_smem = pp.NP >= 32;
+    const int64_t row_bytes = ld * static_cast<int64_t>(sizeof(double));
+    int64_t R = (64 * 1024) / row_bytes;
+    if (R >= 8) R = (R / 8) * 8;
+    R = std::max<int64_t>(1, std::min<int64_t>(R, 256));
+    pp.R = static_cast<int>(R);
+    pp.S = 3;
+    while (pp.S * pp.R < kConsumerWarps + 1) ++pp.S;  // reduction area needs >= 9 rows
+    pp.smem = static_cast<size_t>(pp.S) * pp.R * row_bytes + 2 * pp.S * sizeof(uint64_t) +
+              (pp.p_smem ? row_bytes : 0) + 64;
+    while (pp.smem > 227 * 1024 && pp.S > 2) {
+        --pp.S;
+        pp.smem -= pp.R * row_bytes + 2 * sizeof(uint64_t);
+    }
+    const int64_t ntiles = ceil_div(std::max<int64_t>(A->m, 1), pp.R);
+    pp.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, ntiles)));
+    return pp;
+}
+
+template <int NP, bool PS>
+void launch_pass_t(slq_ctx* ctx, const PassPlan& pp, const PassArgs& a) {
+    auto k = fused_pass_kernel<NP, PS>;
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pp.smem)));
+    k<<<pp.grid, kPassThreads, pp.smem, ctx->stream>>>(a);
+    SLQ_LAUNCH_CHECK(ctx);
+}
+
+void launch_pass(slq_ctx* ctx, const PassPlan& pp, PassArgs a) {
+    a.R = pp.R;
+    a.S = pp.S;
+    switch (pp.NP) {
+        case 1: launch_pass_t<1, false>(ctx, pp, a); break;
+        case 2: launch_pass_t<2, false>(ctx, pp, a); break;
+        case 4: launch_pass_t<4, false>(ctx, pp, a); break;
+        case 8: launch_pass_t<8, false>(ctx, pp, a); break;
+        case 16: launch_pass_t<16, false>(ctx, pp, a); break;
+        default: launch_pass_t<32, true>(ctx, pp, a); break;
+    }
+}
+
+struct LsqrBufs {
+    double *u, *p, *v, *vhat, *w, *zt, *part, *part2, *hist, *tmp_n, *scal;
+    LsqrState* st;
+};
+
+}  // namespace
+
+void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const double* M, const double* Mt,
+              const double* x0, double* x, const slq_solve_opts& opts, double* est_hist,
+              double* err_hist, double* true_hist, LsqrOut& out) {
+    const int64_t m = A->m, n = A->n;
+    const int64_t maxit = std::max<int64_t>(0, opts.maxit);
+    Workspace& ws = ctx->ws;
+    PassPlan pp = plan_pass(ctx, A);
+    const int mtz_grid = static_cast<int>(std::max<int64_t>(1, ceil_div(n, 8)));
+
+    // workspace layout
+    const size_t nvec = static_cast<size_t>(n + 8);
+    double* vecs = static_cast<double*>(ws.lsqr_vec.ensure(sizeof(double) * (nvec * 6 + mtz_grid + maxit + 8 + 16)));
+    LsqrBufs B{};
+    B.p = vecs;
+    B.v = vecs + nvec;
+    B.vhat = vecs + 2 * nvec;
+    B.w = vecs + 3 * nvec;
+    B.zt = vecs + 4 * nvec;  // n+1
+    B.tmp_n = vecs + 5 * nvec;
+    B.part2 = vecs + 6 * nvec;
+    B.hist = B.part2 + mtz_grid;
+    B.scal = B.hist + maxit + 8;
+    B.part = static_cast<double*>(ws.lsqr_part.ensure(sizeof(double) * pp.grid * (n + 1)));
+    B.st = static_cast<LsqrState*>(ws.lsqr_state.ensure(sizeof(LsqrState)));
+    B.u = static_cast<double*>(ws.lsqr_u.ensure(sizeof(double) * std::max<int64_t>(1, m)));
+
+    LsqrState h{};
+    h.eps = opts.eps;
+    h.maxit = maxit;
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(B.st, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    const int* done_flag = &B.st->done;
+
+    cudaEvent_t e0, e1;
+    SLQ_CUDA_CHECK(cudaEventCreate(&e0));
+    SLQ_CUDA_CHECK(cudaEventCreate(&e1));
+    SLQ_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+
+    const bool instrument = opts.x_star || opts.track_true_residual || opts.on_bidiag;
+    std::vector<double> herr, htrue;
+    double* d_xstar = nullptr;
+    DevBuf xsbuf;
+    if (opts.x_star) {
+        d_xstar = static_cast<double*>(xsbuf.ensure(sizeof(double) * n));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(d_xstar, opts.x_star, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    // ||A q + c b||  (instrumentation; not counted, lsqr.hpp:26-37)
+    auto norm_pass = [&](const double* q, double c, double* dst) {
+        PassArgs na{A->A, A->ld, m, n, q, b_dev, nullptr, nullptr, c, B.part, 0, nullptr, 0, 0};
+        launch_pass(ctx, pp, na);
+        sum_strided_kernel<<<1, 32, 0, ctx->stream>>>(B.part + n, pp.grid, n + 1, B.scal);
+        SLQ_LAUNCH_CHECK(ctx);
+        allreduce_sum(ctx, B.scal, 1);
+        sqrt_to_kernel<<<1, 32, 0, ctx->stream>>>(B.scal, dst);
+        SLQ_LAUNCH_CHECK(ctx);
+    };
+    auto record = [&]() {
+        if (opts.x_star) {
+            sub_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, ctx->stream>>>(d_xstar, x, B.tmp_n, n);
+            SLQ_LAUNCH_CHECK(ctx);
+            norm_pass(B.tmp_n, 0.0, B.scal + 2);
+            double v;
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(&v, B.scal + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+            SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            herr.push_back(v);
+        }
+        if (opts.track_true_residual) {
+            norm_pass(x, -1.0, B.scal + 3);
+            double v;
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(&v, B.scal + 3, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+            SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            htrue.push_back(v);
+        }
+    };
+
+    // ---- init: u_hat = A x0 - b, z = A^T u_hat, ||u_hat||^2 (one pass)
+    int64_t allreduces = 0;
+    {
+        PassArgs ia{A->A, A->ld, m, n, x0, b_dev, B.u, nullptr, -1.0, B.part, 1, nullptr, 0, 0};
+        launch_pass(ctx, pp, ia);
+        reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 256)), 256, 0, ctx->stream>>>(
+            B.part, pp.grid, n + 1, B.zt, nullptr);
+        SLQ_LAUNCH_CHECK(ctx);
+        allreduce_sum(ctx, B.zt, n + 1);
+        if (ctx->comm) ++allreduces;
+        if (instrument) record();
+        MtzArgs ma{M, n, B.zt, B.v, B.vhat, B.part2, B.st, B.hist, 1};
+        mtz_kernel<<<mtz_grid, 256, 0, ctx->stream>>>(ma);
+        SLQ_LAUNCH_CHECK(ctx);
+        MvArgs va{Mt, n, B.vhat, B.v, B.p, B.w, x, B.st};
+        mv_update_kernel<<<mtz_grid, 256, 0, ctx->stream>>>(va);
+        SLQ_LAUNCH_CHECK(ctx);
+    }
+    const int64_t init_allreduces = allreduces;
+
+    auto enqueue_iteration = [&]() {
+        PassArgs ta{A->A, A->ld, m, n, B.p, B.u, B.u, &B.st->c_next, 0.0, B.part, 1, done_flag, 0, 0};
+        launch_pass(ctx, pp, ta);
+        reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 256)), 256, 0, ctx->stream>>>(
+            B.part, pp.grid, n + 1, B.zt, done_flag);
+        SLQ_LAUNCH_CHECK(ctx);
+        allreduce_sum(ctx, B.zt, n + 1);
+        MtzArgs ma{M, n, B.zt, B.v, B.vhat, B.part2, B.st, B.hist, 0};
+        mtz_kernel<<<mtz_grid, 256, 0, ctx->stream>>>(ma);
+        SLQ_LAUNCH_CHECK(ctx);
+        MvArgs va{Mt, n, B.vhat, B.v, B.p, B.w, x, B.st};
+        mv_update_kernel<<<mtz_grid, 256, 0, ctx->stream>>>(va);
+        SLQ_LAUNCH_CHECK(ctx);
+    };
+
+    LsqrState hs{};
+    if (instrument) {
+        for (int64_t t = 1; t <= maxit; ++t) {
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, B.st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+            SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            if (hs.done) break;
+            enqueue_iteration();
+            if (ctx->comm) ++allreduces;
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, B.st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+            SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            if (opts.on_bidiag && hs.mode != kModeFinal) {
+                // recomputed norms of u_{t+1} = u_hat / beta and v_{t+1}
+                norm_scaled_kernel<<<1, 1024, 0, ctx->stream>>>(B.u, m, B.zt + n, 0, B.scal + 4);
+                norm_scaled_kernel<<<1, 1024, 0, ctx->stream>>>(B.v, n, nullptr, 1, B.scal + 5);
+                ctx->launches += 2;
+                allreduce_sum(ctx, B.scal + 4, 1);
+                double nn[2];
+                SLQ_CUDA_CHECK(cudaMemcpyAsync(nn, B.scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+                SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+                opts.on_bidiag(opts.on_bidiag_user, t, std::sqrt(nn[0]), std::sqrt(nn[1]));
+            }
+            // the mv_update of this iteration has run: x_t is current
+            if (opts.x_star || opts.track_true_residual) record();
+        }
+    } else if (maxit > 0) {
+        constexpr int kBatch = 8;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        const bool use_graph = ctx->stream != nullptr;
+        if (use_graph) {
+            SLQ_CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+            for (int b = 0; b < kBatch; ++b) enqueue_iteration();
+            SLQ_CUDA_CHECK(cudaStreamEndCapture(ctx->stream, &graph));
+            SLQ_CUDA_CHECK(cudaGraphInstantiate(&exec, graph, 0));
+        }
+        int* hdone = nullptr;
+        SLQ_CUDA_CHECK(cudaMallocHost(&hdone, 2 * sizeof(int)));
+        hdone[0] = hdone[1] = 0;
+        cudaEvent_t ev[2];
+        SLQ_CUDA_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+        SLQ_CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+        int64_t launched = 0;
+        int64_t k = 0;
+        while (launched < maxit) {
+            if (use_graph) {
+                SLQ_CUDA_CHECK(cudaGraphLaunch(exec, ctx->stream));
+                ctx->launches += 4 * kBatch;
+            } else {
+                for (int b = 0; b < kBatch; ++b) enqueue_iteration();
+            }
+            launched += kBatch;
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(&hdone[k & 1], done_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+            SLQ_CUDA_CHECK(cudaEventRecord(ev[k & 1], ctx->stream));
+            if (k > 0) {
+                SLQ_CUDA_CHECK(cudaEventSynchronize(ev[(k - 1) & 1]));
+                if (hdone[(k - 1) & 1]) break;
+            }
+            ++k;
+        }
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+        cudaFreeHost(hdone);
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+    }
+    SLQ_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, B.st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    float ms = 0.f;
+    SLQ_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+
+    out.iterations = hs.iters;
+    out.termination = hs.term;
+    out.n_estimate = hs.iters;
+    if (hs.term == SLQ_TERM_TOLERANCE && hs.iters == 0) out.n_estimate = 0;
+    if (est_hist && out.n_estimate > 0)
+        SLQ_CUDA_CHECK(cudaMemcpy(est_hist, B.hist, sizeof(double) * out.n_estimate, cudaMemcpyDeviceToHost));
+    if (ctx->comm) allreduces = init_allreduces + (instrument ? allreduces - init_allreduces : hs.iters);
+    out.allreduces = allreduces;
+    out.init_allreduces = init_allreduces;
+    out.seconds = ms * 1e-3;
+    out.n_err = static_cast<int64_t>(herr.size());
+    out.n_true = static_cast<int64_t>(htrue.size());
+    if (err_hist)
+        for (size_t i = 0; i < herr.size(); ++i) err_hist[i] = herr[i];
+    if (true_hist)
+        for (size_t i = 0; i < htrue.size(); ++i) true_hist[i] = htrue[i];
+}
+
+double backward_error_dev(slq_ctx* ctx, const slq_dense* A, const double* x, double a_norm) {
+    // r = b - A x:  u_hat = A x - b = -r;  z = A^T u_hat = -A^T r
+    PassPlan pp = plan_pass(ctx, A);
+    const int64_t n = A->n;
+    DevBuf part, zt;
+    double* dpart = static_cast<double*>(part.ensure(sizeof(double) * pp.grid * (n + 1)));
+    double* dzt = static_cast<double*>(zt.ensure(sizeof(double) * (n + 1)));
+    PassArgs a{A->A, A->ld, A->m, n, x, nullptr, nullptr, nullptr, -1.0, dpart, 1, nullptr, 0, 0};
+    launch_pass(ctx, pp, a);
+    reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 256)), 256, 0, ctx->stream>>>(dpart, pp.grid, n + 1,
+                                                                                              dzt, nullptr);
+    SLQ_LAUNCH_CHECK(ctx);
+    allreduce_sum(ctx, dzt, n + 1);
+    std::vector<double> h(n + 1);
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(h.data(), dzt, sizeof(double) * (n + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    double atr = 0.0;
+    for (int64_t j = 0; j < n; ++j) atr += h[j] * h[j];
+    const double rn = std::sqrt(h[n]);
+    if (rn == 0.0) return 0.0;
+    return std::sqrt(atr) / (a_norm * rn);
+}
+
+}  // namespace slq

@@ -1,0 +1,41 @@
+// lsqr.cuh -- host side of the K4/K5 LSQR kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace slq {
+
+// Preconditioned LSQR (lsqr.hpp:50-168) on device-resident data.
+//   A   : this rank's row block (device layout, b in column n unless b_dev given)
+//   M   : n x n upper, column-major (device);  Mt: its row-major copy (device)
+//   x0  : device n-vector (initial guess);   x: device n-vector (output)
+// Histories (host, optional) as in the C-ABI.  With a communicator on ctx the
+// partial A^T u / ||u||^2 of every iteration is summed by one ncclAllReduce.
+struct LsqrOut {
+    int64_t iterations = 0;
+    int termination = SLQ_TERM_MAXITER;
+    int64_t n_estimate = 0, n_err = 0, n_true = 0;
+    int64_t allreduces = 0, init_allreduces = 0;
+    double seconds = 0.0;
+    double backward_error = -1.0;
+};
+
+void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const double* M, const double* Mt,
+              const double* x0, double* x, const slq_solve_opts& opts, double* est_hist,
+              double* err_hist, double* true_hist, LsqrOut& out);
+
+// ||A^T r|| / (a_norm ||r||) for r = b - A x (one fused pass + allreduce).
+double backward_error_dev(slq_ctx* ctx, const slq_dense* A, const double* x, double a_norm);
+
+// comm.cu: in-place sum across ranks (no-op without a communicator).
+void allreduce_sum(slq_ctx* ctx, double* buf, int64_t count);
+void reduce_sum_root(slq_ctx* ctx, double* buf, int64_t count);
+void broadcast_root(slq_ctx* ctx, double* buf, int64_t count);
+
+}  // namespace slq
+
+namespace slq {
+void comm_unique_id(unsigned char out[128]);
+void comm_init(slq_ctx* ctx, const unsigned char id[128], int rank, int nranks);
+void comm_destroy(slq_ctx* ctx);
+}  // namespace slq

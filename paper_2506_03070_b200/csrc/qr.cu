@@ -1,0 +1,526 @@
+// qr.cu -- K3: blocked Householder QR of the sketch, R^-1, x0 (sm_100a).
+//
+// Replaces qr.hpp:21-89 (householder_qr), triangular.hpp:14-33 (tri_inverse),
+// preconditioner.hpp:35-53 (build_preconditioner, initial_guess).
+//
+// Same reflector convention as the reference: beta = -sign(x0) ||x||,
+// tau = (beta - x0) / beta, v scaled by 1 / (x0 - beta) with an implicit unit
+// leading entry, rank test ||x|| < 1e-12 max|Y| (qr.hpp:26, :39-47), and the
+// final diag(R) >= 0 sign flip (qr.hpp:79-86).  Blocked (LAPACK dgeqrf
+// style) for the GPU:
+//   * panel of nb <= 32 columns factored by ONE thread-block cluster (1..16
+//     CTAs) holding the panel rows in shared memory; the two column
+//     reductions per reflector go through DSMEM (fixed order, deterministic);
+//     the same reduction also yields V^T v_k, so the compact-WY factor T
+//     (H_0..H_{nb-1} = I - V T V^T) comes for free;
+//   * trailing update C <- C - V T^T (V^T C) on FP64 tensor cores
+//     (mma.sync m8n8k4 f64 = SASS DMMA); C includes the appended column Sb,
+//     so Q^T Sb (for x0) is produced without forming Q.
+// Q itself is formed only when the caller asks for it (back-to-front
+// application of the stored panels to [I; 0], as qr.hpp:64-77).
+#include <cooperative_groups.h>
+
+#include <chrono>
+#include <cmath>
+
+#include "common.cuh"
+#include "qr.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace slq {
+
+namespace {
+
+constexpr int kPanelThreads = 256;
+constexpr int kNbMax = 32;
+constexpr int kWs = kNbMax + 1;  // padded row stride of the panel slice (bank-conflict free columns)
+
+// max |Y| over a d x n column-major block (qr.hpp:26).  Two-level, deterministic.
+__global__ void maxabs_kernel(const double* Y, int64_t d, int64_t n, int64_t ldy, double* part) {
+    __shared__ double red[32];
+    double mx = 0.0;
+    const int64_t tot = d * n;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < tot;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = e / d, i = e - j * d;
+        mx = fmax(mx, fabs(Y[j * ldy + i]));
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+        part[blockIdx.x] = fmax(mx, red[0]);
+    }
+}
+
+__global__ void maxabs_final_kernel(const double* part, int np, double* rank_tol) {
+    if (threadIdx.x == 0) {
+        double mx = 0.0;
+        for (int i = 0; i < np; ++i) mx = fmax(mx, part[i]);
+        *rank_tol = 1e-12 * mx;
+    }
+}
+
+struct PanelArgs {
+    double* Y;
+    int64_t ldy, d;
+    int64_t k0;        // first column == first row of the panel
+    int kb;            // panel width
+    int64_t rpc;       // rows per CTA
+    const double* rank_tol;
+    double* tau;       // global tau[n]
+    double* T;         // kb x kb (ld kNbMax) compact-WY factor of this panel
+    int* err;          // 0 or 1 + failing column
+};
+
+// Cluster-wide sum of L <= 33 doubles.  Each CTA writes its partial into
+// slot[parity]; after cluster.sync every CTA sums all ranks in rank order.
+// A slot is rewritten two reductions later, after another cluster.sync,
+// so no CTA can still be reading it.
+__device__ __forceinline__ void cluster_sum(cg::cluster_group& cl, double (*slot)[40], int parity, int L,
+                                            double* out) {
+    cl.sync();
+    const unsigned nr = cl.num_blocks();
+    if (threadIdx.x < static_cast<unsigned>(L)) {
+        double s = 0.0;
+        for (unsigned r = 0; r < nr; ++r) {
+            const double* remote = cl.map_shared_rank(&slot[parity][0], r);
+            s += remote[threadIdx.x];
+        }
+        out[threadIdx.x] = s;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
+    extern __shared__ __align__(16) double w[];  // [rpc][kWs] row-major panel slice
+    __shared__ double slot[2][40];
+    __shared__ double red[8][33];
+    __shared__ double tot[40];
+    __shared__ double Ts[kNbMax][kNbMax + 1];
+    cg::cluster_group cl = cg::this_cluster();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const unsigned rank = cl.block_rank();
+    const int kb = a.kb;
+    const int64_t row0 = a.k0 + static_cast<int64_t>(rank) * a.rpc;  // global first row of this CTA
+    const int64_t nrows = (a.d - row0 < a.rpc ? (a.d - row0 > 0 ? a.d - row0 : 0) : a.rpc);
+
+    // load panel slice: w[il][jj] = Y[row0+il, k0+jj]
+    for (int64_t e = tid; e < nrows * kb; e += kPanelThreads) {
+        const int64_t jj = e / nrows, il = e - jj * nrows;
+        w[il * kWs + jj] = a.Y[(a.k0 + jj) * a.ldy + row0 + il];
+    }
+    __syncthreads();
+    const double rank_tol = *a.rank_tol;
+    int parity = 0;
+
+    for (int kk = 0; kk < kb; ++kk) {
+        const int64_t gk = a.k0 + kk;           // global diagonal row
+        const int64_t lk = gk - row0;           // local index of row gk (may be outside)
+        const bool owner = lk >= 0 && lk < nrows;
+        const int64_t ib = lk + 1 > 0 ? lk + 1 : 0;  // first local row strictly below gk
+
+        // (a) sigma = sum_{i>gk} w_ik^2, and x0 = w[gk][kk]
+        double s = 0.0;
+        for (int64_t il = ib + tid; il < nrows; il += kPanelThreads) {
+            const double v = w[il * kWs + kk];
+            s += v * v;
+        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) red[wid][0] = s;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int q = 0; q < 8; ++q) t += red[q][0];
+            slot[parity][0] = t;
+            slot[parity][1] = owner ? w[lk * kWs + kk] : 0.0;
+        }
+        cluster_sum(cl, slot, parity, 2, tot);
+        parity ^= 1;
+        const double sigma = tot[0], x0 = tot[1];
+        const double normx = sqrt(x0 * x0 + sigma);
+        if (normx < rank_tol || normx == 0.0) {
+            if (rank == 0 && tid == 0) atomicCAS(a.err, 0, static_cast<int>(1 + gk));
+            cl.sync();
+            return;
+        }
+        const double beta = (x0 > 0.0) ? -normx : normx;
+        const double v0 = x0 - beta;
+        const double tau = (beta - x0) / beta;
+        // (b) scale the reflector below the diagonal; R diagonal = beta
+        for (int64_t il = ib + tid; il < nrows; il += kPanelThreads) w[il * kWs + kk] /= v0;
+        __syncthreads();
+        if (owner && tid == 0) w[lk * kWs + kk] = beta;
+
+        // (c) dots for every other panel column jj:
+        //     g_jj = w[gk][jj] + sum_{i>gk} w[i][jj] * v_i
+        //     jj > kk: the reference's s_j (qr.hpp:51-53); jj < kk: v_jj^T v_kk (for T)
+        {
+            const int jj = lane;
+            double acc = 0.0;
+            if (jj < kb)
+                for (int64_t il = ib + wid; il < nrows; il += 8) acc += w[il * kWs + jj] * w[il * kWs + kk];
+            red[wid][jj] = acc;
+            __syncthreads();
+            if (tid < 32) {
+                double t = 0.0;
+                for (int q = 0; q < 8; ++q) t += red[q][tid];
+                if (owner && tid < kb && tid != kk) t += w[lk * kWs + tid];
+                slot[parity][tid] = t;
+            }
+        }
+        cluster_sum(cl, slot, parity, kb, tot);
+        parity ^= 1;
+        // (d) apply H_kk to the remaining panel columns
+        {
+            const int jj = lane;
+            if (jj > kk && jj < kb) {
+                const double sj = tot[jj] * tau;
+                for (int64_t il = ib + wid; il < nrows; il += 8) w[il * kWs + jj] -= sj * w[il * kWs + kk];
+                if (owner && wid == 0) w[lk * kWs + jj] -= sj;
+            }
+        }
+        // compact-WY: T[0:kk, kk] = -tau T[0:kk, 0:kk] (V^T v_kk);  T[kk][kk] = tau
+        if (rank == 0) {
+            if (tid < kk) {
+                double t = 0.0;
+                for (int b = tid; b < kk; ++b) t += Ts[tid][b] * tot[b];
+                Ts[tid][kk] = -tau * t;
+            }
+            if (tid == 0) {
+                Ts[kk][kk] = tau;
+                a.tau[gk] = tau;
+            }
+        }
+        __syncthreads();
+    }
+    // write back the factored slice and T
+    for (int64_t e = tid; e < nrows * kb; e += kPanelThreads) {
+        const int64_t jj = e / nrows, il = e - jj * nrows;
+        a.Y[(a.k0 + jj) * a.ldy + row0 + il] = w[il * kWs + jj];
+    }
+    if (rank == 0)
+        for (int e = tid; e < kNbMax * kNbMax; e += kPanelThreads) {
+            const int i = e % kNbMax, j = e / kNbMax;
+            a.T[j * kNbMax + i] = (i < kb && j < kb && i <= j) ? Ts[i][j] : 0.0;
+        }
+    cl.sync();
+}
+
+// --------------------------------------------------- trailing update (DMMA)
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+struct UpdArgs {
+    const double* V;   // panel storage (column-major, ldv), reflector of panel col a at column a
+    int64_t ldv;
+    int64_t k0;        // global row/col of the panel's first reflector
+    int kb;
+    const double* T;   // kNbMax x kNbMax column-major
+    double* C;         // target matrix (column-major, ldc); rows are global rows
+    int64_t ldc;
+    int64_t c_begin, c_end;  // columns of C to update
+    int64_t r_end;           // rows [k0, r_end)
+    int transT;              // 1: C -= V T^T V^T C (apply H_{kb-1}..H_0); 0: C -= V T V^T C
+};
+
+// V(r, a) with the implicit unit diagonal / zero upper part.
+__device__ __forceinline__ double vget(const UpdArgs& u, int64_t r, int a) {
+    if (a >= u.kb || r >= u.r_end) return 0.0;
+    const int64_t g = u.k0 + a;
+    if (r < g) return 0.0;
+    if (r == g) return 1.0;
+    return u.V[(u.k0 + a) * u.ldv + r];
+}
+
+constexpr int kUpdCols = 16;
+
+__global__ void __launch_bounds__(256) update_kernel(UpdArgs u) {
+    __shared__ double Wred[8][kNbMax][kUpdCols + 1];
+    __shared__ double W[kNbMax][kUpdCols + 1];
+    __shared__ double W2[kNbMax][kUpdCols + 1];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int64_t cb = u.c_begin + static_cast<int64_t>(blockIdx.x) * kUpdCols;
+    const int lr = lane & 3, lg = lane >> 2;
+
+    // step 1: W = V^T C  (kNbMax x 16), rows split over warps in k-steps of 4
+    double acc[4][2][2];
+#pragma unroll
+    for (int at = 0; at < 4; ++at)
+#pragma unroll
+        for (int ct = 0; ct < 2; ++ct) acc[at][ct][0] = acc[at][ct][1] = 0.0;
+    const int64_t nrow = u.r_end - u.k0;
+    const int64_t nks = (nrow + 3) / 4;
+    for (int64_t ks = wid; ks < nks; ks += 8) {
+        const int64_t r = u.k0 + ks * 4 + lr;
+        double bf[2];
+#pragma unroll
+        for (int ct = 0; ct < 2; ++ct) {
+            const int64_t c = cb + ct * 8 + lg;
+            bf[ct] = (r < u.r_end && c < u.c_end) ? u.C[c * u.ldc + r] : 0.0;
+        }
+#pragma unroll
+        for (int at = 0; at < 4; ++at) {
+            const double af = vget(u, r, at * 8 + lg);
+#pragma unroll
+            for (int ct = 0; ct < 2; ++ct) dmma(acc[at][ct][0], acc[at][ct][1], af, bf[ct]);
+        }
+    }
+#pragma unroll
+    for (int at = 0; at < 4; ++at)
+#pragma unroll
+        for (int ct = 0; ct < 2; ++ct) {
+            Wred[wid][at * 8 + lg][ct * 8 + 2 * lr] = acc[at][ct][0];
+            Wred[wid][at * 8 + lg][ct * 8 + 2 * lr + 1] = acc[at][ct][1];
+        }
+    __syncthreads();
+    for (int e = tid; e < kNbMax * kUpdCols; e += 256) {
+        const int a = e / kUpdCols, c = e % kUpdCols;
+        double s = 0.0;
+        for (int q = 0; q < 8; ++q) s += Wred[q][a][c];
+        W[a][c] = s;
+    }
+    __syncthreads();
+    // step 2: W2 = T^T W (transT) or T W
+    for (int e = tid; e < kNbMax * kUpdCols; e += 256) {
+        const int a = e / kUpdCols, c = e % kUpdCols;
+        double s = 0.0;
+        if (u.transT) {
+            for (int b = 0; b <= a; ++b) s += u.T[a * kNbMax + b] * W[b][c];  // T^T[a][b] = T[b][a]
+        } else {
+            for (int b = a; b < kNbMax; ++b) s += u.T[b * kNbMax + a] * W[b][c];
+        }
+        W2[a][c] = s;
+    }
+    __syncthreads();
+    // step 3: C -= V W2, 8-row tiles over warps
+    const int64_t ntiles = (nrow + 7) / 8;
+    for (int64_t t = wid; t < ntiles; t += 8) {
+        const int64_t r0 = u.k0 + t * 8;
+        double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int ks = 0; ks < kNbMax / 4; ++ks) {
+            const double af = vget(u, r0 + lg, ks * 4 + lr);
+#pragma unroll
+            for (int ct = 0; ct < 2; ++ct) {
+                const double bfv = W2[ks * 4 + lr][ct * 8 + lg];
+                dmma(d[ct][0], d[ct][1], af, bfv);
+            }
+        }
+        const int64_t r = r0 + lg;
+        if (r < u.r_end) {
+#pragma unroll
+            for (int ct = 0; ct < 2; ++ct)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int64_t c = cb + ct * 8 + 2 * lr + e;
+                    if (c < u.c_end) u.C[c * u.ldc + r] -= d[ct][e];
+                }
+        }
+    }
+}
+
+// R = triu(Y[0:n,0:n]) with the diag >= 0 flip (qr.hpp:79-86); flips the
+// transformed Sb column (Q^T Sb) and records the signs.
+__global__ void extract_r_kernel(const double* Y, int64_t ldy, int64_t n, double* R, double* sign,
+                                 const double* qtb_col, double* qtb) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= n * n) return;
+    const int64_t j = e / n, i = e - j * n;
+    const double dsgn = (Y[i * ldy + i] < 0.0) ? -1.0 : 1.0;
+    R[e] = (i <= j) ? dsgn * Y[j * ldy + i] : 0.0;
+    if (j == 0) {
+        sign[i] = dsgn;
+        if (qtb_col) qtb[i] = dsgn * qtb_col[i];
+    }
+}
+
+__global__ void check_diag_kernel(const double* R, int64_t n, int* err) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n && R[i * n + i] == 0.0) atomicMin(err, static_cast<int>(i));
+}
+
+// M = R^-1 (upper, column-major) and Mt (row-major copy: Mt[i*n+j] = M(i,j)).
+// One warp per column j: x = e_j, back-substitution in column-axpy form with
+// x staged in shared memory (triangular.hpp:14-33 computes the same entries
+// by dot-product back-substitution).
+__global__ void __launch_bounds__(128) tri_inverse_kernel(const double* R, int64_t n, double* M,
+                                                          double* Mt) {
+    extern __shared__ double xs[];  // [4][n]
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * 4 + wid;
+    if (j >= n) return;
+    double* x = xs + wid * n;
+    for (int64_t i = lane; i <= j; i += 32) x[i] = (i == j) ? 1.0 : 0.0;
+    __syncwarp();
+    for (int64_t i = j; i >= 0; --i) {
+        const double xi = x[i] / R[i * n + i];
+        __syncwarp();
+        if (lane == 0) x[i] = xi;
+        const double* ri = R + i * n;
+        for (int64_t l = lane; l < i; l += 32) x[l] -= xi * ri[l];
+        __syncwarp();
+    }
+    for (int64_t i = lane; i < n; i += 32) {
+        const double v = (i <= j) ? x[i] : 0.0;
+        M[j * n + i] = v;
+        if (Mt) Mt[i * n + j] = v;
+    }
+}
+
+// y = M v with M upper (row-major copy Mt): warp per row i.
+// lower != 0: the stored matrix is read as lower triangular (j <= i).
+__global__ void trmv_rows_kernel(const double* Mt, int64_t n, const double* v, double* y, int lower) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (i >= n) return;
+    const double* row = Mt + i * n;
+    double s = 0.0;
+    const int64_t jb = lower ? 0 : i, je = lower ? i + 1 : n;
+    for (int64_t j = jb + lane; j < je; j += 32) s += row[j] * v[j];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) y[i] = s;
+}
+
+__global__ void set_identity_kernel(double* Q, int64_t d, int64_t n) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= d * n) return;
+    const int64_t j = e / d, i = e - j * d;
+    Q[e] = (i == j) ? 1.0 : 0.0;
+}
+
+__global__ void scale_cols_kernel(double* Q, int64_t d, int64_t n, const double* sign) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= d * n) return;
+    Q[e] *= sign[e / d];
+}
+
+void launch_panel(slq_ctx* ctx, const PanelArgs& pa, int cl) {
+    const size_t smem = static_cast<size_t>(pa.rpc) * kWs * sizeof(double);
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    if (cl > 8)
+        SLQ_CUDA_CHECK(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl, 1, 1);
+    cfg.blockDim = dim3(kPanelThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SLQ_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel_kernel, pa));
+    ctx->launches++;
+}
+
+void launch_update(slq_ctx* ctx, const UpdArgs& u) {
+    if (u.c_end <= u.c_begin || u.r_end <= u.k0) return;
+    const unsigned grid = static_cast<unsigned>(ceil_div(u.c_end - u.c_begin, kUpdCols));
+    update_kernel<<<grid, 256, 0, ctx->stream>>>(u);
+    SLQ_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace
+
+void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t ncols, int64_t ldy,
+                   double* R, double* qtb, double* Q, double* sign_out) {
+    if (d < n) fail(SLQ_DIMENSION_MISMATCH, "householder_qr: need rows >= cols");
+    Workspace& ws = ctx->ws;
+    const int64_t npanels = ceil_div(n, kNbMax);
+    double* T = static_cast<double*>(ws.qr_t.ensure(sizeof(double) * kNbMax * kNbMax * std::max<int64_t>(1, npanels)));
+    double* misc = static_cast<double*>(ws.qr_misc.ensure(sizeof(double) * (2 * n + 1024 + 8)));
+    double* tau = misc;
+    double* sign = misc + n;
+    double* part = misc + 2 * n;          // 1024 partial maxima
+    double* rank_tol = misc + 2 * n + 1024;
+    int* err = static_cast<int*>(ws.flags.ensure(4096)) + 4;
+    SLQ_CUDA_CHECK(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+    if (n == 0) return;
+
+    const int nmax = 1024;
+    const int nb_blocks = static_cast<int>(std::min<int64_t>(nmax, ceil_div(d * n, 256)));
+    maxabs_kernel<<<nb_blocks, 256, 0, ctx->stream>>>(Yaug, d, n, ldy, part);
+    SLQ_LAUNCH_CHECK(ctx);
+    maxabs_final_kernel<<<1, 32, 0, ctx->stream>>>(part, nb_blocks, rank_tol);
+    SLQ_LAUNCH_CHECK(ctx);
+
+    for (int64_t p = 0; p < npanels; ++p) {
+        const int64_t k0 = p * kNbMax;
+        const int kb = static_cast<int>(std::min<int64_t>(kNbMax, n - k0));
+        const int64_t rows = d - k0;
+        int cl = 1;
+        const int64_t max_rows_cta = (200 * 1024) / (kWs * 8);  // 775 rows per CTA
+        while (ceil_div(rows, cl) > max_rows_cta && cl < 16) cl *= 2;
+        if (ceil_div(rows, cl) > max_rows_cta) fail(SLQ_UNSUPPORTED, "householder_qr: sketch too tall for the panel kernel");
+        // prefer more CTAs for tall panels: lowers per-column latency of the local work
+        while (cl < 8 && ceil_div(rows, cl) > 256) cl *= 2;
+        PanelArgs pa{Yaug, ldy, d, k0, kb, ceil_div(rows, cl), rank_tol, tau, T + p * kNbMax * kNbMax, err};
+        launch_panel(ctx, pa, cl);
+        UpdArgs u{Yaug, ldy, k0, kb, T + p * kNbMax * kNbMax, Yaug, ldy, k0 + kb, ncols, d, 1};
+        launch_update(ctx, u);
+    }
+    int herr = 0;
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (herr) fail(SLQ_RANK_DEFICIENT, "householder_qr: column " + std::to_string(herr - 1) + " numerically dependent");
+
+    const double* qtb_col = (ncols > n && qtb) ? Yaug + n * ldy : nullptr;
+    extract_r_kernel<<<static_cast<unsigned>(ceil_div(n * n, 256)), 256, 0, ctx->stream>>>(Yaug, ldy, n, R, sign,
+                                                                                        qtb_col, qtb);
+    SLQ_LAUNCH_CHECK(ctx);
+    if (sign_out) SLQ_CUDA_CHECK(cudaMemcpyAsync(sign_out, sign, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (Q) {
+        // Q = H_0 ... H_{n-1} [I_n; 0], panels back to front (qr.hpp:64-77)
+        set_identity_kernel<<<static_cast<unsigned>(ceil_div(d * n, 256)), 256, 0, ctx->stream>>>(Q, d, n);
+        SLQ_LAUNCH_CHECK(ctx);
+        for (int64_t p = npanels - 1; p >= 0; --p) {
+            const int64_t k0 = p * kNbMax;
+            const int kb = static_cast<int>(std::min<int64_t>(kNbMax, n - k0));
+            UpdArgs u{Yaug, ldy, k0, kb, T + p * kNbMax * kNbMax, Q, d, k0, n, d, 0};
+            launch_update(ctx, u);
+        }
+        scale_cols_kernel<<<static_cast<unsigned>(ceil_div(d * n, 256)), 256, 0, ctx->stream>>>(Q, d, n, sign);
+        SLQ_LAUNCH_CHECK(ctx);
+    }
+}
+
+void tri_inverse_dev(slq_ctx* ctx, const double* R, int64_t n, double* M, double* Mt) {
+    int* err = static_cast<int*>(ctx->ws.flags.ensure(4096)) + 8;
+    const int big = 0x7fffffff;
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(err, &big, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    check_diag_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, ctx->stream>>>(R, n, err);
+    SLQ_LAUNCH_CHECK(ctx);
+    int herr = 0;
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (herr != big) fail(SLQ_SINGULAR_TRIANGULAR, "tri_inverse: zero diagonal at " + std::to_string(herr));
+    const size_t smem = 4 * n * sizeof(double);
+    if (smem > 227 * 1024) fail(SLQ_UNSUPPORTED, "tri_inverse: n too large");
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(tri_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    tri_inverse_kernel<<<static_cast<unsigned>(ceil_div(n, 4)), 128, smem, ctx->stream>>>(R, n, M, Mt);
+    SLQ_LAUNCH_CHECK(ctx);
+}
+
+void trmv_upper_dev(slq_ctx* ctx, const double* Mt, int64_t n, const double* v, double* y) {
+    trmv_rows_kernel<<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, ctx->stream>>>(Mt, n, v, y, 0);
+    SLQ_LAUNCH_CHECK(ctx);
+}
+
+void trmv_upper_trans_dev(slq_ctx* ctx, const double* M, int64_t n, const double* v, double* y) {
+    // M column-major read as row-major is M^T (lower triangular)
+    trmv_rows_kernel<<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, ctx->stream>>>(M, n, v, y, 1);
+    SLQ_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace slq

@@ -1,0 +1,574 @@
+// sketch.cu -- K1 sparse-sign generation and K2 sketch apply (sm_100a).
+//
+// K1 replaces sketch.hpp:75-94 (rejection_sample_one), sketch.hpp:149-173
+// (sparse_sign_block) and sketch.hpp:178-194 (generate_sparse_sign), bit-exact.
+// Layout: one warp holds 32/G sketch columns, G = next_pow2(zeta) lanes per
+// column, lane i computing draw i of the column's index substream directly
+// (Weyl counter, rng.cuh).  A shuffle bitonic network sorts the G draws, a
+// shfl_up comparison + __ballot_sync finds duplicates; columns with a
+// duplicate (or a Lemire rejection) are replayed exactly by the group leader
+// (the reference's left-to-right redraw loop), which happens for ~zeta^2/d of
+// the columns (0.7% at d=4000, zeta=8).
+//
+// K2 replaces csc_matrix.hpp:103-120 (spmm(csc, dense)) + csc_matrix.hpp:71-82
+// (S b): Y_aug = S [A | b].  The sketch entries are bucketed once per chunk of
+// K rows of A ("chunk-CSR": entries sorted by (target row r, k)), then each
+// CTA owns a W-column slab of Y_aug held in REGISTERS (thread t owns Y rows
+// t, t+512, ...) and streams its W-column slab of A through shared memory
+// (cp.async double buffer).  Every Y element is accumulated by one thread in
+// ascending k -- the reference's order -- with IEEE mul then add, so one
+// split reproduces the reference Y bit for bit.  No atomics anywhere.
+#include <algorithm>
+#include <cmath>
+
+#include "rng.cuh"
+#include "sketch.cuh"
+
+namespace slq {
+
+namespace {
+
+constexpr uint32_t kPad = 0xFFFFFFFFu;
+
+struct GenArgs {
+    int64_t d, zeta, col_begin, ncols;
+    uint64_t seed_mixed, thresh;
+    double val;
+    uint32_t* compact;
+    int64_t* rows64;
+    double* vals;
+    int64_t* colptr;
+    unsigned long long* stats;
+};
+
+template <class T>
+__device__ void insertion_sort(T* a, int64_t n) {
+    for (int64_t i = 1; i < n; ++i) {
+        T v = a[i];
+        int64_t j = i - 1;
+        while (j >= 0 && a[j] > v) {
+            a[j + 1] = a[j];
+            --j;
+        }
+        a[j + 1] = v;
+    }
+}
+
+template <class T>
+__device__ void heap_sort(T* a, int64_t n) {
+    auto sift = [&](int64_t start, int64_t end) {
+        int64_t root = start;
+        while (2 * root + 1 <= end) {
+            int64_t child = 2 * root + 1, sw = root;
+            if (a[sw] < a[child]) sw = child;
+            if (child + 1 <= end && a[sw] < a[child + 1]) sw = child + 1;
+            if (sw == root) return;
+            T t = a[root];
+            a[root] = a[sw];
+            a[sw] = t;
+            root = sw;
+        }
+    };
+    for (int64_t s = (n - 2) / 2; s >= 0; --s) sift(s, n - 1);
+    for (int64_t e = n - 1; e > 0; --e) {
+        T t = a[0];
+        a[0] = a[e];
+        a[e] = t;
+        sift(0, e - 1);
+    }
+}
+
+template <class T>
+__device__ __forceinline__ void sort_small(T* a, int64_t n) {
+    if (n <= 64) insertion_sort(a, n);
+    else heap_sort(a, n);
+}
+
+// sketch.hpp:75-94, sequential, on an array of T.  Returns resampled flag.
+template <class T>
+__device__ bool replay_column(T* out, int64_t zeta, uint64_t d, uint64_t thresh, uint64_t s0,
+                              unsigned long long* rounds) {
+    SeqRng rng{s0};
+    for (int64_t i = 0; i < zeta; ++i) out[i] = static_cast<T>(rng.below(d, thresh));
+    sort_small(out, zeta);
+    bool resampled = false;
+    for (;;) {
+        int64_t bad = 0;
+        for (int64_t i = 1; i < zeta; ++i) {
+            if (out[i] == out[i - 1]) {
+                out[i] = static_cast<T>(rng.below(d, thresh));
+                ++bad;
+            }
+        }
+        if (bad == 0) break;
+        resampled = true;
+        ++(*rounds);
+        sort_small(out, zeta);
+    }
+    return resampled;
+}
+
+// Warp-group generator: G lanes per column (zeta <= G <= 32), d < 2^31.
+template <int G>
+__global__ void __launch_bounds__(256) gen_warp_kernel(GenArgs a) {
+    constexpr int kCols = 32 / G;
+    __shared__ uint32_t fb[8][32];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int gl = lane & (G - 1);
+    const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t j = gwarp * kCols + lane / G;
+    const bool col_ok = j < a.ncols;
+    const bool active = col_ok && gl < a.zeta;
+    const uint64_t gj = static_cast<uint64_t>(a.col_begin + (col_ok ? j : 0));
+
+    const uint64_t s_idx = stream_state(a.seed_mixed, 2 * gj);
+    bool rej = false;
+    uint32_t key = kPad;
+    if (active) key = static_cast<uint32_t>(lemire(draw_at(s_idx, gl + 1), a.d, a.thresh, rej));
+    rej = rej && active;
+
+    // bitonic sort of G keys within the group (ascending, pads last)
+#pragma unroll
+    for (int k = 2; k <= G; k <<= 1) {
+#pragma unroll
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            uint32_t other = __shfl_xor_sync(0xffffffffu, key, jj);
+            const bool up = (gl & k) == 0;
+            const bool lower = (gl & jj) == 0;
+            key = (lower == up) ? min(key, other) : max(key, other);
+        }
+    }
+    uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1, G);
+    const bool dup = active && gl > 0 && key == prev;
+    const unsigned bal = __ballot_sync(0xffffffffu, dup || rej);
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const bool need = (bal & gmask) != 0;
+    if (__any_sync(0xffffffffu, need)) {
+        if (need && gl == 0) {
+            uint32_t* buf = &fb[wib][lane];
+            unsigned long long rounds = 0;
+            bool res = replay_column(buf, a.zeta, a.d, a.thresh, s_idx, &rounds);
+            if (a.stats) {
+                if (res) atomicAdd(&a.stats[0], 1ull);
+                if (rounds) atomicAdd(&a.stats[1], rounds);
+            }
+        }
+        __syncwarp();
+        if (need && active) key = fb[wib][(lane & ~(G - 1)) + gl];
+        __syncwarp();
+    }
+    if (!active) return;
+    // sketch.hpp:168-169: sign i (drawn in order from stream 2j+1) pairs with
+    // the i-th smallest row.
+    const uint64_t s_val = stream_state(a.seed_mixed, 2 * gj + 1);
+    const bool pos = draw_at(s_val, gl + 1) & 1u;
+    const int64_t e = j * a.zeta + gl;
+    if (a.compact) a.compact[e] = key | (pos ? 0u : 0x80000000u);
+    if (a.rows64) a.rows64[e] = key;
+    if (a.vals) a.vals[e] = pos ? a.val : -a.val;
+    if (a.colptr) {
+        if (gl == 0) a.colptr[j + 1] = (j + 1) * a.zeta;
+        if (j == 0 && gl == 0) a.colptr[0] = 0;
+    }
+}
+
+// Generic path (zeta > 32 or huge d): one thread per column, sequential
+// replay on an int64 work array (rows64, always provided by the host).
+__global__ void gen_generic_kernel(GenArgs a) {
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= a.ncols) return;
+    const uint64_t gj = static_cast<uint64_t>(a.col_begin + j);
+    int64_t* rows = a.rows64 + j * a.zeta;
+    unsigned long long rounds = 0;
+    bool res = replay_column(rows, a.zeta, a.d, a.thresh, stream_state(a.seed_mixed, 2 * gj), &rounds);
+    if (a.stats) {
+        if (res) atomicAdd(&a.stats[0], 1ull);
+        if (rounds) atomicAdd(&a.stats[1], rounds);
+    }
+    SeqRng vr{stream_state(a.seed_mixed, 2 * gj + 1)};
+    for (int64_t i = 0; i < a.zeta; ++i) {
+        const bool pos = vr.next() & 1u;
+        if (a.vals) a.vals[j * a.zeta + i] = pos ? a.val : -a.val;
+        if (a.compact) a.compact[j * a.zeta + i] = static_cast<uint32_t>(rows[i]) | (pos ? 0u : 0x80000000u);
+    }
+    if (a.colptr) {
+        a.colptr[j + 1] = (j + 1) * a.zeta;
+        if (j == 0) a.colptr[0] = 0;
+    }
+}
+
+// ------------------------------------------------------------- K2 bucketize
+
+struct BucketArgs {
+    const uint32_t* compact;
+    const int64_t* colptr;  // null => uniform zeta
+    int64_t zeta, ncols, d;
+    int K, KB;
+    int64_t ptr_stride, ent_stride;  // u16 units per chunk
+    uint16_t* ptr_out;
+    uint16_t* ent_out;
+    int cap;                         // smem key capacity (power of 2)
+    int* overflow;
+};
+
+__global__ void __launch_bounds__(1024) bucketize_kernel(BucketArgs a) {
+    extern __shared__ uint32_t keys[];
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int64_t c = blockIdx.x;
+    const int64_t k0 = c * a.K;
+    const int64_t kc = min(static_cast<int64_t>(a.K), a.ncols - k0);
+    const int64_t eb = a.colptr ? a.colptr[k0] : k0 * a.zeta;
+    const int64_t ee = a.colptr ? a.colptr[k0 + kc] : (k0 + kc) * a.zeta;
+    const int N = static_cast<int>(ee - eb);
+    if (N > a.cap) {
+        if (tid == 0) atomicExch(a.overflow, 1);
+        return;
+    }
+    int NP = 2;
+    while (NP < N) NP <<= 1;
+    const int sh = a.KB + 1;
+    if (a.colptr) {
+        for (int64_t kl = tid; kl < kc; kl += T)
+            for (int64_t e = a.colptr[k0 + kl]; e < a.colptr[k0 + kl + 1]; ++e) {
+                const uint32_t ent = a.compact[e];
+                keys[e - eb] = ((ent & 0x7fffffffu) << sh) | (static_cast<uint32_t>(kl) << 1) | (ent >> 31);
+            }
+    } else {
+        for (int i = tid; i < N; i += T) {
+            const uint32_t ent = a.compact[eb + i];
+            const uint32_t kl = static_cast<uint32_t>(i / a.zeta);
+            keys[i] = ((ent & 0x7fffffffu) << sh) | (kl << 1) | (ent >> 31);
+        }
+    }
+    for (int i = N + tid; i < NP; i += T) keys[i] = kPad;
+    __syncthreads();
+    for (int k = 2; k <= NP; k <<= 1) {
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int i = tid; i < (NP >> 1); i += T) {
+                const int lo = ((i & ~(jj - 1)) << 1) | (i & (jj - 1));
+                const int hi = lo + jj;
+                const bool asc = (lo & k) == 0;
+                const uint32_t x = keys[lo], y = keys[hi];
+                if ((x > y) == asc) {
+                    keys[lo] = y;
+                    keys[hi] = x;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    uint16_t* ent = a.ent_out + c * a.ent_stride;
+    uint16_t* ptr = a.ptr_out + c * a.ptr_stride;
+    const uint32_t lowmask = (1u << sh) - 1u;
+    for (int i = tid; i < N; i += T) {
+        ent[i] = static_cast<uint16_t>(keys[i] & lowmask);
+        const int64_t r = keys[i] >> sh;
+        const int64_t rp = (i == 0) ? -1 : static_cast<int64_t>(keys[i - 1] >> sh);
+        for (int64_t rr = rp + 1; rr <= r; ++rr) ptr[rr] = static_cast<uint16_t>(i);
+    }
+    const int64_t rl = (N == 0) ? -1 : static_cast<int64_t>(keys[N - 1] >> sh);
+    for (int64_t rr = rl + 1 + tid; rr <= a.d; rr += T) ptr[rr] = static_cast<uint16_t>(N);
+}
+
+// ---------------------------------------------------------------- K2 gather
+
+struct GatherArgs {
+    const double* A;  // row-major block, row 0 = local row 0
+    int64_t ld, m, d;
+    int K;
+    int64_t nchunks, nsplit;
+    int64_t ptr_stride, ent_stride;
+    const uint16_t* ptr;
+    const uint16_t* ent;
+    double val;
+    double* Yw;  // [nsplit][ld][d]
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// 16-byte slot of half h of row k in the A stage (W=4): XOR swizzle so the
+// first halves of random rows spread over all eight 16-byte bank groups.
+__device__ __forceinline__ int slot4(int k, int h) { return 2 * k + (h ^ ((k >> 2) & 1)); }
+
+template <int W>
+__device__ __forceinline__ void stage_chunk(const GatherArgs& g, int64_t col0, int64_t c, double* As,
+                                            uint16_t* Ps, uint16_t* Es) {
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int64_t k0 = c * g.K;
+    const int kc = static_cast<int>(min(static_cast<int64_t>(g.K), g.m - k0));
+    const double* base = g.A + k0 * g.ld + col0;
+    if (W == 4) {
+        for (int p = tid; p < 2 * kc; p += T) {
+            const int k = p >> 1, h = p & 1;
+            cp_async16(As + 2 * slot4(k, h), base + k * g.ld + 2 * h);
+        }
+    } else if (W == 2) {
+        for (int k = tid; k < kc; k += T) cp_async16(As + 2 * k, base + k * g.ld);
+    } else {
+        for (int k = tid; k < kc; k += T) cp_async8(As + k, base + k * g.ld);
+    }
+    const uint16_t* gp = g.ptr + c * g.ptr_stride;
+    for (int p = tid; p < g.ptr_stride / 8; p += T) cp_async16(Ps + 8 * p, gp + 8 * p);
+    const uint16_t* ge = g.ent + c * g.ent_stride;
+    const int nent = static_cast<int>(g.ent_stride / 8);
+    for (int p = tid; p < nent; p += T) cp_async16(Es + 8 * p, ge + 8 * p);
+}
+
+template <int W, int RPT>
+__global__ void __launch_bounds__(512, 1) gather_kernel(GatherArgs g) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int tid = threadIdx.x;
+    constexpr int T = 512;
+    const int64_t col0 = static_cast<int64_t>(blockIdx.x) * W;
+    const int64_t split = blockIdx.y;
+    const int64_t cb = split * g.nchunks / g.nsplit;
+    const int64_t ce = (split + 1) * g.nchunks / g.nsplit;
+
+    const size_t a_bytes = static_cast<size_t>(g.K) * W * sizeof(double);
+    const size_t p_bytes = g.ptr_stride * sizeof(uint16_t);
+    const size_t e_bytes = g.ent_stride * sizeof(uint16_t);
+    const size_t st_bytes = a_bytes + p_bytes + e_bytes;
+    auto As = [&](int s) { return reinterpret_cast<double*>(smem + s * st_bytes); };
+    auto Ps = [&](int s) { return reinterpret_cast<uint16_t*>(smem + s * st_bytes + a_bytes); };
+    auto Es = [&](int s) { return reinterpret_cast<uint16_t*>(smem + s * st_bytes + a_bytes + p_bytes); };
+
+    double y[RPT][W];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q)
+#pragma unroll
+        for (int w = 0; w < W; ++w) y[q][w] = 0.0;
+
+    if (cb < ce) stage_chunk<W>(g, col0, cb, As(0), Ps(0), Es(0));
+    cp_commit();
+    for (int64_t c = cb; c < ce; ++c) {
+        const int s = static_cast<int>((c - cb) & 1);
+        if (c + 1 < ce) stage_chunk<W>(g, col0, c + 1, As(s ^ 1), Ps(s ^ 1), Es(s ^ 1));
+        cp_commit();
+        cp_wait<1>();
+        __syncthreads();
+        const double* A_s = As(s);
+        const uint16_t* P_s = Ps(s);
+        const uint16_t* E_s = Es(s);
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const int r = tid + q * T;
+            if (r < g.d) {
+                const int e0 = P_s[r], e1 = P_s[r + 1];
+                for (int e = e0; e < e1; ++e) {
+                    const unsigned en = E_s[e];
+                    const int k = static_cast<int>(en >> 1);
+                    const double v = (en & 1u) ? -g.val : g.val;
+                    if (W == 4) {
+                        const double2 lo = *reinterpret_cast<const double2*>(A_s + 2 * slot4(k, 0));
+                        const double2 hi = *reinterpret_cast<const double2*>(A_s + 2 * slot4(k, 1));
+                        y[q][0] = __dadd_rn(y[q][0], __dmul_rn(v, lo.x));
+                        y[q][1 % W] = __dadd_rn(y[q][1 % W], __dmul_rn(v, lo.y));
+                        y[q][2 % W] = __dadd_rn(y[q][2 % W], __dmul_rn(v, hi.x));
+                        y[q][3 % W] = __dadd_rn(y[q][3 % W], __dmul_rn(v, hi.y));
+                    } else if (W == 2) {
+                        const double2 lo = *reinterpret_cast<const double2*>(A_s + 2 * k);
+                        y[q][0] = __dadd_rn(y[q][0], __dmul_rn(v, lo.x));
+                        y[q][1 % W] = __dadd_rn(y[q][1 % W], __dmul_rn(v, lo.y));
+                    } else {
+                        y[q][0] = __dadd_rn(y[q][0], __dmul_rn(v, A_s[k]));
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    cp_wait<0>();
+    double* Y = g.Yw + split * g.ld * g.d;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        const int r = tid + q * T;
+        if (r < g.d)
+#pragma unroll
+            for (int w = 0; w < W; ++w) Y[(col0 + w) * g.d + r] = y[q][w];
+    }
+}
+
+// Y[:, j] = sum over splits, fixed order (deterministic).
+__global__ void reduce_splits_kernel(const double* Yw, int64_t nsplit, int64_t d, int64_t ld,
+                                     int64_t ncols, double* Y) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= d * ncols) return;
+    double s = Yw[i];
+    for (int64_t p = 1; p < nsplit; ++p) s = __dadd_rn(s, Yw[p * ld * d + i]);
+    Y[i] = s;
+}
+
+uint64_t lemire_thresh(uint64_t d) { return (0 - d) % d; }
+
+}  // namespace
+
+void generate_sparse_sign_dev(slq_ctx* ctx, int64_t d, int64_t zeta, uint64_t seed,
+                              int64_t col_begin, int64_t ncols, uint32_t* compact,
+                              int64_t* rows64, double* vals, int64_t* colptr,
+                              unsigned long long* stats) {
+    if (zeta > d || zeta < 1) fail(SLQ_INVALID_SPARSITY, "generate_sparse_sign: need 1 <= zeta <= d");
+    if (ncols <= 0) {
+        if (colptr) SLQ_CUDA_CHECK(cudaMemsetAsync(colptr, 0, sizeof(int64_t), ctx->stream));
+        return;
+    }
+    GenArgs a{d, zeta, col_begin, ncols, mix64(seed), lemire_thresh(static_cast<uint64_t>(d)),
+              1.0 / std::sqrt(static_cast<double>(zeta)), compact, rows64, vals, colptr, stats};
+    const bool warp_path = zeta <= 32 && d < (int64_t(1) << 31);
+    if (warp_path) {
+        int G = 1;
+        while (G < zeta) G <<= 1;
+        const int64_t cols_per_block = 8 * (32 / G);
+        const unsigned grid = static_cast<unsigned>(ceil_div(ncols, cols_per_block));
+        switch (G) {
+            case 1: gen_warp_kernel<1><<<grid, 256, 0, ctx->stream>>>(a); break;
+            case 2: gen_warp_kernel<2><<<grid, 256, 0, ctx->stream>>>(a); break;
+            case 4: gen_warp_kernel<4><<<grid, 256, 0, ctx->stream>>>(a); break;
+            case 8: gen_warp_kernel<8><<<grid, 256, 0, ctx->stream>>>(a); break;
+            case 16: gen_warp_kernel<16><<<grid, 256, 0, ctx->stream>>>(a); break;
+            default: gen_warp_kernel<32><<<grid, 256, 0, ctx->stream>>>(a); break;
+        }
+        SLQ_LAUNCH_CHECK(ctx);
+    } else {
+        if (!rows64) fail(SLQ_INVALID_ARG, "generic generator path needs an int64 work array");
+        if (compact && d >= (int64_t(1) << 31)) fail(SLQ_UNSUPPORTED, "compact sketch needs d < 2^31");
+        const unsigned grid = static_cast<unsigned>(ceil_div(ncols, 128));
+        gen_generic_kernel<<<grid, 128, 0, ctx->stream>>>(a);
+        SLQ_LAUNCH_CHECK(ctx);
+    }
+}
+
+namespace {
+
+struct ChunkPlan {
+    int K, KB, cap;
+    int64_t nchunks, ptr_stride, ent_stride;
+};
+
+ChunkPlan plan_chunks(int64_t m, int64_t d, int64_t zeta_max) {
+    ChunkPlan p{};
+    // entries per chunk <= 16384 (u16 offsets, 64 KB of sort keys)
+    int zp = 1;
+    while (zp < zeta_max) zp <<= 1;
+    p.K = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(16, 16384 / zp)));
+    p.KB = 0;
+    while ((1 << p.KB) < p.K) ++p.KB;
+    p.cap = 16384;
+    p.nchunks = ceil_div(m, p.K);
+    p.ptr_stride = round_up(d + 1, 8);
+    p.ent_stride = round_up(static_cast<int64_t>(p.K) * zeta_max, 8);
+    return p;
+}
+
+template <int W, int RPT>
+void launch_gather(slq_ctx* ctx, const GatherArgs& g, int64_t nslabs, size_t smem) {
+    auto kern = gather_kernel<W, RPT>;
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    dim3 grid(static_cast<unsigned>(nslabs), static_cast<unsigned>(g.nsplit));
+    kern<<<grid, 512, smem, ctx->stream>>>(g);
+    SLQ_LAUNCH_CHECK(ctx);
+}
+
+}  // namespace
+
+void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32_t* compact,
+                              const int64_t* colptr_dev, int64_t zeta, double val, bool exact,
+                              double* Y) {
+    const int64_t m = A->m, ld = A->ld, ncols_out = A->n + 1;
+    if (d > 16384) fail(SLQ_UNSUPPORTED, "sketch_apply: d > 16384 not supported");
+    if (d >= (int64_t(1) << 21)) fail(SLQ_UNSUPPORTED, "sketch_apply: d too large for chunk keys");
+    Workspace& ws = ctx->ws;
+    if (m == 0) {
+        SLQ_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(double) * d * ncols_out, ctx->stream));
+        return;
+    }
+    ChunkPlan cp = plan_chunks(m, d, zeta);
+    uint16_t* ptr = ws.chunk_ptr.as<uint16_t>();
+    ptr = static_cast<uint16_t*>(ws.chunk_ptr.ensure(sizeof(uint16_t) * cp.ptr_stride * cp.nchunks));
+    uint16_t* ent = static_cast<uint16_t*>(ws.chunk_ent.ensure(sizeof(uint16_t) * cp.ent_stride * cp.nchunks));
+    int* flags = static_cast<int*>(ws.flags.ensure(4096));
+    SLQ_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int), ctx->stream));
+
+    BucketArgs ba{compact, colptr_dev, zeta, m, d, cp.K, cp.KB, cp.ptr_stride, cp.ent_stride, ptr, ent,
+                  cp.cap, flags};
+    const size_t bsmem = sizeof(uint32_t) * cp.cap;
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(bucketize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(bsmem)));
+    bucketize_kernel<<<static_cast<unsigned>(cp.nchunks), 1024, bsmem, ctx->stream>>>(ba);
+    SLQ_LAUNCH_CHECK(ctx);
+
+    // slab width W and rows per thread RPT: RPT * W <= 32 doubles of registers
+    int W = 4;
+    int64_t rpt = ceil_div(d, 512);
+    if (rpt > 8) W = (rpt > 16) ? 1 : 2;
+    int RPT = 1;
+    while (RPT < rpt) RPT <<= 1;
+    const int64_t nslabs = ld / W;
+    // splits: balance waves over the SMs unless the exact serial order is asked for
+    int64_t nsplit = 1;
+    if (!exact) {
+        double best = 1e30;
+        for (int64_t s = 1; s <= 16; ++s) {
+            if (s > cp.nchunks) break;
+            const int64_t ctas = nslabs * s;
+            const double waves = std::ceil(static_cast<double>(ctas) / ctx->num_sms);
+            const double cost = waves / s + 0.02 * s;  // per-split overhead (partials + reduce)
+            if (cost < best - 1e-9) {
+                best = cost;
+                nsplit = s;
+            }
+        }
+    }
+    double* Yw = (nsplit == 1 && ld == ncols_out) ? Y
+                 : static_cast<double*>(ws.ypart.ensure(sizeof(double) * nsplit * ld * d));
+    GatherArgs g{A->A, ld, m, d, cp.K, cp.nchunks, nsplit, cp.ptr_stride, cp.ent_stride, ptr, ent, val, Yw};
+    const size_t smem = 2 * (static_cast<size_t>(cp.K) * W * sizeof(double) +
+                             cp.ptr_stride * sizeof(uint16_t) + cp.ent_stride * sizeof(uint16_t));
+    if (smem > 227 * 1024) fail(SLQ_UNSUPPORTED, "sketch_apply: stage exceeds shared memory");
+    switch (W * 100 + RPT) {
+        case 401: launch_gather<4, 1>(ctx, g, nslabs, smem); break;
+        case 402: launch_gather<4, 2>(ctx, g, nslabs, smem); break;
+        case 404: launch_gather<4, 4>(ctx, g, nslabs, smem); break;
+        case 408: launch_gather<4, 8>(ctx, g, nslabs, smem); break;
+        case 216: launch_gather<2, 16>(ctx, g, nslabs, smem); break;
+        case 132: launch_gather<1, 32>(ctx, g, nslabs, smem); break;
+        default: fail(SLQ_UNSUPPORTED, "sketch_apply: unsupported slab configuration");
+    }
+    if (Yw != Y) {
+        const int64_t tot = d * ncols_out;
+        reduce_splits_kernel<<<static_cast<unsigned>(ceil_div(tot, 256)), 256, 0, ctx->stream>>>(
+            Yw, nsplit, d, ld, ncols_out, Y);
+        SLQ_LAUNCH_CHECK(ctx);
+    }
+    int hflag = 0;
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(&hflag, flags, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (hflag) fail(SLQ_UNSUPPORTED, "sketch_apply: a chunk exceeded 16384 sketch entries");
+}
+
+void sketch_apply_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed,
+                      bool exact, double* Y) {
+    if (zeta > d || zeta < 1) fail(SLQ_INVALID_SPARSITY, "apply: need 1 <= zeta <= d");
+    if (zeta > 1024) fail(SLQ_UNSUPPORTED, "sketch_apply: zeta > 1024");
+    Workspace& ws = ctx->ws;
+    const int64_t m = A->m;
+    uint32_t* compact = static_cast<uint32_t*>(ws.compact.ensure(sizeof(uint32_t) * std::max<int64_t>(1, m * zeta)));
+    int64_t* work = nullptr;
+    if (zeta > 32) work = static_cast<int64_t*>(ws.tmp.ensure(sizeof(int64_t) * m * zeta));
+    generate_sparse_sign_dev(ctx, d, zeta, seed, A->row_begin, m, compact, work, nullptr, nullptr, nullptr);
+    sketch_apply_compact_dev(ctx, A, d, compact, nullptr, zeta, 1.0 / std::sqrt(static_cast<double>(zeta)),
+                             exact, Y);
+}
+
+}  // namespace slq

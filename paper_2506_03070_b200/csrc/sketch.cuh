@@ -1,0 +1,28 @@
+// sketch.cuh -- host entry points of the sparse-sign sketch kernels (K1, K2).
+#pragma once
+
+#include "common.cuh"
+
+namespace slq {
+
+// K1: sparse-sign generator for global columns [col_begin, col_begin+ncols).
+// Outputs (device pointers, each optional): compact u32 entries, reference
+// CSC (rows64 / vals / colptr), stats[2] (u64 counters, accumulated).
+void generate_sparse_sign_dev(slq_ctx* ctx, int64_t d, int64_t zeta, uint64_t seed,
+                              int64_t col_begin, int64_t ncols, uint32_t* compact,
+                              int64_t* rows64, double* vals, int64_t* colptr,
+                              unsigned long long* stats);
+
+// K2: Y_aug = S [A b] for the rows of A (S keyed by global row id).  Writes
+// d x (n+1) column-major into Y (ldy = d).  exact => single split in the
+// reference's accumulation order.
+void sketch_apply_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed,
+                      bool exact, double* Y);
+
+// K2 for a caller CSC sketch already in compact form on the device
+// (colptr_dev int64, may be null for uniform zeta) against device A.
+void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32_t* compact,
+                              const int64_t* colptr_dev, int64_t zeta, double val, bool exact,
+                              double* Y);
+
+}  // namespace slq
