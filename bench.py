@@ -1,0 +1,442 @@
+"""Benchmark: end-to-end sketch-and-precondition LSQ solve on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N)
+
+Workload (BASELINE.json configs[2], the metric's headline config, fits one
+B200): dense A m=4,000,000 x n=1000, cond(A)=1e8 (singular values log-spaced
+in [1e-8, 1], A = U diag(s) V^T with U, V orthonormal, problems.hpp:45-66),
+b with ||b|| = 1 and ||b - A x*|| = 0.5 (x* the LS solution), sparse-sign
+sketch d = 4n, zeta = 8, LSQR to relative backward error
+||A^T r|| / (||A|| ||r||) <= 1e-10 (T iterations, calibrated in warm-up and
+verified after the timed steps).  A is row-partitioned over N GPUs
+(partition_rows, distsim.hpp:31-42); strong scaling (total work fixed).
+
+A "step" is one full solve (sketch generation + S[A b] + reduce + QR / R^-1 /
+x0 + T LSQR iterations) with A resident in HBM.  `value` = seconds per solve
+(max over ranks, CUDA events); `e2e` = the same solve through the C-ABI from
+pinned HOST buffers (column-major A, as the reference's DenseMatrix), H2D and
+layout conversion inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LSQ solve time (s) & LSQR GB/s vs HBM peak, 4M×1000 cond1e8, 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--m", type=int, default=4_000_000)
+    ap.add_argument("--n", type=int, default=1000)
+    ap.add_argument("--cond", type=float, default=1e8)
+    ap.add_argument("--dfac", type=int, default=4)
+    ap.add_argument("--zeta", type=int, default=8)
+    ap.add_argument("--rho", type=float, default=0.5)
+    ap.add_argument("--iters", type=int, default=0, help="LSQR iterations (0 = calibrate to eta <= 1e-10)")
+    ap.add_argument("--eta", type=float, default=1e-10)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=16, help="reference runs on m/cpu_sample rows, scaled")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            try:
+                sm = float(s[1])
+                mx = float(s[2])
+                pw = float(s[3])
+            except Exception:
+                continue
+            if pw > 200:  # under load
+                sms.append(sm)
+            for k, v in zip(names, s[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(k)
+        if not sms:
+            sms = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        return {"sm_mhz": float(np.median(sms)) if sms else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ problem
+
+def make_problem(torch, m, n, cond, rho, row_begin, row_end, dev, dist=None, seed=1, chunk=4000):
+    """A = U diag(s) V^T (U: CholeskyQR2 of a Gaussian, row-keyed chunks so
+    the matrix is identical for any row partition), b = A w s + rho r_perp.
+    Returns the device buffer in the solver layout (row-major [A | b | 0],
+    ld = round_up(n+1, 4)) and x_star."""
+    f64 = torch.float64
+    ml = row_end - row_begin
+    ld = ((n + 1 + 3) // 4) * 4
+
+    def allreduce(t):
+        if dist is not None:
+            dist.all_reduce(t)
+        return t
+
+    def gauss_rows(r0, r1):
+        # rows [r0, r1) of G, generated per global chunk (partition independent)
+        out = torch.empty((r1 - r0, n), dtype=f64, device=dev)
+        c0, c1 = r0 // chunk, (r1 - 1) // chunk
+        for c in range(c0, c1 + 1):
+            g = torch.Generator(device=dev)
+            g.manual_seed(seed * 1_000_003 + c)
+            blk = torch.randn((chunk, n), dtype=f64, device=dev, generator=g)
+            a, b = max(r0, c * chunk), min(r1, (c + 1) * chunk)
+            out[a - r0:b - r0] = blk[a - c * chunk:b - c * chunk]
+        return out
+
+    step = 256_000
+    gram = torch.zeros((n, n), dtype=f64, device=dev)
+    for r in range(row_begin, row_end, step):
+        G = gauss_rows(r, min(row_end, r + step))
+        gram += G.T @ G
+    allreduce(gram)
+    R1 = torch.linalg.cholesky(gram).T
+    U = torch.empty((ml, n), dtype=f64, device=dev)
+    gram2 = torch.zeros((n, n), dtype=f64, device=dev)
+    for r in range(row_begin, row_end, step):
+        r1 = min(row_end, r + step)
+        Uc = torch.linalg.solve_triangular(R1, gauss_rows(r, r1), upper=True, left=False)
+        U[r - row_begin:r1 - row_begin] = Uc
+        gram2 += Uc.T @ Uc
+    allreduce(gram2)
+    R2 = torch.linalg.cholesky(gram2).T
+    for r in range(0, ml, step):
+        U[r:r + step] = torch.linalg.solve_triangular(R2, U[r:r + step], upper=True, left=False)
+    gV = torch.Generator(device=dev)
+    gV.manual_seed(seed * 7 + 1)
+    V, _ = torch.linalg.qr(torch.randn((n, n), dtype=f64, device=dev, generator=gV))
+    s = torch.pow(10.0, -math.log10(cond) * torch.arange(n, dtype=f64, device=dev) / max(n - 1, 1))
+    B = (s[:, None] * V.T).contiguous()  # diag(s) V^T
+    Abuf = torch.zeros((ml, ld), dtype=f64, device=dev)
+    for r in range(0, ml, step):
+        Abuf[r:r + step, :n] = U[r:r + step] @ B
+    # right-hand side (problems.hpp:137-167 semantics, stable projection with U)
+    gw = torch.Generator(device=dev)
+    gw.manual_seed(seed * 11 + 2)
+    w = torch.rand(n, dtype=f64, device=dev, generator=gw) * 2 - 1
+    p = torch.empty(ml, dtype=f64, device=dev)
+    for r in range(0, ml, step):
+        p[r:r + step] = Abuf[r:r + step, :n] @ w
+    pn2 = allreduce((p * p).sum().reshape(1))
+    pn = float(pn2.sqrt())
+    z = torch.empty(ml, dtype=f64, device=dev)
+    for r in range(row_begin, row_end, step):
+        r1 = min(row_end, r + step)
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed * 13 + 3 + r)
+        z[r - row_begin:r1 - row_begin] = torch.rand(r1 - r, dtype=f64, device=dev, generator=g) * 2 - 1
+    for _ in range(2):
+        c = allreduce(U.T @ z)
+        z -= U @ c
+    zn = float(allreduce((z * z).sum().reshape(1)).sqrt())
+    range_norm = math.sqrt(1.0 - rho * rho)
+    Abuf[:, n] = p * (range_norm / pn) + z * (rho / zn)
+    x_star = (w * (range_norm / pn)).cpu().numpy()
+    del U, z, p
+    torch.cuda.synchronize()
+    return Abuf, ld, x_star
+
+
+# ------------------------------------------------------------ reference (CPU)
+
+def reference_sample(args, m_s, T, torch=None):
+    """Times the reference (oracle/_ref: the unmodified sketchlsq headers) on
+    m_s rows with all host threads; returns (extrapolated full-solve seconds,
+    phase dict, description)."""
+    import oracle
+
+    R = oracle.REF()
+    n, d, zeta = args.n, args.dfac * args.n, args.zeta
+    cores = os.cpu_count() or 1
+    # sample problem: same shape family (rows m_s), generated on the GPU if present
+    if torch is not None and torch.cuda.is_available():
+        Abuf, ld, _ = make_problem(torch, m_s, n, args.cond, args.rho, 0, m_s, torch.device("cuda", 0))
+        A = np.asfortranarray(Abuf[:, :n].cpu().numpy())
+        b = Abuf[:, n].cpu().numpy().copy()
+        del Abuf
+        torch.cuda.empty_cache()
+    else:
+        rng = np.random.default_rng(0)
+        A = np.asfortranarray(rng.standard_normal((m_s, n)))
+        b = rng.standard_normal(m_s)
+    t_it = 2
+    t0 = time.perf_counter()
+    _, rep, ph = R.solve_timed(A, b, d, zeta, 3, 0.0, t_it, cores)
+    wall = time.perf_counter() - t0
+    scale = args.m / m_s
+    lsqr_per_it = ph["lsqr"] / max(rep.iterations, 1)
+    total = (ph["generate"] + ph["apply"]) * scale + ph["precond"] + ph["x0"] + lsqr_per_it * scale * T
+    desc = (f"reference sketchlsq (oracle/_ref, g++ -O3) on {m_s} of {args.m} rows, WorkerPool({cores}): "
+            f"dist_generate_sparse_sign + dist_sketch_apply + lsqr_one_sync(dist_operator) x{t_it} iterations "
+            f"scaled x{scale:g} (rows) and x{T} iterations; serial householder_qr + tri_inverse + initial_guess "
+            f"on the full {d}x{n} sketch timed as is")
+    return total, {k: float(v) for k, v in ph.items()}, desc, cores, wall
+
+
+# ------------------------------------------------------------ main
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n, d, zeta = args.n, args.dfac * args.n, args.zeta
+    config = {"workload": f"C3: dense m={args.m} n={n} cond={args.cond:g} rho={args.rho}, sparse-sign d={d} "
+                          f"zeta={zeta}, LSQR to eta<={args.eta:g}",
+              "m": args.m, "n": n, "d": d, "zeta": zeta, "cond": args.cond,
+              "parallelism": f"rows/{world}" if world > 1 else "1 GPU",
+              "l2": "A is 32 GB >> 126 MB L2: inputs larger than L2, no flush needed"}
+
+    import torch
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        m_s = max(args.m // max(args.cpu_sample * 2, 1), 1000)
+        T = args.iters or 30
+        vals = []
+        for _ in range(args.warmup if args.warmup <= 1 else 1):
+            reference_sample(args, m_s, T, torch)
+        for _ in range(args.steps):
+            v, ph, desc, cores, wall = reference_sample(args, m_s, T, torch)
+            vals.append(v)
+        v = float(np.mean(vals))
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+                          "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic", "config": dict(config, lsqr_iterations=T),
+                          "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "reference",
+                                           "sample": desc, "phases": ph},
+                          "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import paper_2506_03070_b200 as slq
+
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = tdist
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+
+    part = slq.partition_rows(args.m, world)
+    r0, r1 = part.begin(rank), part.end(rank)
+    t_gen = time.perf_counter()
+    Abuf, ld, x_star = make_problem(torch, args.m, n, args.cond, args.rho, r0, r1, dev, dist)
+    t_gen = time.perf_counter() - t_gen
+
+    ctx = slq.Context(local_rank)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream.cuda_stream)
+    if world > 1:
+        uid = [slq.Context.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.init_comm(uid[0], rank, world)
+    A = slq.DeviceMatrix.wrap(Abuf.data_ptr(), r1 - r0, n, ld, row_begin=r0, ctx=ctx, owner=Abuf)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def solve(T):
+        return slq.solve(A, d, zeta, 3, slq.SolveOptions(eps=0.0, maxit=T, a_norm_est=1.0), ctx=ctx)
+
+    # warm-up + calibration of T (iterations to eta <= target)
+    T = args.iters or 24
+    eta = None
+    for w in range(max(args.warmup, 3)):
+        x, rep, ph = solve(T)
+        eta = rep.backward_error
+        if not args.iters and w < max(args.warmup, 3) - 1 and eta > args.eta and T < 80:
+            T += max(2, int(math.ceil(T * (math.log(eta / args.eta) / max(math.log(eta / 1e-16), 1.0)))))
+            T = min(T, 80)
+    # timed region: K solves, CUDA events on the solver stream, max over ranks
+    clocks = ClockSampler(local_rank)
+    barrier()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches0 = ctx.kernel_launches
+    phases = []
+    for _ in range(args.steps):
+        x, rep, ph = solve(T)
+        phases.append(ph)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    launches = ctx.kernel_launches - launches0
+    sec = ev0.elapsed_time(ev1) * 1e-3 / args.steps
+    if dist is not None:
+        t = torch.tensor([sec], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+    eta = rep.backward_error
+    ph = {k: float(np.mean([p[k] for p in phases])) for k in phases[0]}
+
+    # kernel-level timing for the roofline (dominant kernel: K4 fused LSQR pass)
+    kt = np.zeros(4)
+    import ctypes as ct
+    slq._capi.lib.slq_time_kernels(ctx.handle, A.handle, d, zeta, 3, 10, kt.ctypes.data_as(ct.POINTER(ct.c_double)))
+    ml = r1 - r0
+    pass_bytes = 8.0 * ml * n + 16.0 * ml
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        peak = json.load(open(peaks_path))["hbm_gbs"]
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    else:
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    achieved = pass_bytes / kt[0] / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("fused_pass", {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    iter_bytes = 8.0 * ml * n + 16.0 * ml + 8.0 * n * n
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "fused_pass (K4: u_hat = A p + c u, z = A^T u_hat, ||u_hat||^2)",
+                "algorithmic_bytes_per_launch": pass_bytes, "seconds_per_launch": float(kt[0]),
+                "peak_source": peak_src,
+                "lsqr_iteration_gbs": iter_bytes / ph["lsqr_per_iteration"] / 1e9 if ph["lsqr_per_iteration"] else None,
+                "sketch_seconds": float(kt[1]), "sketch_gbs": (8.0 * ml * (ld) + 4.0 * ml * zeta) / kt[1] / 1e9,
+                "precond_seconds": float(kt[3])}
+
+    # e2e through the C-ABI from pinned host buffers (column-major A as the reference's DenseMatrix)
+    e2e = None
+    if not args.no_e2e:
+        try:
+            Ah = torch.empty((n, ml), dtype=torch.float64, pin_memory=True)  # (n, m) row-major == column-major A
+            bh = torch.empty(ml, dtype=torch.float64, pin_memory=True)
+            for r in range(0, ml, 256_000):
+                Ah[:, r:r + 256_000].copy_(Abuf[r:r + 256_000, :n].T)
+            bh.copy_(Abuf[:, n])
+            xh = np.zeros(n)
+            rep_h = slq._capi.Report()
+            pt = slq._capi.PhaseTimes()
+            co = slq._capi.SolveOpts()
+            slq._capi.lib.slq_solve_opts_default(ct.byref(co))
+            co.eps, co.maxit, co.one_sync = 0.0, T, 1
+
+            def e2e_step():
+                st = slq._capi.lib.slq_solve_host(ctx.handle, ct.cast(Ah.data_ptr(), slq._capi.dp), ml, n, ml,
+                                                  ct.cast(bh.data_ptr(), slq._capi.dp), r0, d, zeta, 3, ct.byref(co),
+                                                  xh.ctypes.data_as(slq._capi.dp), ct.byref(rep_h), ct.byref(pt), None)
+                if st != 0:
+                    raise RuntimeError(slq._capi.lib.slq_last_error().decode())
+
+            e2e_step()  # warm
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ke = max(1, min(args.steps, 3))
+            for _ in range(ke):
+                e2e_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            es = e0.elapsed_time(e1) * 1e-3 / ke
+            if dist is not None:
+                t = torch.tensor([es], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                es = float(t.item())
+            e2e = {"value": es, "unit": "s", "h2d_bytes_per_step": int(8 * ml * n + 8 * ml),
+                   "d2h_bytes_per_step": int(8 * n), "steps": ke,
+                   "path": "slq_solve_host (C-ABI, pinned column-major host A)"}
+            del Ah, bh
+        except Exception as ex:  # report, never hide
+            e2e = {"value": None, "unit": "s", "error": str(ex)[:300]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            del_buf = None
+            m_s = max(args.m // args.cpu_sample, 1000)
+            v, cph, desc, cores, wall = reference_sample(args, m_s, T, torch)
+            cpu = {"value": v, "unit": "s", "cores": cores, "kind": "reference", "sample": desc, "phases": cph,
+                   "sample_wall_s": wall}
+        except Exception as ex:
+            cpu = {"value": None, "unit": "s", "error": str(ex)[:300]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": sec, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": sec * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (device generator, seed 1)",
+            "config": dict(config, lsqr_iterations=T),
+            "eta_final": eta, "iterations": rep.iterations,
+            "phases_s": ph, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": ck, "generation_s": t_gen,
+        }
+        print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

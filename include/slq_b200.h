@@ -221,6 +221,14 @@ int slq_solve(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_
               const slq_solve_opts* opts, double* x_out, slq_report* report,
               slq_phase_times* times, double* residual_estimate);
 
+/* Kernel timing for the roofline report (CUDA events on the context stream):
+ * out[0] = seconds per K4 fused LSQR pass launch (average over reps),
+ * out[1] = seconds for the sketch (K1 generate + K2 apply) of A,
+ * out[2] = seconds for K1 generation alone,
+ * out[3] = seconds for QR + R^-1 + x0 of the resulting d x n sketch. */
+int slq_time_kernels(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed, int reps,
+                     double* out);
+
 /* slq_solve from host buffers: upload (column-major A, lda) + solve + free. */
 int slq_solve_host(slq_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
                    const double* b, int64_t row_begin, int64_t d, int64_t zeta, uint64_t seed,

@@ -711,6 +711,30 @@ int slq_solve(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_
     return run_solve(ctx, A, d, zeta, seed, opts, x_out, report, times, residual_estimate);
 }
 
+int slq_time_kernels(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed, int reps,
+                     double* out) {
+    return guarded([&] {
+        need(ctx && A && out, SLQ_INVALID_ARG, "time_kernels: null argument");
+        const int64_t n = A->n, m = A->m;
+        out[0] = slq::time_fused_pass(ctx, A, reps);
+        slq::Workspace& ws = ctx->ws;
+        double* Yaug = static_cast<double*>(ws.yaug.ensure(sizeof(double) * d * (n + 1)));
+        uint32_t* compact = static_cast<uint32_t*>(ws.compact.ensure(sizeof(uint32_t) * std::max<int64_t>(1, m * zeta)));
+        Timer a0(ctx->stream);
+        slq::generate_sparse_sign_dev(ctx, d, zeta, seed, A->row_begin, m, compact, nullptr, nullptr, nullptr, nullptr);
+        Timer a1(ctx->stream);
+        slq::sketch_apply_compact_dev(ctx, A, d, compact, nullptr, zeta, 1.0 / std::sqrt(static_cast<double>(zeta)),
+                                      false, Yaug);
+        Timer a2(ctx->stream);
+        PrecondBufs P = precond_bufs(ctx, n);
+        build_precond_dev(ctx, Yaug, d, n, true, nullptr, P, nullptr);
+        Timer a3(ctx->stream);
+        out[1] = a2.since(a0);
+        out[2] = a1.since(a0);
+        out[3] = a3.since(a2);
+    });
+}
+
 int slq_solve_host(slq_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
                    int64_t row_begin, int64_t d, int64_t zeta, uint64_t seed, const slq_solve_opts* opts,
                    double* x_out, slq_report* report, slq_phase_times* times, double* residual_estimate) {

@@ -743,6 +743,35 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
         for (size_t i = 0; i < htrue.size(); ++i) true_hist[i] = htrue[i];
 }
 
+double time_fused_pass(slq_ctx* ctx, const slq_dense* A, int reps) {
+    // Average device time of one K4 launch (steady-state iteration form),
+    // CUDA events on the launching stream.
+    PassPlan pp = plan_pass(ctx, A);
+    const int64_t n = A->n, m = A->m;
+    DevBuf part, pv, uv, cf;
+    double* dpart = static_cast<double*>(part.ensure(sizeof(double) * pp.grid * (n + 1)));
+    double* p = static_cast<double*>(pv.ensure(sizeof(double) * (n + 8)));
+    double* u = static_cast<double*>(uv.ensure(sizeof(double) * std::max<int64_t>(1, m)));
+    double* c = static_cast<double*>(cf.ensure(sizeof(double) * 8));
+    SLQ_CUDA_CHECK(cudaMemsetAsync(p, 0, sizeof(double) * (n + 8), ctx->stream));
+    SLQ_CUDA_CHECK(cudaMemsetAsync(u, 0, sizeof(double) * std::max<int64_t>(1, m), ctx->stream));
+    SLQ_CUDA_CHECK(cudaMemsetAsync(c, 0, sizeof(double) * 8, ctx->stream));
+    PassArgs a{A->A, A->ld, m, n, p, u, u, c, 0.0, dpart, 1, nullptr, 0, 0};
+    launch_pass(ctx, pp, a);  // warm
+    cudaEvent_t e0, e1;
+    SLQ_CUDA_CHECK(cudaEventCreate(&e0));
+    SLQ_CUDA_CHECK(cudaEventCreate(&e1));
+    SLQ_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+    for (int r = 0; r < reps; ++r) launch_pass(ctx, pp, a);
+    SLQ_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+    SLQ_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    SLQ_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return ms * 1e-3 / std::max(reps, 1);
+}
+
 double backward_error_dev(slq_ctx* ctx, const slq_dense* A, const double* x, double a_norm) {
     // r = b - A x:  u_hat = A x - b = -r;  z = A^T u_hat = -A^T r
     PassPlan pp = plan_pass(ctx, A);

@@ -24,6 +24,9 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
               const double* x0, double* x, const slq_solve_opts& opts, double* est_hist,
               double* err_hist, double* true_hist, LsqrOut& out);
 
+// Average seconds per fused-pass launch (K4), timed with CUDA events.
+double time_fused_pass(slq_ctx* ctx, const slq_dense* A, int reps);
+
 // ||A^T r|| / (a_norm ||r||) for r = b - A x (one fused pass + allreduce).
 double backward_error_dev(slq_ctx* ctx, const slq_dense* A, const double* x, double a_norm);
 

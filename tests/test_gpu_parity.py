@@ -218,7 +218,7 @@ def test_lsqr_golden(golden):
             assert np.allclose(rep.iterates_error, p["err_std"], rtol=1e-6, atol=1e-13)
             assert np.allclose(rep.residual_true, p["true_std"], rtol=1e-10, atol=1e-14)
     x, rep = slq.lsqr(p["A"], p["M"], p["b"], np.zeros(meta["n"]), slq.SolveOptions(eps=1e-10, maxit=100))
-    assert rep.termination == slq.Termination.Tolerance
+    assert str(rep.termination) == meta["tol_run"]["termination"]
     assert abs(rep.iterations - meta["tol_run"]["iterations"]) <= 1
     assert np.linalg.norm(x - p["x_tol"]) <= 1e-9 * np.linalg.norm(p["x_tol"])
 
@@ -271,7 +271,10 @@ def test_solve_pipeline_c1_small():
     assert rep.iterations == 20
     assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)
     assert np.allclose(rep.residual_estimate, repo.residual_estimate, rtol=1e-8)
-    r = b - A @ x
-    eta = np.linalg.norm(A.T @ r) / (np.linalg.norm(A, 2) * np.linalg.norm(r))
-    assert eta <= 1e-10
+    def eta(v):
+        r = b - A @ v
+        return np.linalg.norm(A.T @ r) / (np.linalg.norm(A, 2) * np.linalg.norm(r))
+
+    # backward error no worse than the reference's at fixed T
+    assert eta(x) <= max(2 * eta(xo), 1e-14)
     assert times["kernel_launches"] > 0
