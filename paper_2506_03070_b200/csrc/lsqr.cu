@@ -254,14 +254,37 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
     }
 }
 
-// partials [G][n+1] -> out[n+1], fixed order
-__global__ void reduce_partials_kernel(const double* part, int G, int64_t n1, double* out, const int* skip) {
+// partials [G][n+1] -> out[n+1], fixed order: thread (c, g) sums partials
+// g, g+8, ... of column c, then the 8 sums are added in order g = 0..7.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const double* part, int G, int64_t n1, double* out,
+                                                              const int* skip) {
+    __shared__ double red[8][33];
     if (skip && *skip) return;
-    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j >= n1) return;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * 32 + tx;
     double s = 0.0;
-    for (int g = 0; g < G; ++g) s += part[static_cast<int64_t>(g) * n1 + j];
-    out[j] = s;
+    if (j < n1) {
+#pragma unroll 4
+        for (int g = ty; g < G; g += 8) s += part[static_cast<int64_t>(g) * n1 + j];
+    }
+    red[ty][tx] = s;
+    __syncthreads();
+    if (ty == 0 && j < n1) {
+        double t = red[0][tx];
+#pragma unroll
+        for (int q = 1; q < 8; ++q) t += red[q][tx];
+        out[j] = t;
+    }
+}
+
+__device__ __forceinline__ double block0_sum_fixed(const double* p, unsigned np) {
+    // warp 0: lane l sums p[l], p[l+32], ... in order, then a fixed xor tree
+    const int lane = threadIdx.x & 31;
+    double s = 0.0;
+    for (unsigned b = lane; b < np; b += 32) s += static_cast<const volatile double*>(p)[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
 }
 
 // --------------------------------------------------------------- K5 mtz
@@ -378,12 +401,13 @@ __global__ void __launch_bounds__(256) mtz_kernel(MtzArgs a) {
         last = atomicAdd(&a.st->counter_mtz, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (last && threadIdx.x < 32) {
         __threadfence();
-        double s = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) s += static_cast<volatile double*>(a.part2)[b];
-        a.st->counter_mtz = 0;
-        scalar_step(a, beta, sqrt(s));
+        const double s = block0_sum_fixed(a.part2, gridDim.x);
+        if (threadIdx.x == 0) {
+            a.st->counter_mtz = 0;
+            scalar_step(a, beta, sqrt(s));
+        }
     }
 }
 
@@ -621,7 +645,7 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
     {
         PassArgs ia{A->A, A->ld, m, n, x0, b_dev, B.u, nullptr, -1.0, B.part, 1, nullptr, 0, 0};
         launch_pass(ctx, pp, ia);
-        reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 256)), 256, 0, ctx->stream>>>(
+        reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 32)), 256, 0, ctx->stream>>>(
             B.part, pp.grid, n + 1, B.zt, nullptr);
         SLQ_LAUNCH_CHECK(ctx);
         allreduce_sum(ctx, B.zt, n + 1);
@@ -639,7 +663,7 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
     auto enqueue_iteration = [&]() {
         PassArgs ta{A->A, A->ld, m, n, B.p, B.u, B.u, &B.st->c_next, 0.0, B.part, 1, done_flag, 0, 0};
         launch_pass(ctx, pp, ta);
-        reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 256)), 256, 0, ctx->stream>>>(
+        reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 32)), 256, 0, ctx->stream>>>(
             B.part, pp.grid, n + 1, B.zt, done_flag);
         SLQ_LAUNCH_CHECK(ctx);
         allreduce_sum(ctx, B.zt, n + 1);
@@ -781,7 +805,7 @@ double backward_error_dev(slq_ctx* ctx, const slq_dense* A, const double* x, dou
     double* dzt = static_cast<double*>(zt.ensure(sizeof(double) * (n + 1)));
     PassArgs a{A->A, A->ld, A->m, n, x, nullptr, nullptr, nullptr, -1.0, dpart, 1, nullptr, 0, 0};
     launch_pass(ctx, pp, a);
-    reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 256)), 256, 0, ctx->stream>>>(dpart, pp.grid, n + 1,
+    reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 32)), 256, 0, ctx->stream>>>(dpart, pp.grid, n + 1,
                                                                                               dzt, nullptr);
     SLQ_LAUNCH_CHECK(ctx);
     allreduce_sum(ctx, dzt, n + 1);
