@@ -26,7 +26,7 @@ int main() {
     Vector x0 = initial_guess(P, sketch_vector(S, b));
     SolveOptions opts;
     opts.eps = 0.0;
-    opts.maxit = 20;
+    opts.maxit = 40;
     auto [x, rep] = lsqr(A, P, b, x0, opts);
 
     // backward error ||A^T r|| / (||A||_F ||r||) on the host

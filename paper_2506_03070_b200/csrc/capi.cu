@@ -6,6 +6,8 @@
 // types (errors.hpp:9-76).
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -225,11 +227,21 @@ int run_solve(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_
         uint32_t* compact = static_cast<uint32_t*>(ws.compact.ensure(sizeof(uint32_t) * std::max<int64_t>(1, m * zeta)));
         int64_t* work = zeta > 32 ? static_cast<int64_t*>(ws.tmp.ensure(sizeof(int64_t) * m * zeta)) : nullptr;
 
+        // SLQ_TRACE=1: host timestamps per phase on stderr (diagnostics)
+        static const bool trace = std::getenv("SLQ_TRACE") != nullptr;
+        const auto h0 = std::chrono::steady_clock::now();
+        auto mark = [&](const char* what) {
+            if (trace)
+                std::fprintf(stderr, "[slq] %-10s host %.3f ms\n", what,
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+        };
         Timer t0(ctx->stream);
         slq::generate_sparse_sign_dev(ctx, d, zeta, seed, A->row_begin, m, compact, work, nullptr, nullptr, nullptr);
+        mark("generate");
         Timer t1(ctx->stream);
         slq::sketch_apply_compact_dev(ctx, A, d, compact, nullptr, zeta, 1.0 / std::sqrt(static_cast<double>(zeta)),
                                       false, Yaug);
+        mark("apply");
         Timer t2(ctx->stream);
         slq::reduce_sum_root(ctx, Yaug, d * (n + 1));
         Timer t3(ctx->stream);
@@ -261,15 +273,18 @@ int run_solve(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_
             slq::broadcast_root(ctx, P.Mt, n * n);
             slq::broadcast_root(ctx, P.x0, n);
         }
+        mark("precond");
         Timer t5(ctx->stream);
-        double* x = static_cast<double*>(ws.qr_w.ensure(sizeof(double) * (n + 8)));
+        double* x = static_cast<double*>(ws.xbuf.ensure(sizeof(double) * (n + 8)));
         slq::LsqrOut lo;
         slq::lsqr_dev(ctx, A, nullptr, P.M, P.Mt, P.x0, x, opts, est, nullptr, nullptr, lo);
+        mark("lsqr");
         Timer t6(ctx->stream);
         if (opts.backward_tol > 0.0 || opts.a_norm_est > 0.0)
             lo.backward_error = slq::backward_error_dev(ctx, A, x, opts.a_norm_est > 0.0 ? opts.a_norm_est : 1.0);
         if (x_out) SLQ_CUDA_CHECK(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
         fill_report(report, lo);
+        mark("finish");
         if (times) {
             times->generate = t1.since(t0);
             times->apply = t2.since(t1);
@@ -324,6 +339,7 @@ int slq_ctx_destroy(slq_ctx* ctx) {
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         slq::comm_destroy(ctx);
+        if (ctx->lsqr_exec) cudaGraphExecDestroy(ctx->lsqr_exec);
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -333,6 +349,9 @@ int slq_ctx_set_stream(slq_ctx* ctx, void* s) {
     return guarded([&] {
         need(ctx != nullptr, SLQ_INVALID_ARG, "null ctx");
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        if (ctx->lsqr_exec) cudaGraphExecDestroy(ctx->lsqr_exec);
+        ctx->lsqr_exec = nullptr;
+        ctx->lsqr_key.clear();
         ctx->stream = static_cast<cudaStream_t>(s);
         ctx->own_stream = false;
     });

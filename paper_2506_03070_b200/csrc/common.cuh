@@ -75,6 +75,7 @@ struct Workspace {
     DevBuf qr_t, qr_w, qr_q, qr_misc;
     DevBuf lsqr_vec, lsqr_part, lsqr_state, lsqr_u;
     DevBuf mats;         // M, Mt
+    DevBuf xbuf;         // solution vector
     DevBuf tmp;
 };
 
@@ -93,6 +94,9 @@ struct slq_ctx {
     int rank = 0;
     int nranks = 1;
     int64_t nccl_calls = 0;
+    // cached LSQR iteration graph (rebuilt when any captured pointer / size changes)
+    cudaGraphExec_t lsqr_exec = nullptr;
+    std::vector<uint64_t> lsqr_key;
 };
 
 struct slq_dense {

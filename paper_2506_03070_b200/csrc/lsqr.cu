@@ -264,8 +264,14 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const double* part
     const int64_t j = static_cast<int64_t>(blockIdx.x) * 32 + tx;
     double s = 0.0;
     if (j < n1) {
-#pragma unroll 4
-        for (int g = ty; g < G; g += 8) s += part[static_cast<int64_t>(g) * n1 + j];
+        double acc[4] = {0, 0, 0, 0};
+        int g = ty;
+        for (; g + 24 < G; g += 32) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] += part[static_cast<int64_t>(g + 8 * u) * n1 + j];
+        }
+        for (int u = 0; g < G; g += 8, ++u) acc[u & 3] += part[static_cast<int64_t>(g) * n1 + j];
+        s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     }
     red[ty][tx] = s;
     __syncthreads();
@@ -285,6 +291,21 @@ __device__ __forceinline__ double block0_sum_fixed(const double* p, unsigned np)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     return s;
+}
+
+// Warp dot product over [b, e) with stride 32 per lane: 8 independent
+// accumulators keep 8 loads in flight per lane (the naive loop is one L2
+// round trip per 32 elements); combined in a fixed order (deterministic).
+template <class F>
+__device__ __forceinline__ double lane_dot(int64_t b, int64_t e, int lane, F term) {
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t i = b + lane;
+    for (; i + 7 * 32 < e; i += 8 * 32) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] += term(i + 32 * u);
+    }
+    for (int u = 0; i < e; i += 32, ++u) acc[u & 7] += term(i);
+    return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
 }
 
 // --------------------------------------------------------------- K5 mtz
@@ -386,7 +407,7 @@ __global__ void __launch_bounds__(256) mtz_kernel(MtzArgs a) {
     if (j < a.n) {
         const double* col = a.M + j * a.n;
         double s = 0.0;
-        for (int64_t i = lane; i <= j; i += 32) s = fma(col[i], a.zt[i] * zs, s);
+        s = lane_dot(0, j + 1, lane, [&](int64_t i) { return col[i] * (a.zt[i] * zs); });
         s = warp_sum(s);
         vh = a.init ? s : __dadd_rn(s, __dmul_rn(-beta, a.v[j]));  // lsqr.hpp:137
         if (lane == 0) a.vhat[j] = vh;
@@ -437,7 +458,7 @@ __global__ void __launch_bounds__(256) mv_update_kernel(MvArgs a) {
             const double inv_alpha = 1.0 / a.st->alpha;  // lsqr.hpp:141 scal(1/alpha, v_hat)
             const double* row = a.Mt + i * a.n;
             double s = 0.0;
-            for (int64_t j = i + lane; j < a.n; j += 32) s = fma(row[j], a.vhat[j] * inv_alpha, s);
+            s = lane_dot(i, a.n, lane, [&](int64_t j) { return row[j] * (a.vhat[j] * inv_alpha); });
             s = warp_sum(s);
             if (lane == 0) {
                 a.v[i] = a.vhat[i] * inv_alpha;
@@ -701,15 +722,29 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
         }
     } else if (maxit > 0) {
         constexpr int kBatch = 8;
-        cudaGraph_t graph = nullptr;
-        cudaGraphExec_t exec = nullptr;
         const bool use_graph = ctx->stream != nullptr;
         if (use_graph) {
-            SLQ_CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-            for (int b = 0; b < kBatch; ++b) enqueue_iteration();
-            SLQ_CUDA_CHECK(cudaStreamEndCapture(ctx->stream, &graph));
-            SLQ_CUDA_CHECK(cudaGraphInstantiate(&exec, graph, 0));
+            const std::vector<uint64_t> key = {
+                reinterpret_cast<uint64_t>(A->A), static_cast<uint64_t>(m), static_cast<uint64_t>(n),
+                static_cast<uint64_t>(A->ld), reinterpret_cast<uint64_t>(b_dev), reinterpret_cast<uint64_t>(M),
+                reinterpret_cast<uint64_t>(Mt), reinterpret_cast<uint64_t>(x), reinterpret_cast<uint64_t>(B.u),
+                reinterpret_cast<uint64_t>(B.p), reinterpret_cast<uint64_t>(B.part), reinterpret_cast<uint64_t>(B.st),
+                reinterpret_cast<uint64_t>(B.hist), static_cast<uint64_t>(pp.grid), static_cast<uint64_t>(pp.R),
+                static_cast<uint64_t>(pp.S), reinterpret_cast<uint64_t>(ctx->comm), reinterpret_cast<uint64_t>(ctx->stream)};
+            if (!ctx->lsqr_exec || ctx->lsqr_key != key) {
+                if (ctx->lsqr_exec) cudaGraphExecDestroy(ctx->lsqr_exec);
+                ctx->lsqr_exec = nullptr;
+                cudaGraph_t graph = nullptr;
+                SLQ_CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+                for (int b = 0; b < kBatch; ++b) enqueue_iteration();
+                SLQ_CUDA_CHECK(cudaStreamEndCapture(ctx->stream, &graph));
+                SLQ_CUDA_CHECK(cudaGraphInstantiate(&ctx->lsqr_exec, graph, 0));
+                cudaGraphDestroy(graph);
+                ctx->lsqr_key = key;
+                ctx->launches -= 4 * kBatch;  // captured, not launched
+            }
         }
+        cudaGraphExec_t exec = use_graph ? ctx->lsqr_exec : nullptr;
         int* hdone = nullptr;
         SLQ_CUDA_CHECK(cudaMallocHost(&hdone, 2 * sizeof(int)));
         hdone[0] = hdone[1] = 0;
@@ -738,8 +773,6 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
         cudaEventDestroy(ev[0]);
         cudaEventDestroy(ev[1]);
         cudaFreeHost(hdone);
-        if (exec) cudaGraphExecDestroy(exec);
-        if (graph) cudaGraphDestroy(graph);
     }
     SLQ_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
     SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, B.st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));

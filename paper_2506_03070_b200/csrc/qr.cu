@@ -32,7 +32,7 @@ namespace slq {
 
 namespace {
 
-constexpr int kPanelThreads = 256;
+constexpr int kPanelThreads = 512;
 constexpr int kNbMax = 32;
 constexpr int kWs = kNbMax + 1;  // padded row stride of the panel slice (bank-conflict free columns)
 
@@ -75,32 +75,73 @@ struct PanelArgs {
     int* err;          // 0 or 1 + failing column
 };
 
-// Cluster-wide sum of L <= 33 doubles.  Each CTA writes its partial into
-// slot[parity]; after cluster.sync every CTA sums all ranks in rank order.
-// A slot is rewritten two reductions later, after another cluster.sync,
-// so no CTA can still be reading it.
-__device__ __forceinline__ void cluster_sum(cg::cluster_group& cl, double (*slot)[40], int parity, int L,
-                                            double* out) {
-    cl.sync();
-    const unsigned nr = cl.num_blocks();
+// Point-to-point cluster reduction: warp 0 of every CTA pushes its L partials
+// into slot [me] of every CTA's inbox (DSMEM stores) and arrives (release,
+// cluster scope) on that CTA's mbarrier; each CTA then waits on its own
+// mbarrier (acquire) and sums the inbox in rank order -- one DSMEM hop instead
+// of a full cluster barrier.  inbox / mbar double-buffered by reduction parity:
+// a CTA can only rewrite an inbox two reductions later, after every CTA has
+// arrived for the reduction in between, i.e. after it finished reading.
+__device__ __forceinline__ void push_reduce(cg::cluster_group& cl, double (*inbox)[16][33], uint64_t* mbar, int r,
+                                            int L, const double* mine, double* out) {
+    const int p = r & 1;
+    const unsigned phase = static_cast<unsigned>((r >> 1) & 1);
+    const unsigned me = cl.block_rank(), nr = cl.num_blocks();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        if (lane < L) {
+            const double v = mine[lane];
+            for (unsigned q = 0; q < nr; ++q) *cl.map_shared_rank(&inbox[p][me][lane], q) = v;
+        }
+        asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
+        __syncwarp();
+        if (lane < static_cast<int>(nr)) {
+            const unsigned local = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[p]));
+            unsigned remote;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local), "r"(static_cast<unsigned>(lane)));
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
+        }
+    }
+    {
+        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[p]));
+        unsigned ok = 0;
+        do {
+            asm volatile(
+                "{\n .reg .pred P;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n"
+                " selp.u32 %0, 1, 0, P;\n}\n"
+                : "=r"(ok)
+                : "r"(a), "r"(phase)
+                : "memory");
+        } while (!ok);
+    }
     if (threadIdx.x < static_cast<unsigned>(L)) {
         double s = 0.0;
-        for (unsigned r = 0; r < nr; ++r) {
-            const double* remote = cl.map_shared_rank(&slot[parity][0], r);
-            s += remote[threadIdx.x];
-        }
+        for (unsigned q = 0; q < nr; ++q) s += inbox[p][q][threadIdx.x];
         out[threadIdx.x] = s;
     }
     __syncthreads();
 }
 
 __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
+    constexpr int kWarps = kPanelThreads / 32;
     extern __shared__ __align__(16) double w[];  // [rpc][kWs] row-major panel slice
     __shared__ double slot[2][40];
-    __shared__ double red[8][33];
+    __shared__ double red[kWarps][33];
     __shared__ double tot[40];
     __shared__ double Ts[kNbMax][kNbMax + 1];
+    __shared__ double inbox[2][16][33];
+    __shared__ uint64_t mbar[2];
     cg::cluster_group cl = cg::this_cluster();
+    if (threadIdx.x == 0) {
+        const unsigned nrk = cl.num_blocks();
+        for (int q = 0; q < 2; ++q) {
+            const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[q]));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(nrk) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    cl.sync();  // every CTA's mbarriers exist before anyone arrives remotely
+    int nred = 0;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned rank = cl.block_rank();
     const int kb = a.kb;
@@ -116,28 +157,34 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
     const double rank_tol = *a.rank_tol;
     int parity = 0;
 
+    // partial sigma of column 0 (rows > k0); lane 0 of each warp accumulates it
+    double sig = 0.0;
+    {
+        const int64_t ib0 = (a.k0 - row0 + 1 > 0) ? a.k0 - row0 + 1 : 0;
+        for (int64_t il = ib0 + tid; il < nrows; il += kPanelThreads) {
+            const double v = w[il * kWs];
+            sig += v * v;
+        }
+        for (int o = 16; o > 0; o >>= 1) sig += __shfl_xor_sync(0xffffffffu, sig, o);
+    }
+
     for (int kk = 0; kk < kb; ++kk) {
         const int64_t gk = a.k0 + kk;           // global diagonal row
         const int64_t lk = gk - row0;           // local index of row gk (may be outside)
         const bool owner = lk >= 0 && lk < nrows;
         const int64_t ib = lk + 1 > 0 ? lk + 1 : 0;  // first local row strictly below gk
 
-        // (a) sigma = sum_{i>gk} w_ik^2, and x0 = w[gk][kk]
-        double s = 0.0;
-        for (int64_t il = ib + tid; il < nrows; il += kPanelThreads) {
-            const double v = w[il * kWs + kk];
-            s += v * v;
-        }
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) red[wid][0] = s;
+        // (a) sigma = sum_{i>gk} w_ik^2 (accumulated by the previous update), x0 = w[gk][kk]
+        if (lane == 0) red[wid][0] = sig;
         __syncthreads();
         if (tid == 0) {
             double t = 0.0;
-            for (int q = 0; q < 8; ++q) t += red[q][0];
+            for (int q = 0; q < kWarps; ++q) t += red[q][0];
             slot[parity][0] = t;
             slot[parity][1] = owner ? w[lk * kWs + kk] : 0.0;
         }
-        cluster_sum(cl, slot, parity, 2, tot);
+        __syncthreads();
+        push_reduce(cl, inbox, mbar, nred++, 2, slot[parity], tot);
         parity ^= 1;
         const double sigma = tot[0], x0 = tot[1];
         const double normx = sqrt(x0 * x0 + sigma);
@@ -154,33 +201,40 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
         __syncthreads();
         if (owner && tid == 0) w[lk * kWs + kk] = beta;
 
-        // (c) dots for every other panel column jj:
-        //     g_jj = w[gk][jj] + sum_{i>gk} w[i][jj] * v_i
+        // (c) g_jj = w[gk][jj] + sum_{i>gk} w[i][jj] v_i for every other panel column:
         //     jj > kk: the reference's s_j (qr.hpp:51-53); jj < kk: v_jj^T v_kk (for T)
         {
-            const int jj = lane;
             double acc = 0.0;
-            if (jj < kb)
-                for (int64_t il = ib + wid; il < nrows; il += 8) acc += w[il * kWs + jj] * w[il * kWs + kk];
-            red[wid][jj] = acc;
+            if (lane < kb)
+                for (int64_t il = ib + wid; il < nrows; il += kWarps) acc += w[il * kWs + lane] * w[il * kWs + kk];
+            red[wid][lane] = acc;
             __syncthreads();
             if (tid < 32) {
                 double t = 0.0;
-                for (int q = 0; q < 8; ++q) t += red[q][tid];
+                for (int q = 0; q < kWarps; ++q) t += red[q][tid];
                 if (owner && tid < kb && tid != kk) t += w[lk * kWs + tid];
                 slot[parity][tid] = t;
             }
         }
-        cluster_sum(cl, slot, parity, kb, tot);
+        __syncthreads();
+        push_reduce(cl, inbox, mbar, nred++, kb, slot[parity], tot);
         parity ^= 1;
-        // (d) apply H_kk to the remaining panel columns
+        // (d) apply H_kk to the remaining panel columns; lane kk+1 also sums the
+        //     squares of its updated entries below the next diagonal (next sigma)
+        sig = 0.0;
         {
             const int jj = lane;
+            const int64_t lk1 = lk + 1;  // local index of the next diagonal row
             if (jj > kk && jj < kb) {
                 const double sj = tot[jj] * tau;
-                for (int64_t il = ib + wid; il < nrows; il += 8) w[il * kWs + jj] -= sj * w[il * kWs + kk];
+                for (int64_t il = ib + wid; il < nrows; il += kWarps) {
+                    const double nv = w[il * kWs + jj] - sj * w[il * kWs + kk];
+                    w[il * kWs + jj] = nv;
+                    if (jj == kk + 1 && il != lk1) sig += nv * nv;
+                }
                 if (owner && wid == 0) w[lk * kWs + jj] -= sj;
             }
+            sig = __shfl_sync(0xffffffffu, sig, (kk + 1) & 31);
         }
         // compact-WY: T[0:kk, kk] = -tau T[0:kk, 0:kk] (V^T v_kk);  T[kk][kk] = tau
         if (rank == 0) {
@@ -239,88 +293,121 @@ __device__ __forceinline__ double vget(const UpdArgs& u, int64_t r, int a) {
     return u.V[(u.k0 + a) * u.ldv + r];
 }
 
-constexpr int kUpdCols = 16;
+// Tiles of the trailing update: RB rows x CB columns per CTA.  Two kernels
+// per panel: U1 forms per-row-block partials of W = V^T C, U2 sums them (fixed
+// order), applies T (or T^T) and updates its tile C -= V W2.  V and C tiles are
+// staged in shared memory (coalesced column loads) and multiplied with DMMA.
+constexpr int kRB = 128;
+constexpr int kCB = 32;
+constexpr int kLdT = kRB + 4;  // smem leading dimension (doubles): conflict-free fragments
 
-__global__ void __launch_bounds__(256) update_kernel(UpdArgs u) {
-    __shared__ double Wred[8][kNbMax][kUpdCols + 1];
-    __shared__ double W[kNbMax][kUpdCols + 1];
-    __shared__ double W2[kNbMax][kUpdCols + 1];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int64_t cb = u.c_begin + static_cast<int64_t>(blockIdx.x) * kUpdCols;
+// Stage V rows [r0, r0+kRB) (implicit unit diagonal / zero upper part) as Vs[a][i]
+__device__ __forceinline__ void stage_v(const UpdArgs& u, int64_t r0, double* Vs) {
+    for (int e = threadIdx.x; e < kNbMax * kRB; e += blockDim.x) {
+        const int a = e / kRB, i = e % kRB;
+        Vs[a * kLdT + i] = vget(u, r0 + i, a);
+    }
+}
+
+// Stage C rows [r0, r0+kRB) x columns [c0, c0+kCB) as Cs[c][i]
+__device__ __forceinline__ void stage_c(const UpdArgs& u, int64_t r0, int64_t c0, double* Cs) {
+    for (int e = threadIdx.x; e < kCB * kRB; e += blockDim.x) {
+        const int c = e / kRB, i = e % kRB;
+        const int64_t r = r0 + i, cc = c0 + c;
+        Cs[c * kLdT + i] = (r < u.r_end && cc < u.c_end) ? u.C[cc * u.ldc + r] : 0.0;
+    }
+}
+
+// U1: Wpart[rb][cb] = V_rb^T C_rb  (kNbMax x kCB)
+__global__ void __launch_bounds__(256) update_w_kernel(UpdArgs u, double* Wpart) {
+    extern __shared__ __align__(16) double sm[];
+    double* Vs = sm;
+    double* Cs = sm + kNbMax * kLdT;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int lr = lane & 3, lg = lane >> 2;
+    const int64_t r0 = u.k0 + static_cast<int64_t>(blockIdx.y) * kRB;
+    const int64_t c0 = u.c_begin + static_cast<int64_t>(blockIdx.x) * kCB;
+    stage_v(u, r0, Vs);
+    stage_c(u, r0, c0, Cs);
+    __syncthreads();
+    // 16 output tiles (4 along a, 4 along c); warp w owns tiles 2w, 2w+1
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    const int t0 = 2 * warp;
+    const int at = t0 >> 2;  // both tiles share the a-tile
+    const int ct0 = t0 & 3, ct1 = ct0 + 1;
+#pragma unroll 8
+    for (int ks = 0; ks < kRB / 4; ++ks) {
+        const int i = ks * 4 + lr;
+        const double af = Vs[(at * 8 + lg) * kLdT + i];
+        const double b0 = Cs[(ct0 * 8 + lg) * kLdT + i];
+        const double b1 = Cs[(ct1 * 8 + lg) * kLdT + i];
+        dmma(acc[0][0], acc[0][1], af, b0);
+        dmma(acc[1][0], acc[1][1], af, b1);
+    }
+    double* W = Wpart + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * (kNbMax * kCB);
+    const int a = at * 8 + lg;
+    W[a * kCB + ct0 * 8 + 2 * lr] = acc[0][0];
+    W[a * kCB + ct0 * 8 + 2 * lr + 1] = acc[0][1];
+    W[a * kCB + ct1 * 8 + 2 * lr] = acc[1][0];
+    W[a * kCB + ct1 * 8 + 2 * lr + 1] = acc[1][1];
+}
 
-    // step 1: W = V^T C  (kNbMax x 16), rows split over warps in k-steps of 4
-    double acc[4][2][2];
-#pragma unroll
-    for (int at = 0; at < 4; ++at)
-#pragma unroll
-        for (int ct = 0; ct < 2; ++ct) acc[at][ct][0] = acc[at][ct][1] = 0.0;
-    const int64_t nrow = u.r_end - u.k0;
-    const int64_t nks = (nrow + 3) / 4;
-    for (int64_t ks = wid; ks < nks; ks += 8) {
-        const int64_t r = u.k0 + ks * 4 + lr;
-        double bf[2];
-#pragma unroll
-        for (int ct = 0; ct < 2; ++ct) {
-            const int64_t c = cb + ct * 8 + lg;
-            bf[ct] = (r < u.r_end && c < u.c_end) ? u.C[c * u.ldc + r] : 0.0;
-        }
-#pragma unroll
-        for (int at = 0; at < 4; ++at) {
-            const double af = vget(u, r, at * 8 + lg);
-#pragma unroll
-            for (int ct = 0; ct < 2; ++ct) dmma(acc[at][ct][0], acc[at][ct][1], af, bf[ct]);
-        }
+// U2: W = sum_rb Wpart[rb][cb];  W2 = T^T W (or T W);  C_rb -= V_rb W2
+__global__ void __launch_bounds__(256) update_apply_kernel(UpdArgs u, const double* Wpart) {
+    extern __shared__ __align__(16) double sm[];
+    double* Vs = sm;
+    double* Cs = sm + kNbMax * kLdT;
+    double* W = Cs + kCB * kLdT;             // [kNbMax][kCB + 1]
+    double* W2 = W + kNbMax * (kCB + 1);     // [kNbMax][kCB + 1]
+    double* Ts = W2 + kNbMax * (kCB + 1);    // [kNbMax][kNbMax + 1]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lr = lane & 3, lg = lane >> 2;
+    const int64_t r0 = u.k0 + static_cast<int64_t>(blockIdx.y) * kRB;
+    const int64_t c0 = u.c_begin + static_cast<int64_t>(blockIdx.x) * kCB;
+    const int nrb = gridDim.y;
+    for (int e = tid; e < kNbMax * kCB; e += 256) {
+        double acc = 0.0;
+        for (int rb = 0; rb < nrb; ++rb) acc += Wpart[(static_cast<int64_t>(rb) * gridDim.x + blockIdx.x) * (kNbMax * kCB) + e];
+        W[(e / kCB) * (kCB + 1) + e % kCB] = acc;
     }
-#pragma unroll
-    for (int at = 0; at < 4; ++at)
-#pragma unroll
-        for (int ct = 0; ct < 2; ++ct) {
-            Wred[wid][at * 8 + lg][ct * 8 + 2 * lr] = acc[at][ct][0];
-            Wred[wid][at * 8 + lg][ct * 8 + 2 * lr + 1] = acc[at][ct][1];
-        }
+    for (int e = tid; e < kNbMax * kNbMax; e += 256) Ts[(e % kNbMax) * (kNbMax + 1) + e / kNbMax] = u.T[e];  // Ts[i][j] = T(i,j)
+    stage_v(u, r0, Vs);
+    stage_c(u, r0, c0, Cs);
     __syncthreads();
-    for (int e = tid; e < kNbMax * kUpdCols; e += 256) {
-        const int a = e / kUpdCols, c = e % kUpdCols;
-        double s = 0.0;
-        for (int q = 0; q < 8; ++q) s += Wred[q][a][c];
-        W[a][c] = s;
-    }
-    __syncthreads();
-    // step 2: W2 = T^T W (transT) or T W
-    for (int e = tid; e < kNbMax * kUpdCols; e += 256) {
-        const int a = e / kUpdCols, c = e % kUpdCols;
-        double s = 0.0;
+    for (int e = tid; e < kNbMax * kCB; e += 256) {
+        const int a = e / kCB, c = e % kCB;
+        double acc = 0.0;
         if (u.transT) {
-            for (int b = 0; b <= a; ++b) s += u.T[a * kNbMax + b] * W[b][c];  // T^T[a][b] = T[b][a]
+            for (int b = 0; b <= a; ++b) acc += Ts[b * (kNbMax + 1) + a] * W[b * (kCB + 1) + c];
         } else {
-            for (int b = a; b < kNbMax; ++b) s += u.T[b * kNbMax + a] * W[b][c];
+            for (int b = a; b < kNbMax; ++b) acc += Ts[a * (kNbMax + 1) + b] * W[b * (kCB + 1) + c];
         }
-        W2[a][c] = s;
+        W2[a * (kCB + 1) + c] = acc;
     }
     __syncthreads();
-    // step 3: C -= V W2, 8-row tiles over warps
-    const int64_t ntiles = (nrow + 7) / 8;
-    for (int64_t t = wid; t < ntiles; t += 8) {
-        const int64_t r0 = u.k0 + t * 8;
-        double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    // output tiles: (kRB/8) x (kCB/8) = 16 x 4 = 64; warp w owns 8 (two row tiles x four c tiles)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int rt = warp * 2 + q;
+        double d[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
         for (int ks = 0; ks < kNbMax / 4; ++ks) {
-            const double af = vget(u, r0 + lg, ks * 4 + lr);
+            const double af = Vs[(ks * 4 + lr) * kLdT + rt * 8 + lg];  // V(row rt*8+lg, col ks*4+lr)
 #pragma unroll
-            for (int ct = 0; ct < 2; ++ct) {
-                const double bfv = W2[ks * 4 + lr][ct * 8 + lg];
-                dmma(d[ct][0], d[ct][1], af, bfv);
+            for (int ct = 0; ct < 4; ++ct) {
+                const double bf = W2[(ks * 4 + lr) * (kCB + 1) + ct * 8 + lg];
+                dmma(d[ct][0], d[ct][1], af, bf);
             }
         }
-        const int64_t r = r0 + lg;
+        const int64_t r = r0 + rt * 8 + lg;
         if (r < u.r_end) {
 #pragma unroll
-            for (int ct = 0; ct < 2; ++ct)
+            for (int ct = 0; ct < 4; ++ct)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    const int64_t c = cb + ct * 8 + 2 * lr + e;
-                    if (c < u.c_end) u.C[c * u.ldc + r] -= d[ct][e];
+                    const int cl = ct * 8 + 2 * lr + e;
+                    const int64_t c = c0 + cl;
+                    if (c < u.c_end) u.C[c * u.ldc + r] = Cs[cl * kLdT + rt * 8 + lg] - d[ct][e];
                 }
         }
     }
@@ -425,8 +512,16 @@ void launch_panel(slq_ctx* ctx, const PanelArgs& pa, int cl) {
 
 void launch_update(slq_ctx* ctx, const UpdArgs& u) {
     if (u.c_end <= u.c_begin || u.r_end <= u.k0) return;
-    const unsigned grid = static_cast<unsigned>(ceil_div(u.c_end - u.c_begin, kUpdCols));
-    update_kernel<<<grid, 256, 0, ctx->stream>>>(u);
+    const unsigned ncb = static_cast<unsigned>(ceil_div(u.c_end - u.c_begin, kCB));
+    const unsigned nrb = static_cast<unsigned>(ceil_div(u.r_end - u.k0, kRB));
+    double* Wpart = static_cast<double*>(ctx->ws.qr_w.ensure(sizeof(double) * kNbMax * kCB * ncb * nrb));
+    const size_t sm1 = sizeof(double) * (kNbMax + kCB) * kLdT;
+    const size_t sm2 = sm1 + sizeof(double) * (2 * kNbMax * (kCB + 1) + kNbMax * (kNbMax + 1));
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(update_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm1)));
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(update_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2)));
+    update_w_kernel<<<dim3(ncb, nrb), 256, sm1, ctx->stream>>>(u, Wpart);
+    SLQ_LAUNCH_CHECK(ctx);
+    update_apply_kernel<<<dim3(ncb, nrb), 256, sm2, ctx->stream>>>(u, Wpart);
     SLQ_LAUNCH_CHECK(ctx);
 }
 

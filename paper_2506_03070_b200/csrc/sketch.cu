@@ -273,6 +273,8 @@ __global__ void __launch_bounds__(1024) bucketize_kernel(BucketArgs a) {
 
 // ---------------------------------------------------------------- K2 gather
 
+constexpr int kGThreads = 512;
+
 struct GatherArgs {
     const double* A;  // row-major block, row 0 = local row 0
     int64_t ld, m, d;
@@ -282,60 +284,62 @@ struct GatherArgs {
     const uint16_t* ptr;
     const uint16_t* ent;
     double val;
-    double* Yw;  // [nsplit][ld][d]
+    int64_t ldw;   // columns of Yw (>= ld, multiple of the slab width)
+    double* Yw;    // [nsplit][ldw][d]
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g));
 }
-__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(g));
-}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// 16-byte slot of half h of row k in the A stage (W=4): XOR swizzle so the
-// first halves of random rows spread over all eight 16-byte bank groups.
-__device__ __forceinline__ int slot4(int k, int h) { return 2 * k + (h ^ ((k >> 2) & 1)); }
+// 16-byte half h of A-slab row k (4 columns = 32 bytes) lives at slot
+// 2k + (h ^ ((k >> 2) & 1)): the first halves of random rows then spread over
+// all eight 16-byte bank groups (row parity x bit 2 of k), as do the second.
+__device__ __forceinline__ int gslot(int k, int h) { return 2 * k + (h ^ ((k >> 2) & 1)); }
 
-template <int W>
-__device__ __forceinline__ void stage_chunk(const GatherArgs& g, int64_t col0, int64_t c, double* As,
-                                            uint16_t* Ps, uint16_t* Es) {
-    const int tid = threadIdx.x, T = blockDim.x;
+__device__ __forceinline__ void stage_chunk(const GatherArgs& g, int64_t col0, int64_t c, double* As, uint16_t* Ps,
+                                            uint16_t* Es) {
+    const int tid = threadIdx.x;
     const int64_t k0 = c * g.K;
     const int kc = static_cast<int>(min(static_cast<int64_t>(g.K), g.m - k0));
     const double* base = g.A + k0 * g.ld + col0;
-    if (W == 4) {
-        for (int p = tid; p < 2 * kc; p += T) {
-            const int k = p >> 1, h = p & 1;
-            cp_async16(As + 2 * slot4(k, h), base + k * g.ld + 2 * h);
-        }
-    } else if (W == 2) {
-        for (int k = tid; k < kc; k += T) cp_async16(As + 2 * k, base + k * g.ld);
-    } else {
-        for (int k = tid; k < kc; k += T) cp_async8(As + k, base + k * g.ld);
+    for (int p = tid; p < 2 * kc; p += kGThreads) {
+        const int k = p >> 1, h = p & 1;
+        cp_async16(As + 2 * gslot(k, h), base + static_cast<int64_t>(k) * g.ld + 2 * h);
     }
     const uint16_t* gp = g.ptr + c * g.ptr_stride;
-    for (int p = tid; p < g.ptr_stride / 8; p += T) cp_async16(Ps + 8 * p, gp + 8 * p);
+    for (int p = tid; p < g.ptr_stride / 8; p += kGThreads) cp_async16(Ps + 8 * p, gp + 8 * p);
     const uint16_t* ge = g.ent + c * g.ent_stride;
     const int nent = static_cast<int>(g.ent_stride / 8);
-    for (int p = tid; p < nent; p += T) cp_async16(Es + 8 * p, ge + 8 * p);
+    for (int p = tid; p < nent; p += kGThreads) cp_async16(Es + 8 * p, ge + 8 * p);
 }
 
-template <int W, int RPT>
-__global__ void __launch_bounds__(512, 1) gather_kernel(GatherArgs g) {
+template <bool EXACT>
+__device__ __forceinline__ double acc_step(double y, double v, double a) {
+    // EXACT: the reference's y += v * a with two roundings (csc_matrix.hpp:116)
+    return EXACT ? __dadd_rn(y, __dmul_rn(v, a)) : fma(v, a, y);
+}
+
+// CTA = one 4-column slab of Y_aug, all d rows in REGISTERS: thread t owns
+// rows t, t+512, ... (RPT of them).  Per chunk of K rows of A the slab
+// segment (K x 32 bytes), the chunk's row pointers and its entries sorted by
+// (r, k) are staged by cp.async (double buffer); each thread walks its rows'
+// entries in ascending k -- the reference's order -- gathering 32 bytes of A
+// per entry.
+template <int RPT, bool EXACT>
+__global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int tid = threadIdx.x;
-    constexpr int T = 512;
-    const int64_t col0 = static_cast<int64_t>(blockIdx.x) * W;
+    const int64_t col0 = static_cast<int64_t>(blockIdx.x) * 4;
     const int64_t split = blockIdx.y;
     const int64_t cb = split * g.nchunks / g.nsplit;
     const int64_t ce = (split + 1) * g.nchunks / g.nsplit;
 
-    const size_t a_bytes = static_cast<size_t>(g.K) * W * sizeof(double);
+    const size_t a_bytes = static_cast<size_t>(g.K) * 4 * sizeof(double);
     const size_t p_bytes = g.ptr_stride * sizeof(uint16_t);
     const size_t e_bytes = g.ent_stride * sizeof(uint16_t);
     const size_t st_bytes = a_bytes + p_bytes + e_bytes;
@@ -343,17 +347,17 @@ __global__ void __launch_bounds__(512, 1) gather_kernel(GatherArgs g) {
     auto Ps = [&](int s) { return reinterpret_cast<uint16_t*>(smem + s * st_bytes + a_bytes); };
     auto Es = [&](int s) { return reinterpret_cast<uint16_t*>(smem + s * st_bytes + a_bytes + p_bytes); };
 
-    double y[RPT][W];
+    double y[RPT][4];
 #pragma unroll
     for (int q = 0; q < RPT; ++q)
 #pragma unroll
-        for (int w = 0; w < W; ++w) y[q][w] = 0.0;
+        for (int w = 0; w < 4; ++w) y[q][w] = 0.0;
 
-    if (cb < ce) stage_chunk<W>(g, col0, cb, As(0), Ps(0), Es(0));
+    if (cb < ce) stage_chunk(g, col0, cb, As(0), Ps(0), Es(0));
     cp_commit();
     for (int64_t c = cb; c < ce; ++c) {
         const int s = static_cast<int>((c - cb) & 1);
-        if (c + 1 < ce) stage_chunk<W>(g, col0, c + 1, As(s ^ 1), Ps(s ^ 1), Es(s ^ 1));
+        if (c + 1 < ce) stage_chunk(g, col0, c + 1, As(s ^ 1), Ps(s ^ 1), Es(s ^ 1));
         cp_commit();
         cp_wait<1>();
         __syncthreads();
@@ -362,40 +366,32 @@ __global__ void __launch_bounds__(512, 1) gather_kernel(GatherArgs g) {
         const uint16_t* E_s = Es(s);
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
-            const int r = tid + q * T;
+            const int r = tid + q * kGThreads;
             if (r < g.d) {
                 const int e0 = P_s[r], e1 = P_s[r + 1];
                 for (int e = e0; e < e1; ++e) {
                     const unsigned en = E_s[e];
                     const int k = static_cast<int>(en >> 1);
                     const double v = (en & 1u) ? -g.val : g.val;
-                    if (W == 4) {
-                        const double2 lo = *reinterpret_cast<const double2*>(A_s + 2 * slot4(k, 0));
-                        const double2 hi = *reinterpret_cast<const double2*>(A_s + 2 * slot4(k, 1));
-                        y[q][0] = __dadd_rn(y[q][0], __dmul_rn(v, lo.x));
-                        y[q][1 % W] = __dadd_rn(y[q][1 % W], __dmul_rn(v, lo.y));
-                        y[q][2 % W] = __dadd_rn(y[q][2 % W], __dmul_rn(v, hi.x));
-                        y[q][3 % W] = __dadd_rn(y[q][3 % W], __dmul_rn(v, hi.y));
-                    } else if (W == 2) {
-                        const double2 lo = *reinterpret_cast<const double2*>(A_s + 2 * k);
-                        y[q][0] = __dadd_rn(y[q][0], __dmul_rn(v, lo.x));
-                        y[q][1 % W] = __dadd_rn(y[q][1 % W], __dmul_rn(v, lo.y));
-                    } else {
-                        y[q][0] = __dadd_rn(y[q][0], __dmul_rn(v, A_s[k]));
-                    }
+                    const double2 lo = *reinterpret_cast<const double2*>(A_s + 2 * gslot(k, 0));
+                    const double2 hi = *reinterpret_cast<const double2*>(A_s + 2 * gslot(k, 1));
+                    y[q][0] = acc_step<EXACT>(y[q][0], v, lo.x);
+                    y[q][1] = acc_step<EXACT>(y[q][1], v, lo.y);
+                    y[q][2] = acc_step<EXACT>(y[q][2], v, hi.x);
+                    y[q][3] = acc_step<EXACT>(y[q][3], v, hi.y);
                 }
             }
         }
         __syncthreads();
     }
     cp_wait<0>();
-    double* Y = g.Yw + split * g.ld * g.d;
+    double* Y = g.Yw + split * g.ldw * g.d;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
-        const int r = tid + q * T;
+        const int r = tid + q * kGThreads;
         if (r < g.d)
 #pragma unroll
-            for (int w = 0; w < W; ++w) Y[(col0 + w) * g.d + r] = y[q][w];
+            for (int w = 0; w < 4; ++w) Y[(col0 + w) * g.d + r] = y[q][w];
     }
 }
 
@@ -457,27 +453,42 @@ struct ChunkPlan {
 
 ChunkPlan plan_chunks(int64_t m, int64_t d, int64_t zeta_max) {
     ChunkPlan p{};
-    // entries per chunk <= 16384 (u16 offsets, 64 KB of sort keys)
     int zp = 1;
     while (zp < zeta_max) zp <<= 1;
-    p.K = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(16, 16384 / zp)));
+    p.ptr_stride = round_up(d + 1, 8);
+    // largest power-of-two K (<= 2048, entries <= 16384 for u16 offsets) whose
+    // double-buffered stage (A slab 32 B/row + row pointers + entries) fits
+    int K = 2048;
+    while (K > 16 && (static_cast<int64_t>(K) * zp > 16384 ||
+                      2 * (K * 32 + p.ptr_stride * 2 + round_up(static_cast<int64_t>(K) * zeta_max, 8) * 2) > 220 * 1024))
+        K >>= 1;
+    p.K = K;
     p.KB = 0;
     while ((1 << p.KB) < p.K) ++p.KB;
     p.cap = 16384;
     p.nchunks = ceil_div(m, p.K);
-    p.ptr_stride = round_up(d + 1, 8);
     p.ent_stride = round_up(static_cast<int64_t>(p.K) * zeta_max, 8);
     return p;
 }
 
-template <int W, int RPT>
-void launch_gather(slq_ctx* ctx, const GatherArgs& g, int64_t nslabs, size_t smem) {
-    auto kern = gather_kernel<W, RPT>;
-    SLQ_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
+template <int RPT, bool EXACT>
+void launch_gather_t(slq_ctx* ctx, const GatherArgs& g, int64_t nslabs, size_t smem) {
+    auto kern = gather_kernel<RPT, EXACT>;
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     dim3 grid(static_cast<unsigned>(nslabs), static_cast<unsigned>(g.nsplit));
-    kern<<<grid, 512, smem, ctx->stream>>>(g);
+    kern<<<grid, kGThreads, smem, ctx->stream>>>(g);
     SLQ_LAUNCH_CHECK(ctx);
+}
+
+template <bool EXACT>
+void launch_gather(slq_ctx* ctx, const GatherArgs& g, int rpt, int64_t nslabs, size_t smem) {
+    switch (rpt) {
+        case 1: launch_gather_t<1, EXACT>(ctx, g, nslabs, smem); break;
+        case 2: launch_gather_t<2, EXACT>(ctx, g, nslabs, smem); break;
+        case 4: launch_gather_t<4, EXACT>(ctx, g, nslabs, smem); break;
+        case 8: launch_gather_t<8, EXACT>(ctx, g, nslabs, smem); break;
+        default: fail(SLQ_UNSUPPORTED, "sketch_apply: d > 4096 not supported by the register-slab gather");
+    }
 }
 
 }  // namespace
@@ -495,7 +506,7 @@ void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const
     }
     ChunkPlan cp = plan_chunks(m, d, zeta);
     uint16_t* ptr = ws.chunk_ptr.as<uint16_t>();
-    ptr = static_cast<uint16_t*>(ws.chunk_ptr.ensure(sizeof(uint16_t) * cp.ptr_stride * cp.nchunks));
+    ptr = static_cast<uint16_t*>(ws.chunk_ptr.ensure(sizeof(uint16_t) * (cp.ptr_stride * cp.nchunks + d + 64)));  // slack: part slices may run past the last chunk
     uint16_t* ent = static_cast<uint16_t*>(ws.chunk_ent.ensure(sizeof(uint16_t) * cp.ent_stride * cp.nchunks));
     int* flags = static_cast<int*>(ws.flags.ensure(4096));
     SLQ_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int), ctx->stream));
@@ -508,14 +519,12 @@ void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const
     bucketize_kernel<<<static_cast<unsigned>(cp.nchunks), 1024, bsmem, ctx->stream>>>(ba);
     SLQ_LAUNCH_CHECK(ctx);
 
-    // slab width W and rows per thread RPT: RPT * W <= 32 doubles of registers
-    int W = 4;
-    int64_t rpt = ceil_div(d, 512);
-    if (rpt > 8) W = (rpt > 16) ? 1 : 2;
-    int RPT = 1;
-    while (RPT < rpt) RPT <<= 1;
-    const int64_t nslabs = ld / W;
-    // splits: balance waves over the SMs unless the exact serial order is asked for
+    // 4-column slab per CTA, all d rows of the slab in registers (<= 8 rows per thread)
+    int rpt = 1;
+    while (rpt * kGThreads < d) rpt <<= 1;
+    const int64_t ldw = round_up(ld, 4);
+    const int64_t nslabs = ldw / 4;
+    // splits along m: balance waves over the SMs unless the exact serial order is asked for
     int64_t nsplit = 1;
     if (!exact) {
         double best = 1e30;
@@ -530,25 +539,18 @@ void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const
             }
         }
     }
-    double* Yw = (nsplit == 1 && ld == ncols_out) ? Y
-                 : static_cast<double*>(ws.ypart.ensure(sizeof(double) * nsplit * ld * d));
-    GatherArgs g{A->A, ld, m, d, cp.K, cp.nchunks, nsplit, cp.ptr_stride, cp.ent_stride, ptr, ent, val, Yw};
-    const size_t smem = 2 * (static_cast<size_t>(cp.K) * W * sizeof(double) +
-                             cp.ptr_stride * sizeof(uint16_t) + cp.ent_stride * sizeof(uint16_t));
+    double* Yw = (nsplit == 1 && ldw == ncols_out) ? Y
+                 : static_cast<double*>(ws.ypart.ensure(sizeof(double) * nsplit * ldw * d));
+    GatherArgs g{A->A, ld, m, d, cp.K, cp.nchunks, nsplit, cp.ptr_stride, cp.ent_stride, ptr, ent, val, ldw, Yw};
+    const size_t smem = 2 * (static_cast<size_t>(cp.K) * 4 * sizeof(double) + cp.ptr_stride * sizeof(uint16_t) +
+                             cp.ent_stride * sizeof(uint16_t));
     if (smem > 227 * 1024) fail(SLQ_UNSUPPORTED, "sketch_apply: stage exceeds shared memory");
-    switch (W * 100 + RPT) {
-        case 401: launch_gather<4, 1>(ctx, g, nslabs, smem); break;
-        case 402: launch_gather<4, 2>(ctx, g, nslabs, smem); break;
-        case 404: launch_gather<4, 4>(ctx, g, nslabs, smem); break;
-        case 408: launch_gather<4, 8>(ctx, g, nslabs, smem); break;
-        case 216: launch_gather<2, 16>(ctx, g, nslabs, smem); break;
-        case 132: launch_gather<1, 32>(ctx, g, nslabs, smem); break;
-        default: fail(SLQ_UNSUPPORTED, "sketch_apply: unsupported slab configuration");
-    }
+    if (exact) launch_gather<true>(ctx, g, rpt, nslabs, smem);
+    else launch_gather<false>(ctx, g, rpt, nslabs, smem);
     if (Yw != Y) {
         const int64_t tot = d * ncols_out;
         reduce_splits_kernel<<<static_cast<unsigned>(ceil_div(tot, 256)), 256, 0, ctx->stream>>>(
-            Yw, nsplit, d, ld, ncols_out, Y);
+            Yw, nsplit, d, ldw, ncols_out, Y);
         SLQ_LAUNCH_CHECK(ctx);
     }
     int hflag = 0;
