@@ -150,6 +150,9 @@ class COracle(_Base):
         L.orc_rejection_sample_columns.argtypes = [_i64, _i64, _i64, _u64, _ip, _ip, _ip]
         L.orc_spmm_csc_dense.argtypes = [_i64, _i64, _ip, _dp, _ip, _dp, _i64, _dp]
         L.orc_csc_matvec.argtypes = [_i64, _i64, _ip, _dp, _ip, _dp, _dp]
+        L.orc_csc_rmatvec.argtypes = [_i64, _i64, _ip, _dp, _ip, _dp, _dp]
+        L.orc_lsqr_csc.argtypes = [_i64, _i64, _ip, _dp, _ip, _dp, _dp, _dp, ct.c_double, ct.c_long, ct.c_int,
+                                   _dp, ct.c_int, _dp, ct.POINTER(_OrcReport), _dp, _dp, _dp]
         L.orc_spmm_csc_csc.argtypes = [_i64, _ip, _dp, _ip, _i64, _ip, _dp, _ip, _dp]
         L.orc_matvec.argtypes = [_dp, _i64, _i64, _dp, _dp]
         L.orc_rmatvec.argtypes = [_dp, _i64, _i64, _dp, _dp]
@@ -203,6 +206,46 @@ class COracle(_Base):
         y = np.zeros(d)
         self._check(self.lib.orc_csc_matvec(d, x.size, _i(rows), _d(vals), _i(colptr), _d(x), _d(y)))
         return y
+
+    def spmm_csc(self, d, srows, svals, scolptr, m, n, arows, avals, acolptr):
+        """Y = S A for CSC S (d x m) and CSC A (m x n): csc_matrix.hpp:123-136"""
+        Y = np.zeros((d, n), order="F")
+        self._check(self.lib.orc_spmm_csc_csc(d, _i(srows), _d(svals), _i(scolptr), n, _i(arows), _d(avals),
+                                              _i(acolptr), _d(Y)))
+        return Y
+
+    def sketch_apply_csc(self, d, zeta, seed, m, n, arows, avals, acolptr, b=None):
+        rows, vals, colptr, _ = self.generate_sparse_sign(d, m, zeta, seed)
+        Y = self.spmm_csc(d, rows, vals, colptr, m, n, arows, avals, acolptr)
+        Sb = self.csc_matvec(d, rows, vals, colptr, b) if b is not None else None
+        return Y, Sb
+
+    def csc_matvec_A(self, m, n, arows, avals, acolptr, x):
+        """y = A x for CSC A (m x n): csc_matrix.hpp:71-82"""
+        y = np.zeros(m)
+        self._check(self.lib.orc_csc_matvec(m, n, _i(arows), _d(avals), _i(acolptr), _d(_col(x)), _d(y)))
+        return y
+
+    def csc_rmatvec_A(self, m, n, arows, avals, acolptr, y):
+        """x = A^T y for CSC A: csc_matrix.hpp:85-96"""
+        x = np.zeros(n)
+        self._check(self.lib.orc_csc_rmatvec(m, n, _i(arows), _d(avals), _i(acolptr), _d(_col(y)), _d(x)))
+        return x
+
+    def lsqr_csc(self, m, n, arows, avals, acolptr, M, b, x0, eps=1e-10, maxit=100, one_sync=False, x_star=None,
+                 track_true=False):
+        M = _f(M)
+        x = np.zeros(n)
+        rep = _OrcReport()
+        est = np.zeros(max(maxit, 1) + 1)
+        err = np.zeros(max(maxit, 1) + 2)
+        tru = np.zeros(max(maxit, 1) + 2)
+        xs = _col(x_star) if x_star is not None else None
+        self._check(self.lib.orc_lsqr_csc(m, n, _i(arows), _d(avals), _i(acolptr), _d(M), _d(_col(b)),
+                                          _d(_col(x0)), eps, maxit, int(one_sync), _d(xs), int(track_true),
+                                          _d(x), ct.byref(rep), _d(est), _d(err), _d(tru)))
+        return x, Report(rep.iterations, TERMINATION[rep.termination], est[: rep.n_estimate].copy(),
+                         err[: rep.n_err].copy(), tru[: rep.n_true].copy())
 
     def sketch_apply(self, d, zeta, seed, A, b=None):
         A = _f(A)
@@ -324,6 +367,8 @@ class RefOracle(_Base):
         L.ref_lsqr.argtypes = [_dp, _i64, _i64, _dp, _dp, _dp, ct.c_double, _i64, ct.c_int, _dp,
                                ct.c_int, ct.c_int, _dp, ct.POINTER(_RefReport), _dp, _dp, _dp]
         L.ref_partition_rows.argtypes = [_i64, ct.c_int, _ip]
+        L.ref_lsqr_csc.argtypes = [_i64, _i64, _ip, _dp, _ip, _dp, _dp, _dp, ct.c_double, _i64, ct.c_int, _dp,
+                                   ct.c_int, ct.c_int, _dp, ct.POINTER(_RefReport), _dp, _dp, _dp]
         L.ref_dist_generate_sparse_sign.argtypes = [_i64, _i64, _i64, _u64, ct.c_int, _ip, _dp, _ip]
         L.ref_dist_sketch_apply.argtypes = [_i64, _i64, _i64, _u64, _dp, _i64, _dp, ct.c_int, _dp, _dp]
         L.ref_gen_dense.argtypes = [_i64, _i64, ct.c_double, _u64, _dp]
@@ -417,6 +462,27 @@ class RefOracle(_Base):
         out = np.zeros(p + 1, np.int64)
         self._check(self.lib.ref_partition_rows(m, p, _i(out)))
         return out
+
+    def sketch_apply_csc(self, d, zeta, seed, m, n, arows, avals, acolptr):
+        Y = np.zeros((d, n), order="F")
+        self._check(self.lib.ref_sketch_apply_csc(d, m, zeta, seed, n, _i(arows), _d(avals), _i(acolptr), _d(Y)))
+        return Y
+
+    def lsqr_csc(self, m, n, arows, avals, acolptr, M, b, x0, eps=1e-10, maxit=100, one_sync=False, x_star=None,
+                 track_true=False, workers=0):
+        M = _f(M)
+        x = np.zeros(n)
+        rep = _RefReport()
+        est = np.zeros(max(maxit, 1) + 1)
+        err = np.zeros(max(maxit, 1) + 2)
+        tru = np.zeros(max(maxit, 1) + 2)
+        xs = _col(x_star) if x_star is not None else None
+        self._check(self.lib.ref_lsqr_csc(m, n, _i(arows), _d(avals), _i(acolptr), _d(M), _d(_col(b)),
+                                          _d(_col(x0)), eps, maxit, int(one_sync), _d(xs), int(track_true), workers,
+                                          _d(x), ct.byref(rep), _d(est), _d(err), _d(tru)))
+        return x, Report(rep.iterations, TERMINATION[rep.termination], est[: rep.n_estimate].copy(),
+                         err[: rep.n_err].copy(), tru[: rep.n_true].copy(), rep.sync_count,
+                         rep.broadcasts, rep.init_reductions, rep.init_broadcasts, rep.wall_time)
 
     def dist_generate_sparse_sign(self, d, m, zeta, seed, p):
         rows = np.zeros(m * zeta, np.int64)

@@ -238,6 +238,44 @@ int ref_lsqr(const double* A, int64_t m, int64_t n, const double* M, const doubl
     } catch (...) { return map_exc(); }
 }
 
+// lsqr.hpp:198-202 / :208-212 (CscMatrix overloads); workers > 0: DistOperator<CscMatrix>
+int ref_lsqr_csc(int64_t m, int64_t n, const int64_t* rows, const double* vals, const int64_t* colptr,
+                 const double* M, const double* b, const double* x0, double eps, int64_t maxit, int one_sync,
+                 const double* x_star, int track_true, int workers, double* x_out, ref_report* rep, double* est,
+                 double* err, double* tru) {
+    try {
+        CscMatrix A(m, n);
+        const int64_t nnz = colptr[n];
+        A.row_indices.assign(rows, rows + nnz);
+        A.values.assign(vals, vals + nnz);
+        A.col_pointers.assign(colptr, colptr + n + 1);
+        Preconditioner P;
+        P.M = wrap(M, n, n);
+        Vector bv(b, b + m), xv(x0, x0 + n), xs;
+        SolveOptions o;
+        o.eps = eps;
+        o.maxit = maxit;
+        if (x_star) {
+            xs.assign(x_star, x_star + n);
+            o.x_star = &xs;
+        }
+        o.track_true_residual = track_true != 0;
+        std::pair<Vector, SolveReport> res;
+        if (workers <= 0) {
+            res = one_sync ? lsqr_one_sync(A, P, bv, xv, o) : lsqr(A, P, bv, xv, o);
+        } else {
+            WorkerPool pool(workers);
+            auto dA = distribute(A, pool);
+            DistributedVector db = distribute(bv, pool);
+            auto op = dist_operator(dA);
+            res = one_sync ? lsqr_one_sync(op, P, db, xv, o) : lsqr(op, P, db, xv, o);
+        }
+        std::memcpy(x_out, res.first.data(), sizeof(double) * n);
+        fill(res.second, rep, est, err, tru);
+        return 0;
+    } catch (...) { return map_exc(); }
+}
+
 // distsim.hpp:31
 int ref_partition_rows(int64_t m, int p, int64_t* boundaries) {
     try {

@@ -191,6 +191,18 @@ int orc_csc_matvec(idx d, idx m, const idx* rows, const double* vals, const idx*
     return OK;
 }
 
+/* csc_matrix.hpp:85-96 -- x = S^T y (per-column dot) */
+int orc_csc_rmatvec(idx d, idx m, const idx* rows, const double* vals, const idx* colptr,
+                    const double* y, double* x) {
+    (void)d;
+    for (idx j = 0; j < m; ++j) {
+        double s = 0.0;
+        for (idx p = colptr[j]; p < colptr[j + 1]; ++p) s += vals[p] * y[rows[p]];
+        x[j] = s;
+    }
+    return OK;
+}
+
 /* csc_matrix.hpp:123-136 -- Y = S A for CSC A (m x n) */
 int orc_spmm_csc_csc(idx d, const idx* srows, const double* svals, const idx* scolptr,
                      idx n, const idx* arows, const double* avals, const idx* acolptr, double* Y) {
@@ -369,17 +381,38 @@ typedef struct {
     long n_err;        /* entries written to iterates_error */
 } orc_lsqr_report;
 
-static void record(const double* A, idx m, idx n, const double* b, const double* x,
+/* The Op surface of operators.hpp:15-51 (SerialOperator<DenseMatrix> and
+ * SerialOperator<CscMatrix>): only matvec / rmatvec differ. */
+typedef struct {
+    idx m, n;
+    int csc;
+    const double* A;        /* dense column-major */
+    const idx* rows;        /* CSC */
+    const double* vals;
+    const idx* colptr;
+} orc_op;
+
+static void op_matvec(const orc_op* op, const double* x, double* y) {
+    if (op->csc) orc_csc_matvec(op->m, op->n, op->rows, op->vals, op->colptr, x, y);
+    else orc_matvec(op->A, op->m, op->n, x, y);
+}
+
+static void op_rmatvec(const orc_op* op, const double* y, double* x) {
+    if (op->csc) orc_csc_rmatvec(op->m, op->n, op->rows, op->vals, op->colptr, y, x);
+    else orc_rmatvec(op->A, op->m, op->n, y, x);
+}
+
+static void record(const orc_op* op, idx m, idx n, const double* b, const double* x,
                    const double* x_star, int track_true, double* err_hist, double* true_hist,
                    orc_lsqr_report* rep, double* wm, double* wn) {
     /* lsqr.hpp:26-37 + operators.hpp:37-42 */
     if (x_star) {
         for (idx j = 0; j < n; ++j) wn[j] = x_star[j] - x[j];
-        orc_matvec(A, m, n, wn, wm);
+        op_matvec(op, wn, wm);
         err_hist[rep->n_err++] = norm2(wm, m);
     }
     if (track_true) {
-        orc_matvec(A, m, n, x, wm);
+        op_matvec(op, x, wm);
         for (idx i = 0; i < m; ++i) wm[i] = b[i] + (-1.0) * wm[i];
         true_hist[rep->n_true++] = norm2(wm, m);
     }
@@ -387,10 +420,11 @@ static void record(const double* A, idx m, idx n, const double* b, const double*
 
 /* lsqr.hpp:50-168 (lsqr_impl), serial operator operators.hpp:15-51.
  * one_sync selects lsqr.hpp:120-127 vs lsqr.hpp:128-132. */
-int orc_lsqr(const double* A, idx m, idx n, const double* M, const double* b, const double* x0,
-             double eps, long maxit, int one_sync, const double* x_star, int track_true,
-             double* x_out, orc_lsqr_report* rep, double* est_hist, double* err_hist,
-             double* true_hist) {
+static int lsqr_op(const orc_op* op, const double* M, const double* b, const double* x0,
+                   double eps, long maxit, int one_sync, const double* x_star, int track_true,
+                   double* x_out, orc_lsqr_report* rep, double* est_hist, double* err_hist,
+                   double* true_hist) {
+    const idx m = op->m, n = op->n;
     memset(rep, 0, sizeof(*rep));
     double* u = (double*)malloc(sizeof(double) * (size_t)m);
     double* uh = (double*)malloc(sizeof(double) * (size_t)m);
@@ -404,14 +438,14 @@ int orc_lsqr(const double* A, idx m, idx n, const double* M, const double* b, co
     double* x = x_out;
     memcpy(x, x0, sizeof(double) * (size_t)n);
 
-    orc_matvec(A, m, n, x0, wm);
+    op_matvec(op, x0, wm);
     for (idx i = 0; i < m; ++i) u[i] = b[i] + (-1.0) * wm[i];
     const double beta1 = norm2(u, m);
-    record(A, m, n, b, x, x_star, track_true, err_hist, true_hist, rep, wm, wn);
+    record(op, m, n, b, x, x_star, track_true, err_hist, true_hist, rep, wm, wn);
     int status = OK;
     if (beta1 == 0.0) { rep->termination = TERM_TOLERANCE; rep->iterations = 0; goto done; }
     for (idx i = 0; i < m; ++i) u[i] *= 1.0 / beta1;
-    orc_rmatvec(A, m, n, u, tn);
+    op_rmatvec(op, u, tn);
     orc_tri_upper_rmatvec(M, n, tn, v);
     double alpha = norm2(v, n);
     if (alpha == 0.0) { rep->termination = TERM_TOLERANCE; rep->iterations = 0; goto done; }
@@ -423,11 +457,11 @@ int orc_lsqr(const double* A, idx m, idx n, const double* M, const double* b, co
     rep->iterations = maxit;
     for (long t = 1; t <= maxit; ++t) {
         orc_tri_upper_matvec(M, n, v, tn);
-        orc_matvec(A, m, n, tn, uh);
+        op_matvec(op, tn, uh);
         for (idx i = 0; i < m; ++i) uh[i] += -alpha * u[i];
         double beta;
         if (one_sync) {
-            orc_rmatvec(A, m, n, uh, tn);
+            op_rmatvec(op, uh, tn);
             beta = norm2(uh, m);
         } else {
             beta = norm2(uh, m);
@@ -440,7 +474,7 @@ int orc_lsqr(const double* A, idx m, idx n, const double* M, const double* b, co
                 for (idx i = 0; i < m; ++i) uh[i] *= 1.0 / beta;
             } else {
                 for (idx i = 0; i < m; ++i) uh[i] *= 1.0 / beta;
-                orc_rmatvec(A, m, n, uh, tn);
+                op_rmatvec(op, uh, tn);
             }
             memcpy(u, uh, sizeof(double) * (size_t)m);
             orc_tri_upper_rmatvec(M, n, tn, tn2);          /* v_hat = M^T z */
@@ -461,7 +495,7 @@ int orc_lsqr(const double* A, idx m, idx n, const double* M, const double* b, co
                 orc_tri_upper_matvec(M, n, v, tn2);
                 for (idx j = 0; j < n; ++j) w[j] = tn2[j] + (-theta / rho) * w[j];
                 est_hist[rep->n_estimate++] = phi_bar;
-                record(A, m, n, b, x, x_star, track_true, err_hist, true_hist, rep, wm, wn);
+                record(op, m, n, b, x, x_star, track_true, err_hist, true_hist, rep, wm, wn);
                 if (phi_bar <= eps * beta1) {
                     rep->termination = TERM_TOLERANCE;
                     rep->iterations = t;
@@ -478,7 +512,7 @@ int orc_lsqr(const double* A, idx m, idx n, const double* M, const double* b, co
             phi_bar = (beta_term / rho) * phi_bar;
             for (idx j = 0; j < n; ++j) x[j] += (phi / rho) * w[j];
             est_hist[rep->n_estimate++] = phi_bar;
-            record(A, m, n, b, x, x_star, track_true, err_hist, true_hist, rep, wm, wn);
+            record(op, m, n, b, x, x_star, track_true, err_hist, true_hist, rep, wm, wn);
             rep->termination = TERM_BREAKDOWN;
             rep->iterations = t;
             break;
@@ -487,6 +521,25 @@ int orc_lsqr(const double* A, idx m, idx n, const double* M, const double* b, co
 done:
     free(u); free(uh); free(wm); free(v); free(w); free(tn); free(tn2); free(wn);
     return status;
+}
+
+int orc_lsqr(const double* A, idx m, idx n, const double* M, const double* b, const double* x0,
+             double eps, long maxit, int one_sync, const double* x_star, int track_true,
+             double* x_out, orc_lsqr_report* rep, double* est_hist, double* err_hist,
+             double* true_hist) {
+    orc_op op = {m, n, 0, A, NULL, NULL, NULL};
+    return lsqr_op(&op, M, b, x0, eps, maxit, one_sync, x_star, track_true, x_out, rep, est_hist,
+                   err_hist, true_hist);
+}
+
+/* lsqr.hpp:198-202 / :208-212 -- CscMatrix overloads (SerialOperator<CscMatrix>) */
+int orc_lsqr_csc(idx m, idx n, const idx* rows, const double* vals, const idx* colptr,
+                 const double* M, const double* b, const double* x0, double eps, long maxit,
+                 int one_sync, const double* x_star, int track_true, double* x_out,
+                 orc_lsqr_report* rep, double* est_hist, double* err_hist, double* true_hist) {
+    orc_op op = {m, n, 1, NULL, rows, vals, colptr};
+    return lsqr_op(&op, M, b, x0, eps, maxit, one_sync, x_star, track_true, x_out, rep, est_hist,
+                   err_hist, true_hist);
 }
 
 /* ----------------------------------------------------- partitioning */

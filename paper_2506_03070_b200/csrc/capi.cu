@@ -277,11 +277,12 @@ int run_solve(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_
         Timer t5(ctx->stream);
         double* x = static_cast<double*>(ws.xbuf.ensure(sizeof(double) * (n + 8)));
         slq::LsqrOut lo;
-        slq::lsqr_dev(ctx, A, nullptr, P.M, P.Mt, P.x0, x, opts, est, nullptr, nullptr, lo);
+        auto op = slq::make_dense_op(ctx, A);
+        slq::lsqr_dev(ctx, *op, nullptr, P.M, P.Mt, P.x0, x, opts, est, nullptr, nullptr, lo);
         mark("lsqr");
         Timer t6(ctx->stream);
         if (opts.backward_tol > 0.0 || opts.a_norm_est > 0.0)
-            lo.backward_error = slq::backward_error_dev(ctx, A, x, opts.a_norm_est > 0.0 ? opts.a_norm_est : 1.0);
+            lo.backward_error = slq::backward_error_dev(ctx, *op, x, opts.a_norm_est > 0.0 ? opts.a_norm_est : 1.0);
         if (x_out) SLQ_CUDA_CHECK(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
         fill_report(report, lo);
         mark("finish");
@@ -718,7 +719,8 @@ int slq_lsqr(slq_ctx* ctx, const slq_dense* A, const double* M, const double* b,
         double* x = static_cast<double*>(dx.ensure(sizeof(double) * (n + 8)));
         slq::LsqrOut lo;
         const auto h0 = std::chrono::steady_clock::now();
-        slq::lsqr_dev(ctx, A, bd, P.M, P.Mt, P.x0, x, opts, residual_estimate, iterates_error, residual_true, lo);
+        slq::lsqr_dev(ctx, *slq::make_dense_op(ctx, A), bd, P.M, P.Mt, P.x0, x, opts, residual_estimate, iterates_error,
+                      residual_true, lo);
         SLQ_CUDA_CHECK(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
         lo.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
         fill_report(report, lo);
@@ -735,7 +737,7 @@ int slq_time_kernels(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, 
     return guarded([&] {
         need(ctx && A && out, SLQ_INVALID_ARG, "time_kernels: null argument");
         const int64_t n = A->n, m = A->m;
-        out[0] = slq::time_fused_pass(ctx, A, reps);
+        out[0] = slq::time_fused_pass(ctx, *slq::make_dense_op(ctx, A), reps);
         slq::Workspace& ws = ctx->ws;
         double* Yaug = static_cast<double*>(ws.yaug.ensure(sizeof(double) * d * (n + 1)));
         uint32_t* compact = static_cast<uint32_t*>(ws.compact.ensure(sizeof(uint32_t) * std::max<int64_t>(1, m * zeta)));

@@ -23,6 +23,7 @@
 //                    lsqr.hpp:115 and :156).
 // The iteration is captured in a CUDA graph (8 iterations per launch); a
 // device-side done flag turns the tail of the last graph into no-ops.
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -287,7 +288,7 @@ __device__ __forceinline__ double block0_sum_fixed(const double* p, unsigned np)
     // warp 0: lane l sums p[l], p[l+32], ... in order, then a fixed xor tree
     const int lane = threadIdx.x & 31;
     double s = 0.0;
-    for (unsigned b = lane; b < np; b += 32) s += static_cast<const volatile double*>(p)[b];
+    for (unsigned b = lane; b < np; b += 32) s += __ldcg(p + b);  // L2-coherent, loads batchable
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     return s;
@@ -579,6 +580,29 @@ void launch_pass(slq_ctx* ctx, const PassPlan& pp, PassArgs a) {
     }
 }
 
+class DenseOp final : public PassOp {
+public:
+    DenseOp(slq_ctx* ctx, const slq_dense* A) : A_(A), pp_(plan_pass(ctx, A)) {
+        m = A->m;
+        n = A->n;
+    }
+    int grid() const override { return pp_.grid; }
+    void pass(slq_ctx* ctx, const PassCall& c) const override {
+        PassArgs a{A_->A, A_->ld, m, n, c.p, c.u_in, c.u_out, c.coef, c.c_fixed, c.part, c.want_z, c.skip, 0, 0};
+        launch_pass(ctx, pp_, a);
+    }
+    std::vector<uint64_t> key() const override {
+        return {1, reinterpret_cast<uint64_t>(A_->A), static_cast<uint64_t>(m), static_cast<uint64_t>(n),
+                static_cast<uint64_t>(A_->ld), static_cast<uint64_t>(pp_.grid), static_cast<uint64_t>(pp_.R),
+                static_cast<uint64_t>(pp_.S)};
+    }
+    double pass_bytes() const override { return 8.0 * m * n + 16.0 * m; }
+
+private:
+    const slq_dense* A_;
+    PassPlan pp_;
+};
+
 struct LsqrBufs {
     double *u, *p, *v, *vhat, *w, *zt, *part, *part2, *hist, *tmp_n, *scal;
     LsqrState* st;
@@ -586,13 +610,17 @@ struct LsqrBufs {
 
 }  // namespace
 
-void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const double* M, const double* Mt,
+std::unique_ptr<PassOp> make_dense_op(slq_ctx* ctx, const slq_dense* A) {
+    return std::unique_ptr<PassOp>(new DenseOp(ctx, A));
+}
+
+void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* M, const double* Mt,
               const double* x0, double* x, const slq_solve_opts& opts, double* est_hist,
               double* err_hist, double* true_hist, LsqrOut& out) {
-    const int64_t m = A->m, n = A->n;
+    const int64_t m = op.m, n = op.n;
     const int64_t maxit = std::max<int64_t>(0, opts.maxit);
     Workspace& ws = ctx->ws;
-    PassPlan pp = plan_pass(ctx, A);
+    const int grid = op.grid();
     const int mtz_grid = static_cast<int>(std::max<int64_t>(1, ceil_div(n, 8)));
 
     // workspace layout
@@ -608,7 +636,7 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
     B.part2 = vecs + 6 * nvec;
     B.hist = B.part2 + mtz_grid;
     B.scal = B.hist + maxit + 8;
-    B.part = static_cast<double*>(ws.lsqr_part.ensure(sizeof(double) * pp.grid * (n + 1)));
+    B.part = static_cast<double*>(ws.lsqr_part.ensure(sizeof(double) * grid * (n + 1)));
     B.st = static_cast<LsqrState*>(ws.lsqr_state.ensure(sizeof(LsqrState)));
     B.u = static_cast<double*>(ws.lsqr_u.ensure(sizeof(double) * std::max<int64_t>(1, m)));
 
@@ -624,6 +652,30 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
     SLQ_CUDA_CHECK(cudaEventCreate(&e1));
     SLQ_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
 
+    // Keep M and M^T (16 MB at n = 1000) resident in L2 while A streams past
+    // with an evict-first policy: the per-iteration triangular applies then
+    // hit L2 instead of HBM.
+    bool l2_window = false;
+    {
+        const double* lo = std::min(M, Mt);
+        const size_t bytes = (std::max(M, Mt) - lo == n * n) ? 2 * n * n * sizeof(double) : n * n * sizeof(double);
+        static bool limit_set = false;
+        if (!limit_set) {
+            size_t cur = 0;
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            if (cur < (size_t(64) << 20)) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(64) << 20);
+            limit_set = true;
+        }
+        cudaStreamAttrValue av = {};
+        av.accessPolicyWindow.base_ptr = const_cast<double*>(std::max(M, Mt) - lo == n * n ? lo : M);
+        av.accessPolicyWindow.num_bytes = bytes;
+        av.accessPolicyWindow.hitRatio = 1.0f;
+        av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        l2_window = cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &av) == cudaSuccess;
+        cudaGetLastError();  // the window is an optimisation: ignore refusal
+    }
+
     const bool instrument = opts.x_star || opts.track_true_residual || opts.on_bidiag;
     std::vector<double> herr, htrue;
     double* d_xstar = nullptr;
@@ -634,9 +686,8 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
     }
     // ||A q + c b||  (instrumentation; not counted, lsqr.hpp:26-37)
     auto norm_pass = [&](const double* q, double c, double* dst) {
-        PassArgs na{A->A, A->ld, m, n, q, b_dev, nullptr, nullptr, c, B.part, 0, nullptr, 0, 0};
-        launch_pass(ctx, pp, na);
-        sum_strided_kernel<<<1, 32, 0, ctx->stream>>>(B.part + n, pp.grid, n + 1, B.scal);
+        op.pass(ctx, PassCall{q, b_dev, nullptr, nullptr, c, B.part, 0, nullptr});
+        sum_strided_kernel<<<1, 32, 0, ctx->stream>>>(B.part + n, grid, n + 1, B.scal);
         SLQ_LAUNCH_CHECK(ctx);
         allreduce_sum(ctx, B.scal, 1);
         sqrt_to_kernel<<<1, 32, 0, ctx->stream>>>(B.scal, dst);
@@ -664,10 +715,9 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
     // ---- init: u_hat = A x0 - b, z = A^T u_hat, ||u_hat||^2 (one pass)
     int64_t allreduces = 0;
     {
-        PassArgs ia{A->A, A->ld, m, n, x0, b_dev, B.u, nullptr, -1.0, B.part, 1, nullptr, 0, 0};
-        launch_pass(ctx, pp, ia);
+        op.pass(ctx, PassCall{x0, b_dev, B.u, nullptr, -1.0, B.part, 1, nullptr});
         reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 32)), 256, 0, ctx->stream>>>(
-            B.part, pp.grid, n + 1, B.zt, nullptr);
+            B.part, grid, n + 1, B.zt, nullptr);
         SLQ_LAUNCH_CHECK(ctx);
         allreduce_sum(ctx, B.zt, n + 1);
         if (ctx->comm) ++allreduces;
@@ -682,10 +732,9 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
     const int64_t init_allreduces = allreduces;
 
     auto enqueue_iteration = [&]() {
-        PassArgs ta{A->A, A->ld, m, n, B.p, B.u, B.u, &B.st->c_next, 0.0, B.part, 1, done_flag, 0, 0};
-        launch_pass(ctx, pp, ta);
+        op.pass(ctx, PassCall{B.p, B.u, B.u, &B.st->c_next, 0.0, B.part, 1, done_flag});
         reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 32)), 256, 0, ctx->stream>>>(
-            B.part, pp.grid, n + 1, B.zt, done_flag);
+            B.part, grid, n + 1, B.zt, done_flag);
         SLQ_LAUNCH_CHECK(ctx);
         allreduce_sum(ctx, B.zt, n + 1);
         MtzArgs ma{M, n, B.zt, B.v, B.vhat, B.part2, B.st, B.hist, 0};
@@ -724,13 +773,13 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
         constexpr int kBatch = 8;
         const bool use_graph = ctx->stream != nullptr;
         if (use_graph) {
-            const std::vector<uint64_t> key = {
-                reinterpret_cast<uint64_t>(A->A), static_cast<uint64_t>(m), static_cast<uint64_t>(n),
-                static_cast<uint64_t>(A->ld), reinterpret_cast<uint64_t>(b_dev), reinterpret_cast<uint64_t>(M),
-                reinterpret_cast<uint64_t>(Mt), reinterpret_cast<uint64_t>(x), reinterpret_cast<uint64_t>(B.u),
-                reinterpret_cast<uint64_t>(B.p), reinterpret_cast<uint64_t>(B.part), reinterpret_cast<uint64_t>(B.st),
-                reinterpret_cast<uint64_t>(B.hist), static_cast<uint64_t>(pp.grid), static_cast<uint64_t>(pp.R),
-                static_cast<uint64_t>(pp.S), reinterpret_cast<uint64_t>(ctx->comm), reinterpret_cast<uint64_t>(ctx->stream)};
+            std::vector<uint64_t> key = op.key();
+            const uint64_t extra[] = {
+                reinterpret_cast<uint64_t>(b_dev), reinterpret_cast<uint64_t>(M), reinterpret_cast<uint64_t>(Mt),
+                reinterpret_cast<uint64_t>(x), reinterpret_cast<uint64_t>(B.u), reinterpret_cast<uint64_t>(B.p),
+                reinterpret_cast<uint64_t>(B.part), reinterpret_cast<uint64_t>(B.st), reinterpret_cast<uint64_t>(B.hist),
+                reinterpret_cast<uint64_t>(ctx->comm), reinterpret_cast<uint64_t>(ctx->stream)};
+            key.insert(key.end(), std::begin(extra), std::end(extra));
             if (!ctx->lsqr_exec || ctx->lsqr_key != key) {
                 if (ctx->lsqr_exec) cudaGraphExecDestroy(ctx->lsqr_exec);
                 ctx->lsqr_exec = nullptr;
@@ -775,6 +824,12 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
         cudaFreeHost(hdone);
     }
     SLQ_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+    if (l2_window) {
+        cudaStreamAttrValue av = {};
+        av.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &av);
+        cudaGetLastError();
+    }
     SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, B.st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
     SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     float ms = 0.f;
@@ -800,26 +855,25 @@ void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const doubl
         for (size_t i = 0; i < htrue.size(); ++i) true_hist[i] = htrue[i];
 }
 
-double time_fused_pass(slq_ctx* ctx, const slq_dense* A, int reps) {
+double time_fused_pass(slq_ctx* ctx, const PassOp& op, int reps) {
     // Average device time of one K4 launch (steady-state iteration form),
     // CUDA events on the launching stream.
-    PassPlan pp = plan_pass(ctx, A);
-    const int64_t n = A->n, m = A->m;
+    const int64_t n = op.n, m = op.m;
     DevBuf part, pv, uv, cf;
-    double* dpart = static_cast<double*>(part.ensure(sizeof(double) * pp.grid * (n + 1)));
+    double* dpart = static_cast<double*>(part.ensure(sizeof(double) * op.grid() * (n + 1)));
     double* p = static_cast<double*>(pv.ensure(sizeof(double) * (n + 8)));
     double* u = static_cast<double*>(uv.ensure(sizeof(double) * std::max<int64_t>(1, m)));
     double* c = static_cast<double*>(cf.ensure(sizeof(double) * 8));
     SLQ_CUDA_CHECK(cudaMemsetAsync(p, 0, sizeof(double) * (n + 8), ctx->stream));
     SLQ_CUDA_CHECK(cudaMemsetAsync(u, 0, sizeof(double) * std::max<int64_t>(1, m), ctx->stream));
     SLQ_CUDA_CHECK(cudaMemsetAsync(c, 0, sizeof(double) * 8, ctx->stream));
-    PassArgs a{A->A, A->ld, m, n, p, u, u, c, 0.0, dpart, 1, nullptr, 0, 0};
-    launch_pass(ctx, pp, a);  // warm
+    const PassCall call{p, u, u, c, 0.0, dpart, 1, nullptr};
+    op.pass(ctx, call);  // warm
     cudaEvent_t e0, e1;
     SLQ_CUDA_CHECK(cudaEventCreate(&e0));
     SLQ_CUDA_CHECK(cudaEventCreate(&e1));
     SLQ_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
-    for (int r = 0; r < reps; ++r) launch_pass(ctx, pp, a);
+    for (int r = 0; r < reps; ++r) op.pass(ctx, call);
     SLQ_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
     SLQ_CUDA_CHECK(cudaEventSynchronize(e1));
     float ms = 0.f;
@@ -829,17 +883,15 @@ double time_fused_pass(slq_ctx* ctx, const slq_dense* A, int reps) {
     return ms * 1e-3 / std::max(reps, 1);
 }
 
-double backward_error_dev(slq_ctx* ctx, const slq_dense* A, const double* x, double a_norm) {
+double backward_error_dev(slq_ctx* ctx, const PassOp& op, const double* x, double a_norm) {
     // r = b - A x:  u_hat = A x - b = -r;  z = A^T u_hat = -A^T r
-    PassPlan pp = plan_pass(ctx, A);
-    const int64_t n = A->n;
-    DevBuf part, zt;
-    double* dpart = static_cast<double*>(part.ensure(sizeof(double) * pp.grid * (n + 1)));
-    double* dzt = static_cast<double*>(zt.ensure(sizeof(double) * (n + 1)));
-    PassArgs a{A->A, A->ld, A->m, n, x, nullptr, nullptr, nullptr, -1.0, dpart, 1, nullptr, 0, 0};
-    launch_pass(ctx, pp, a);
-    reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 32)), 256, 0, ctx->stream>>>(dpart, pp.grid, n + 1,
-                                                                                              dzt, nullptr);
+    const int64_t n = op.n;
+    Workspace& ws = ctx->ws;
+    double* dpart = static_cast<double*>(ws.lsqr_part.ensure(sizeof(double) * op.grid() * (n + 1)));
+    double* dzt = static_cast<double*>(ws.tmp.ensure(sizeof(double) * (n + 1)));
+    op.pass(ctx, PassCall{x, nullptr, nullptr, nullptr, -1.0, dpart, 1, nullptr});
+    reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 32)), 256, 0, ctx->stream>>>(dpart, op.grid(), n + 1,
+                                                                                             dzt, nullptr);
     SLQ_LAUNCH_CHECK(ctx);
     allreduce_sum(ctx, dzt, n + 1);
     std::vector<double> h(n + 1);

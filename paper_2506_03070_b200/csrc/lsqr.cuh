@@ -1,6 +1,9 @@
 // lsqr.cuh -- host side of the K4/K5 LSQR kernels.
 #pragma once
 
+#include <memory>
+#include <vector>
+
 #include "common.cuh"
 
 namespace slq {
@@ -11,6 +14,32 @@ namespace slq {
 //   x0  : device n-vector (initial guess);   x: device n-vector (output)
 // Histories (host, optional) as in the C-ABI.  With a communicator on ctx the
 // partial A^T u / ||u||^2 of every iteration is summed by one ncclAllReduce.
+// One HBM pass of the LSQR operator: u_hat = A p + c u (u_in == nullptr: u is
+// the right-hand side stored with A), z = A^T u_hat (per-CTA partials in
+// part[grid][n+1], the last entry holding ||u_hat||^2).  Dense (lsqr.cu) and
+// sparse CSR (sparse.cu) implementations.
+struct PassCall {
+    const double* p;
+    const double* u_in;
+    double* u_out;
+    const double* coef;  // device scalar c, or nullptr -> c_fixed
+    double c_fixed;
+    double* part;
+    int want_z;
+    const int* skip;     // nonzero -> no-op
+};
+
+struct PassOp {
+    int64_t m = 0, n = 0;
+    virtual ~PassOp() = default;
+    virtual int grid() const = 0;
+    virtual void pass(slq_ctx* ctx, const PassCall& c) const = 0;
+    virtual std::vector<uint64_t> key() const = 0;  // identity for the graph cache
+    virtual double pass_bytes() const = 0;          // algorithmic bytes of one pass
+};
+
+std::unique_ptr<PassOp> make_dense_op(slq_ctx* ctx, const slq_dense* A);
+
 struct LsqrOut {
     int64_t iterations = 0;
     int termination = SLQ_TERM_MAXITER;
@@ -20,15 +49,15 @@ struct LsqrOut {
     double backward_error = -1.0;
 };
 
-void lsqr_dev(slq_ctx* ctx, const slq_dense* A, const double* b_dev, const double* M, const double* Mt,
+void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* M, const double* Mt,
               const double* x0, double* x, const slq_solve_opts& opts, double* est_hist,
               double* err_hist, double* true_hist, LsqrOut& out);
 
 // Average seconds per fused-pass launch (K4), timed with CUDA events.
-double time_fused_pass(slq_ctx* ctx, const slq_dense* A, int reps);
+double time_fused_pass(slq_ctx* ctx, const PassOp& op, int reps);
 
 // ||A^T r|| / (a_norm ||r||) for r = b - A x (one fused pass + allreduce).
-double backward_error_dev(slq_ctx* ctx, const slq_dense* A, const double* x, double a_norm);
+double backward_error_dev(slq_ctx* ctx, const PassOp& op, const double* x, double a_norm);
 
 // comm.cu: in-place sum across ranks (no-op without a communicator).
 void allreduce_sum(slq_ctx* ctx, double* buf, int64_t count);

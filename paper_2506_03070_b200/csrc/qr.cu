@@ -76,41 +76,43 @@ struct PanelArgs {
 };
 
 // Point-to-point cluster reduction: warp 0 of every CTA pushes its L partials
-// into slot [me] of every CTA's inbox (DSMEM stores) and arrives (release,
-// cluster scope) on that CTA's mbarrier; each CTA then waits on its own
-// mbarrier (acquire) and sums the inbox in rank order -- one DSMEM hop instead
-// of a full cluster barrier.  inbox / mbar double-buffered by reduction parity:
-// a CTA can only rewrite an inbox two reductions later, after every CTA has
-// arrived for the reduction in between, i.e. after it finished reading.
+// into slot [me] of every CTA's inbox with st.async (DSMEM store that
+// completes bytes on the destination's mbarrier), so no cluster barrier and
+// no cluster-scope fence (which would invalidate L1) is needed; each CTA arms
+// its own mbarrier with the expected byte count, waits, and sums the inbox in
+// rank order.  inbox / mbar are double-buffered by reduction parity: a CTA
+// can only push reduction r+2 after every CTA armed (i.e. finished waiting
+// on) reduction r+1, so a buffer is never overwritten while being read.
 __device__ __forceinline__ void push_reduce(cg::cluster_group& cl, double (*inbox)[16][33], uint64_t* mbar, int r,
                                             int L, const double* mine, double* out) {
     const int p = r & 1;
     const unsigned phase = static_cast<unsigned>((r >> 1) & 1);
     const unsigned me = cl.block_rank(), nr = cl.num_blocks();
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        if (lane < L) {
-            const double v = mine[lane];
-            for (unsigned q = 0; q < nr; ++q) *cl.map_shared_rank(&inbox[p][me][lane], q) = v;
-        }
-        asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
-        __syncwarp();
-        if (lane < static_cast<int>(nr)) {
-            const unsigned local = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[p]));
-            unsigned remote;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local), "r"(static_cast<unsigned>(lane)));
-            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
+    const unsigned bar = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[p]));
+    if (threadIdx.x == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                     "r"(static_cast<unsigned>(nr * L * sizeof(double)))
+                     : "memory");
+    if (threadIdx.x < static_cast<unsigned>(L)) {
+        const double v = mine[threadIdx.x];
+        const unsigned slot = static_cast<unsigned>(__cvta_generic_to_shared(&inbox[p][me][threadIdx.x]));
+        for (unsigned q = 0; q < nr; ++q) {
+            unsigned rslot, rbar;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rslot) : "r"(slot), "r"(q));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rbar) : "r"(bar), "r"(q));
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(rslot),
+                         "l"(__double_as_longlong(v)), "r"(rbar)
+                         : "memory");
         }
     }
     {
-        const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[p]));
         unsigned ok = 0;
         do {
             asm volatile(
-                "{\n .reg .pred P;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n"
+                "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
                 " selp.u32 %0, 1, 0, P;\n}\n"
                 : "=r"(ok)
-                : "r"(a), "r"(phase)
+                : "r"(bar), "r"(phase)
                 : "memory");
         } while (!ok);
     }
@@ -125,67 +127,66 @@ __device__ __forceinline__ void push_reduce(cg::cluster_group& cl, double (*inbo
 __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
     constexpr int kWarps = kPanelThreads / 32;
     extern __shared__ __align__(16) double w[];  // [rpc][kWs] row-major panel slice
-    __shared__ double slot[2][40];
     __shared__ double red[kWarps][33];
+    __shared__ double mine[2][40];
     __shared__ double tot[40];
     __shared__ double Ts[kNbMax][kNbMax + 1];
     __shared__ double inbox[2][16][33];
     __shared__ uint64_t mbar[2];
     cg::cluster_group cl = cg::this_cluster();
     if (threadIdx.x == 0) {
-        const unsigned nrk = cl.num_blocks();
         for (int q = 0; q < 2; ++q) {
-            const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[q]));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(nrk) : "memory");
+            const unsigned ad = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[q]));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(ad) : "memory");
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    cl.sync();  // every CTA's mbarriers exist before anyone arrives remotely
-    int nred = 0;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned rank = cl.block_rank();
     const int kb = a.kb;
     const int64_t row0 = a.k0 + static_cast<int64_t>(rank) * a.rpc;  // global first row of this CTA
-    const int64_t nrows = (a.d - row0 < a.rpc ? (a.d - row0 > 0 ? a.d - row0 : 0) : a.rpc);
+    const int nrows = static_cast<int>(a.d - row0 < a.rpc ? (a.d - row0 > 0 ? a.d - row0 : 0) : a.rpc);
 
     // load panel slice: w[il][jj] = Y[row0+il, k0+jj]
-    for (int64_t e = tid; e < nrows * kb; e += kPanelThreads) {
+    for (int64_t e = tid; e < static_cast<int64_t>(nrows) * kb; e += kPanelThreads) {
         const int64_t jj = e / nrows, il = e - jj * nrows;
         w[il * kWs + jj] = a.Y[(a.k0 + jj) * a.ldy + row0 + il];
     }
-    __syncthreads();
+    cl.sync();  // slice loaded; every CTA's mbarriers exist before anyone arrives remotely
     const double rank_tol = *a.rank_tol;
-    int parity = 0;
+    int nred = 0;
 
-    // partial sigma of column 0 (rows > k0); lane 0 of each warp accumulates it
-    double sig = 0.0;
+    // Row ownership is fixed for the whole panel: warp w owns local rows w, w+16, ...
+    // (filtered to the rows below the current diagonal).  Every per-row step of a
+    // column is then warp-local and only the two reductions need block barriers.
+    double sig = 0.0;  // partial sigma of the current column (valid in every lane)
     {
-        const int64_t ib0 = (a.k0 - row0 + 1 > 0) ? a.k0 - row0 + 1 : 0;
-        for (int64_t il = ib0 + tid; il < nrows; il += kPanelThreads) {
-            const double v = w[il * kWs];
-            sig += v * v;
-        }
+        const int ib0 = static_cast<int>(a.k0 - row0 + 1 > 0 ? a.k0 - row0 + 1 : 0);
+        for (int il = wid + 16 * lane; il < nrows; il += 16 * 32)
+            if (il >= ib0) sig += w[il * kWs] * w[il * kWs];
         for (int o = 16; o > 0; o >>= 1) sig += __shfl_xor_sync(0xffffffffu, sig, o);
     }
 
     for (int kk = 0; kk < kb; ++kk) {
-        const int64_t gk = a.k0 + kk;           // global diagonal row
-        const int64_t lk = gk - row0;           // local index of row gk (may be outside)
+        const int64_t gk = a.k0 + kk;                 // global diagonal row
+        const int lk = static_cast<int>(gk - row0);   // local index of row gk (may be outside)
         const bool owner = lk >= 0 && lk < nrows;
-        const int64_t ib = lk + 1 > 0 ? lk + 1 : 0;  // first local row strictly below gk
+        const int ib = lk + 1 > 0 ? lk + 1 : 0;       // first local row strictly below gk
+        const int i0 = wid + 16 * ((ib - wid + 15 > 0 ? ib - wid + 15 : 0) / 16);  // first owned row >= ib
 
-        // (a) sigma = sum_{i>gk} w_ik^2 (accumulated by the previous update), x0 = w[gk][kk]
+        // (a) sigma = sum_{i>gk} w_ik^2, x0 = w[gk][kk]: block then cluster reduction
         if (lane == 0) red[wid][0] = sig;
         __syncthreads();
-        if (tid == 0) {
-            double t = 0.0;
-            for (int q = 0; q < kWarps; ++q) t += red[q][0];
-            slot[parity][0] = t;
-            slot[parity][1] = owner ? w[lk * kWs + kk] : 0.0;
+        if (wid == 0) {
+            double t = (lane < kWarps) ? red[lane][0] : 0.0;
+            for (int o = 8; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (lane == 0) {
+                mine[0][0] = t;
+                mine[0][1] = owner ? w[lk * kWs + kk] : 0.0;
+            }
+            __syncwarp();
         }
-        __syncthreads();
-        push_reduce(cl, inbox, mbar, nred++, 2, slot[parity], tot);
-        parity ^= 1;
+        push_reduce(cl, inbox, mbar, nred++, 2, mine[0], tot);
         const double sigma = tot[0], x0 = tot[1];
         const double normx = sqrt(x0 * x0 + sigma);
         if (normx < rank_tol || normx == 0.0) {
@@ -196,41 +197,54 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
         const double beta = (x0 > 0.0) ? -normx : normx;
         const double v0 = x0 - beta;
         const double tau = (beta - x0) / beta;
-        // (b) scale the reflector below the diagonal; R diagonal = beta
-        for (int64_t il = ib + tid; il < nrows; il += kPanelThreads) w[il * kWs + kk] /= v0;
-        __syncthreads();
+        // (b) scale the reflector below the diagonal (each warp its own rows); R diagonal = beta
+        for (int il = i0 + 16 * lane; il < nrows; il += 16 * 32) w[il * kWs + kk] /= v0;
+        __syncwarp();
         if (owner && tid == 0) w[lk * kWs + kk] = beta;
 
         // (c) g_jj = w[gk][jj] + sum_{i>gk} w[i][jj] v_i for every other panel column:
         //     jj > kk: the reference's s_j (qr.hpp:51-53); jj < kk: v_jj^T v_kk (for T)
         {
-            double acc = 0.0;
-            if (lane < kb)
-                for (int64_t il = ib + wid; il < nrows; il += kWarps) acc += w[il * kWs + lane] * w[il * kWs + kk];
-            red[wid][lane] = acc;
+            double acc0 = 0.0, acc1 = 0.0;
+            if (lane < kb) {
+                int il = i0;
+                for (; il + 16 < nrows; il += 32) {
+                    acc0 += w[il * kWs + lane] * w[il * kWs + kk];
+                    acc1 += w[(il + 16) * kWs + lane] * w[(il + 16) * kWs + kk];
+                }
+                if (il < nrows) acc0 += w[il * kWs + lane] * w[il * kWs + kk];
+            }
+            red[wid][lane] = acc0 + acc1;
             __syncthreads();
-            if (tid < 32) {
+            if (wid == 0) {
                 double t = 0.0;
-                for (int q = 0; q < kWarps; ++q) t += red[q][tid];
-                if (owner && tid < kb && tid != kk) t += w[lk * kWs + tid];
-                slot[parity][tid] = t;
+                for (int q = 0; q < kWarps; ++q) t += red[q][lane];
+                if (owner && lane < kb && lane != kk) t += w[lk * kWs + lane];
+                mine[1][lane] = t;
+                __syncwarp();
             }
         }
-        __syncthreads();
-        push_reduce(cl, inbox, mbar, nred++, kb, slot[parity], tot);
-        parity ^= 1;
+        push_reduce(cl, inbox, mbar, nred++, kb, mine[1], tot);
         // (d) apply H_kk to the remaining panel columns; lane kk+1 also sums the
         //     squares of its updated entries below the next diagonal (next sigma)
         sig = 0.0;
         {
             const int jj = lane;
-            const int64_t lk1 = lk + 1;  // local index of the next diagonal row
+            const int lk1 = lk + 1;
             if (jj > kk && jj < kb) {
                 const double sj = tot[jj] * tau;
-                for (int64_t il = ib + wid; il < nrows; il += kWarps) {
-                    const double nv = w[il * kWs + jj] - sj * w[il * kWs + kk];
-                    w[il * kWs + jj] = nv;
-                    if (jj == kk + 1 && il != lk1) sig += nv * nv;
+                int il = i0;
+                for (; il + 16 < nrows; il += 32) {
+                    const double n0 = w[il * kWs + jj] - sj * w[il * kWs + kk];
+                    const double n1 = w[(il + 16) * kWs + jj] - sj * w[(il + 16) * kWs + kk];
+                    w[il * kWs + jj] = n0;
+                    w[(il + 16) * kWs + jj] = n1;
+                    if (jj == kk + 1) sig += (il != lk1 ? n0 * n0 : 0.0) + (il + 16 != lk1 ? n1 * n1 : 0.0);
+                }
+                if (il < nrows) {
+                    const double n0 = w[il * kWs + jj] - sj * w[il * kWs + kk];
+                    w[il * kWs + jj] = n0;
+                    if (jj == kk + 1 && il != lk1) sig += n0 * n0;
                 }
                 if (owner && wid == 0) w[lk * kWs + jj] -= sj;
             }
@@ -240,7 +254,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
         if (rank == 0) {
             if (tid < kk) {
                 double t = 0.0;
-                for (int b = tid; b < kk; ++b) t += Ts[tid][b] * tot[b];
+                for (int b2 = tid; b2 < kk; ++b2) t += Ts[tid][b2] * tot[b2];
                 Ts[tid][kk] = -tau * t;
             }
             if (tid == 0) {
@@ -248,10 +262,10 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
                 a.tau[gk] = tau;
             }
         }
-        __syncthreads();
     }
+    __syncthreads();
     // write back the factored slice and T
-    for (int64_t e = tid; e < nrows * kb; e += kPanelThreads) {
+    for (int64_t e = tid; e < static_cast<int64_t>(nrows) * kb; e += kPanelThreads) {
         const int64_t jj = e / nrows, il = e - jj * nrows;
         a.Y[(a.k0 + jj) * a.ldy + row0 + il] = w[il * kWs + jj];
     }
