@@ -128,6 +128,41 @@ int slq_spmm_csc_dense(slq_ctx* ctx, int64_t d, int64_t m, const int64_t* row_in
                        const double* values, const int64_t* col_pointers, const double* A,
                        int64_t n, int64_t lda, double* Y);
 
+/* ------------------------------------------------ device sparse matrix -- */
+
+/* A row block of a sparse A in CSR on the device (int64 row pointers, int32
+ * column indices, fp64 values).  Replaces the CscMatrix operand of
+ * sketch.hpp:298, csc_matrix.hpp:71-136 and lsqr.hpp:198-212, and its row
+ * distribution csc_row_block / distribute (csc_matrix.hpp:139-152,
+ * distsim.hpp:235-246). */
+typedef struct slq_sparse slq_sparse;
+
+/* From the reference's host CSC layout (col_pointers[n+1], row_indices[nnz]
+ * int64, values[nnz] fp64) of this rank's rows [0, m), first row = global
+ * row row_begin; b (m, may be NULL) is the right-hand side of these rows. */
+int slq_sparse_upload_csc(slq_ctx* ctx, int64_t m, int64_t n, const int64_t* col_pointers,
+                          const int64_t* row_indices, const double* values, const double* b,
+                          int64_t row_begin, slq_sparse** out);
+/* Allocates the device CSR (with bulk-copy slack) for the caller to fill in
+ * place: row_ptr[m+1], col_idx[nnz] (sorted within rows), values[nnz],
+ * b[m] when with_b. */
+int slq_sparse_create_csr(slq_ctx* ctx, int64_t m, int64_t n, int64_t nnz, int64_t row_begin, int with_b,
+                          slq_sparse** out, int64_t** row_ptr, int32_t** col_idx, double** values,
+                          double** b);
+int slq_sparse_set_rhs(slq_sparse* A, const double* b_host);
+int slq_sparse_free(slq_sparse* A);
+
+/* sketch.hpp:298 + :304 for a sparse operand: Y = S A (d x n, column-major)
+ * and Sb, bit-identical to spmm(csc, csc) / matvec(csc) on one GPU. */
+int slq_sketch_apply_sparse(slq_ctx* ctx, const slq_sparse* A, int64_t d, int64_t zeta, uint64_t seed,
+                            double* Y, double* Sb);
+
+/* csc_matrix.hpp:123-136 spmm(csc, csc): Y = S A for a caller CSC sketch S
+ * (d x m, +-v values) and a host CSC A (m x n); reference order (bit-identical). */
+int slq_spmm_csc_csc(slq_ctx* ctx, int64_t d, int64_t m, const int64_t* s_rows, const double* s_vals,
+                     const int64_t* s_colptr, int64_t n, const int64_t* a_colptr, const int64_t* a_rows,
+                     const double* a_vals, double* Y);
+
 /* ------------------------------------------------------ preconditioner -- */
 
 /* qr.hpp:21-89 householder_qr.  Y d x n column-major (ldy >= d); Q (d x n,
@@ -202,6 +237,11 @@ int slq_lsqr(slq_ctx* ctx, const slq_dense* A, const double* M, const double* b,
              const slq_solve_opts* opts, double* x_out, slq_report* report,
              double* residual_estimate, double* iterates_error, double* residual_true);
 
+/* lsqr.hpp:198-202 / :208-212 -- LSQR over a sparse operand (arguments as slq_lsqr). */
+int slq_lsqr_sparse(slq_ctx* ctx, const slq_sparse* A, const double* M, const double* b, const double* x0,
+                    const slq_solve_opts* opts, double* x_out, slq_report* report,
+                    double* residual_estimate, double* iterates_error, double* residual_true);
+
 /* ---------------------------------------------------- whole pipeline --- */
 
 typedef struct {
@@ -220,6 +260,11 @@ typedef struct {
 int slq_solve(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed,
               const slq_solve_opts* opts, double* x_out, slq_report* report,
               slq_phase_times* times, double* residual_estimate);
+
+/* slq_solve for a sparse operand (BASELINE config C4). */
+int slq_solve_sparse(slq_ctx* ctx, const slq_sparse* A, int64_t d, int64_t zeta, uint64_t seed,
+                     const slq_solve_opts* opts, double* x_out, slq_report* report,
+                     slq_phase_times* times, double* residual_estimate);
 
 /* Kernel timing for the roofline report (CUDA events on the context stream):
  * out[0] = seconds per K4 fused LSQR pass launch (average over reps),

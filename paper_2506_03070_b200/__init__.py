@@ -27,6 +27,7 @@ from .api import (  # noqa: F401
     SketchParams,
     SolveOptions,
     SolveReport,
+    SparseDeviceMatrix,
     SparseSignSketch,
     Termination,
     Unsupported,

@@ -114,6 +114,16 @@ _SIGS = {
     "slq_lsqr": (ct.c_int, [vp, vp, dp, dp, dp, ct.POINTER(SolveOpts), dp, ct.POINTER(Report), dp, dp, dp]),
     "slq_solve": (ct.c_int, [vp, vp, i64, i64, u64, ct.POINTER(SolveOpts), dp, ct.POINTER(Report),
                              ct.POINTER(PhaseTimes), dp]),
+    "slq_sparse_upload_csc": (ct.c_int, [vp, i64, i64, ip, ip, dp, dp, i64, ct.POINTER(vp)]),
+    "slq_sparse_create_csr": (ct.c_int, [vp, i64, i64, i64, i64, ct.c_int, ct.POINTER(vp), ct.POINTER(vp),
+                                         ct.POINTER(vp), ct.POINTER(vp), ct.POINTER(vp)]),
+    "slq_sparse_set_rhs": (ct.c_int, [vp, dp]),
+    "slq_sparse_free": (ct.c_int, [vp]),
+    "slq_spmm_csc_csc": (ct.c_int, [vp, i64, i64, ip, dp, ip, i64, ip, ip, dp, dp]),
+    "slq_sketch_apply_sparse": (ct.c_int, [vp, vp, i64, i64, u64, dp, dp]),
+    "slq_lsqr_sparse": (ct.c_int, [vp, vp, dp, dp, dp, ct.POINTER(SolveOpts), dp, ct.POINTER(Report), dp, dp, dp]),
+    "slq_solve_sparse": (ct.c_int, [vp, vp, i64, i64, u64, ct.POINTER(SolveOpts), dp, ct.POINTER(Report),
+                                    ct.POINTER(PhaseTimes), dp]),
     "slq_time_kernels": (ct.c_int, [vp, vp, i64, i64, u64, ct.c_int, dp]),
     "slq_solve_host": (ct.c_int, [vp, dp, i64, i64, i64, dp, i64, i64, i64, u64, ct.POINTER(SolveOpts), dp,
                                   ct.POINTER(Report), ct.POINTER(PhaseTimes), dp]),

@@ -85,6 +85,10 @@ def _check(code: int) -> None:
         raise _STATUS.get(code, Error)(msg)
 
 
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
 def _d(a):
     return None if a is None else a.ctypes.data_as(C.dp)
 
@@ -367,8 +371,18 @@ class SketchParams:
 
 
 def apply(S: SparseSignSketch, A, ctx=None) -> np.ndarray:
-    """sketch.hpp:297 apply(SparseSignSketch, DenseMatrix) -> csc_matrix.hpp:103-120.
+    """sketch.hpp:297 apply(SparseSignSketch, DenseMatrix) -> csc_matrix.hpp:103-120,
+    sketch.hpp:298 apply(SparseSignSketch, CscMatrix) -> csc_matrix.hpp:123-136.
     Bit-identical to the reference (same accumulation order, IEEE mul+add)."""
+    if isinstance(A, CscMatrix):
+        M = S.matrix
+        if M.cols != A.rows:
+            raise DimensionMismatch("spmm(csc,csc): inner dimensions disagree")
+        Y = np.zeros((M.rows, A.cols), order="F")
+        _check(C.lib.slq_spmm_csc_csc(_ctx(ctx).handle, M.rows, M.cols, _i(M.row_indices), _d(M.values),
+                                      _i(M.col_pointers), A.cols, _i(_i64(A.col_pointers)), _i(_i64(A.row_indices)),
+                                      _d(_vec(A.values)), _d(Y)))
+        return Y
     A = _f64(A)
     m, n = A.shape
     M = S.matrix
@@ -541,6 +555,57 @@ class DeviceMatrix:
         return Y, Sb
 
 
+class SparseDeviceMatrix:
+    """A row block of a sparse A resident in HBM as CSR (the reference's
+    CscMatrix operand, converted on the device)."""
+
+    def __init__(self, handle, m, n, row_begin, ctx, owner=None):
+        self.handle = handle
+        self.m, self.n, self.row_begin = m, n, row_begin
+        self.ctx = ctx
+        self._owner = owner
+
+    @classmethod
+    def from_csc(cls, A: CscMatrix, b=None, row_begin=0, ctx=None):
+        ctx = _ctx(ctx)
+        cp, rw, vl = _i64(A.col_pointers), _i64(A.row_indices), _vec(A.values)
+        bb = _vec(b) if b is not None else None
+        h = C.vp()
+        _check(C.lib.slq_sparse_upload_csc(ctx.handle, A.rows, A.cols, _i(cp), _i(rw), _d(vl), _d(bb), row_begin,
+                                           ct.byref(h)))
+        return cls(h, A.rows, A.cols, row_begin, ctx)
+
+    @classmethod
+    def create_csr(cls, m, n, nnz, row_begin=0, with_b=True, ctx=None):
+        """Allocate a device CSR to be filled in place; returns (matrix, (row_ptr, col_idx, values, b) pointers)."""
+        ctx = _ctx(ctx)
+        h = C.vp()
+        ptrs = [C.vp() for _ in range(4)]
+        _check(C.lib.slq_sparse_create_csr(ctx.handle, m, n, nnz, row_begin, int(with_b), ct.byref(h),
+                                           *[ct.byref(p) for p in ptrs]))
+        return cls(h, m, n, row_begin, ctx), tuple(p.value for p in ptrs)
+
+    def set_rhs(self, b):
+        _check(C.lib.slq_sparse_set_rhs(self.handle, _d(_vec(b))))
+
+    def free(self):
+        if self.handle:
+            C.lib.slq_sparse_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def sketch(self, d, zeta, seed):
+        Y = np.zeros((d, self.n), order="F")
+        Sb = np.zeros(d)
+        _check(C.lib.slq_sketch_apply_sparse(self.ctx.handle, self.handle, d, zeta, seed & (2**64 - 1), _d(Y), _d(Sb)))
+        return Y, Sb
+
+
 # ------------------------------------------------------------------- LSQR
 
 
@@ -587,6 +652,8 @@ def _report(r: C.Report, est, err, tru) -> SolveReport:
 
 def _lsqr(A, P, b, x0, opts, one_sync, ctx):
     ctx = _ctx(ctx)
+    if isinstance(A, (CscMatrix, SparseDeviceMatrix)):
+        return _lsqr_sparse(A, P, b, x0, opts, one_sync, ctx)
     if isinstance(A, DeviceMatrix):
         dm = A
         m, n = A.m, A.n
@@ -614,6 +681,34 @@ def _lsqr(A, P, b, x0, opts, one_sync, ctx):
     rep = C.Report()
     _check(C.lib.slq_lsqr(ctx.handle, dm.handle, _d(M), _d(bb), _d(x0), ct.byref(co), _d(x), ct.byref(rep),
                           _d(est), _d(err), _d(tru)))
+    del keep
+    return x, _report(rep, est, err, tru)
+
+
+def _lsqr_sparse(A, P, b, x0, opts, one_sync, ctx):
+    if isinstance(A, CscMatrix):
+        bb = _vec(b)
+        if bb.size != A.rows:
+            raise DimensionMismatch("rmatvec(csc): length mismatch")
+        dm = SparseDeviceMatrix.from_csc(A, bb, ctx=ctx)
+        bb = None
+    else:
+        dm = A
+        bb = _vec(b) if b is not None else None
+    n = dm.n
+    M = _f64(P.M if isinstance(P, Preconditioner) else P)
+    if M.shape != (n, n):
+        raise DimensionMismatch("tri_upper_matvec")
+    x0 = _vec(x0)
+    if x0.size != n:
+        raise DimensionMismatch("matvec(csc): length mismatch")
+    co, keep = _opts(opts, one_sync, n)
+    maxit = max(int(co.maxit), 0)
+    est, err, tru = np.zeros(maxit + 2), np.zeros(maxit + 2), np.zeros(maxit + 2)
+    x = np.zeros(n)
+    rep = C.Report()
+    _check(C.lib.slq_lsqr_sparse(ctx.handle, dm.handle, _d(M), _d(bb), _d(x0), ct.byref(co), _d(x), ct.byref(rep),
+                                 _d(est), _d(err), _d(tru)))
     del keep
     return x, _report(rep, est, err, tru)
 
@@ -648,7 +743,10 @@ def solve(A, d, zeta, seed, opts: SolveOptions | None = None, b=None, one_sync=T
     lsqr.hpp:175).  ``A`` is a DeviceMatrix (this rank's rows; b stored with
     it) or a host array (then ``b`` is required).  Returns (x, report, phase_times)."""
     ctx = _ctx(ctx)
-    if not isinstance(A, DeviceMatrix):
+    sparse = isinstance(A, (CscMatrix, SparseDeviceMatrix))
+    if isinstance(A, CscMatrix):
+        A = SparseDeviceMatrix.from_csc(A, b, ctx=ctx)
+    elif not sparse and not isinstance(A, DeviceMatrix):
         A = DeviceMatrix.from_numpy(A, b, ctx=ctx)
     co, keep = _opts(opts, one_sync, A.n)
     maxit = max(int(co.maxit), 0)
@@ -656,7 +754,8 @@ def solve(A, d, zeta, seed, opts: SolveOptions | None = None, b=None, one_sync=T
     x = np.zeros(A.n)
     rep = C.Report()
     pt = C.PhaseTimes()
-    _check(C.lib.slq_solve(ctx.handle, A.handle, d, zeta, seed & (2**64 - 1), ct.byref(co), _d(x), ct.byref(rep),
-                           ct.byref(pt), _d(est)))
+    fn = C.lib.slq_solve_sparse if sparse else C.lib.slq_solve
+    _check(fn(ctx.handle, A.handle, d, zeta, seed & (2**64 - 1), ct.byref(co), _d(x), ct.byref(rep), ct.byref(pt),
+              _d(est)))
     del keep
     return x, _report(rep, est, None, None), pt.as_dict()

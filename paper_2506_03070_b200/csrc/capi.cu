@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -16,6 +17,7 @@
 #include "lsqr.cuh"
 #include "qr.cuh"
 #include "sketch.cuh"
+#include "sparse.cuh"
 
 namespace {
 
@@ -209,23 +211,58 @@ void fill_report(slq_report* r, const slq::LsqrOut& o) {
     r->backward_error = o.backward_error;
 }
 
-int run_solve(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed, const slq_solve_opts* opts_in,
+// The dense or sparse operand of one rank: how to sketch it and how to make its LSQR pass.
+struct Operand {
+    int64_t m = 0, n = 0;
+    // writes Y_aug (d x (n+1), column-major) = S [A b]; returns seconds spent generating S (0 if fused)
+    std::function<void(double* Yaug, int64_t d, int64_t zeta, uint64_t seed, Timer* t_gen)> sketch;
+    std::function<std::unique_ptr<slq::PassOp>()> make_op;
+};
+
+Operand dense_operand(slq_ctx* ctx, const slq_dense* A) {
+    Operand o;
+    o.m = A->m;
+    o.n = A->n;
+    o.sketch = [ctx, A](double* Yaug, int64_t d, int64_t zeta, uint64_t seed, Timer* t_gen) {
+        slq::Workspace& ws = ctx->ws;
+        const int64_t m = A->m;
+        uint32_t* compact = static_cast<uint32_t*>(ws.compact.ensure(sizeof(uint32_t) * std::max<int64_t>(1, m * zeta)));
+        int64_t* work = zeta > 32 ? static_cast<int64_t*>(ws.tmp.ensure(sizeof(int64_t) * m * zeta)) : nullptr;
+        slq::generate_sparse_sign_dev(ctx, d, zeta, seed, A->row_begin, m, compact, work, nullptr, nullptr, nullptr);
+        if (t_gen) SLQ_CUDA_CHECK(cudaEventRecord(t_gen->e, ctx->stream));
+        slq::sketch_apply_compact_dev(ctx, A, d, compact, nullptr, zeta, 1.0 / std::sqrt(static_cast<double>(zeta)),
+                                      false, Yaug);
+    };
+    o.make_op = [ctx, A] { return slq::make_dense_op(ctx, A); };
+    return o;
+}
+
+Operand sparse_operand(slq_ctx* ctx, const slq_sparse* A) {
+    Operand o;
+    o.m = A->m;
+    o.n = A->n;
+    o.sketch = [ctx, A](double* Yaug, int64_t d, int64_t zeta, uint64_t seed, Timer* t_gen) {
+        if (t_gen) SLQ_CUDA_CHECK(cudaEventRecord(t_gen->e, ctx->stream));
+        slq::sketch_apply_sparse_dev(ctx, A, d, zeta, seed, Yaug);
+    };
+    o.make_op = [ctx, A] { return slq::make_sparse_op(ctx, A); };
+    return o;
+}
+
+int run_solve(slq_ctx* ctx, const Operand& A, int64_t d, int64_t zeta, uint64_t seed, const slq_solve_opts* opts_in,
               double* x_out, slq_report* report, slq_phase_times* times, double* est) {
     return guarded([&] {
-        need(ctx && A, SLQ_INVALID_ARG, "solve: null handle");
+        need(ctx != nullptr, SLQ_INVALID_ARG, "solve: null handle");
         slq_solve_opts opts;
         if (opts_in) opts = *opts_in;
         else slq_solve_opts_default(&opts);
-        const int64_t n = A->n;
+        const int64_t n = A.n;
         need(n >= 1, SLQ_INVALID_DIMS, "solve: n < 1");
         need(d > n, SLQ_INVALID_DIMS, "SketchParams: need n < d <= m");
         need(zeta >= 1 && zeta <= d, SLQ_INVALID_SPARSITY, "SketchParams: need 1 <= zeta <= d");
         const int64_t launches0 = ctx->launches, nccl0 = ctx->nccl_calls;
         slq::Workspace& ws = ctx->ws;
         double* Yaug = static_cast<double*>(ws.yaug.ensure(sizeof(double) * d * (n + 1)));
-        const int64_t m = A->m;
-        uint32_t* compact = static_cast<uint32_t*>(ws.compact.ensure(sizeof(uint32_t) * std::max<int64_t>(1, m * zeta)));
-        int64_t* work = zeta > 32 ? static_cast<int64_t*>(ws.tmp.ensure(sizeof(int64_t) * m * zeta)) : nullptr;
 
         // SLQ_TRACE=1: host timestamps per phase on stderr (diagnostics)
         static const bool trace = std::getenv("SLQ_TRACE") != nullptr;
@@ -236,11 +273,8 @@ int run_solve(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_
                              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
         };
         Timer t0(ctx->stream);
-        slq::generate_sparse_sign_dev(ctx, d, zeta, seed, A->row_begin, m, compact, work, nullptr, nullptr, nullptr);
-        mark("generate");
         Timer t1(ctx->stream);
-        slq::sketch_apply_compact_dev(ctx, A, d, compact, nullptr, zeta, 1.0 / std::sqrt(static_cast<double>(zeta)),
-                                      false, Yaug);
+        A.sketch(Yaug, d, zeta, seed, &t1);
         mark("apply");
         Timer t2(ctx->stream);
         slq::reduce_sum_root(ctx, Yaug, d * (n + 1));
@@ -277,7 +311,7 @@ int run_solve(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_
         Timer t5(ctx->stream);
         double* x = static_cast<double*>(ws.xbuf.ensure(sizeof(double) * (n + 8)));
         slq::LsqrOut lo;
-        auto op = slq::make_dense_op(ctx, A);
+        auto op = A.make_op();
         slq::lsqr_dev(ctx, *op, nullptr, P.M, P.Mt, P.x0, x, opts, est, nullptr, nullptr, lo);
         mark("lsqr");
         Timer t6(ctx->stream);
@@ -729,7 +763,193 @@ int slq_lsqr(slq_ctx* ctx, const slq_dense* A, const double* M, const double* b,
 
 int slq_solve(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed, const slq_solve_opts* opts,
               double* x_out, slq_report* report, slq_phase_times* times, double* residual_estimate) {
-    return run_solve(ctx, A, d, zeta, seed, opts, x_out, report, times, residual_estimate);
+    if (!ctx || !A) {
+        g_last_error = "solve: null handle";
+        return SLQ_INVALID_ARG;
+    }
+    return run_solve(ctx, dense_operand(ctx, A), d, zeta, seed, opts, x_out, report, times, residual_estimate);
+}
+
+int slq_solve_sparse(slq_ctx* ctx, const slq_sparse* A, int64_t d, int64_t zeta, uint64_t seed,
+                     const slq_solve_opts* opts, double* x_out, slq_report* report, slq_phase_times* times,
+                     double* residual_estimate) {
+    if (!ctx || !A) {
+        g_last_error = "solve_sparse: null handle";
+        return SLQ_INVALID_ARG;
+    }
+    if (!A->b) {
+        g_last_error = "solve_sparse: the matrix has no right-hand side (slq_sparse_set_rhs)";
+        return SLQ_INVALID_ARG;
+    }
+    return run_solve(ctx, sparse_operand(ctx, A), d, zeta, seed, opts, x_out, report, times, residual_estimate);
+}
+
+int slq_sparse_upload_csc(slq_ctx* ctx, int64_t m, int64_t n, const int64_t* col_pointers, const int64_t* row_indices,
+                          const double* values, const double* b, int64_t row_begin, slq_sparse** out) {
+    return guarded([&] {
+        need(ctx && out && col_pointers, SLQ_INVALID_ARG, "sparse_upload_csc: null argument");
+        need(m >= 0 && n >= 0 && row_begin >= 0, SLQ_INVALID_DIMS, "sparse_upload_csc: bad shape");
+        need(n < (int64_t(1) << 31), SLQ_UNSUPPORTED, "sparse_upload_csc: n >= 2^31");
+        const int64_t nnz = col_pointers[n];
+        for (int64_t e = 0; e < nnz; ++e)
+            if (row_indices[e] < 0 || row_indices[e] >= m) slq::fail(SLQ_INVALID_ARG, "sparse_upload_csc: row index out of range");
+        SLQ_CUDA_CHECK(cudaSetDevice(ctx->device));
+        auto* A = new slq_sparse();
+        A->ctx = ctx;
+        A->m = m;
+        A->n = n;
+        A->nnz = nnz;
+        A->row_begin = row_begin;
+        try {
+            slq::sparse_alloc(ctx, A, true);
+            slq::sparse_from_csc(ctx, A, col_pointers, row_indices, values);
+            if (b) SLQ_CUDA_CHECK(cudaMemcpy(A->b, b, sizeof(double) * m, cudaMemcpyHostToDevice));
+            else {
+                cudaFree(A->b);
+                A->b = nullptr;
+            }
+        } catch (...) {
+            slq::sparse_free(A);
+            delete A;
+            throw;
+        }
+        *out = A;
+    });
+}
+
+int slq_sparse_create_csr(slq_ctx* ctx, int64_t m, int64_t n, int64_t nnz, int64_t row_begin, int with_b,
+                          slq_sparse** out, int64_t** row_ptr, int32_t** col_idx, double** values, double** b) {
+    return guarded([&] {
+        need(ctx && out, SLQ_INVALID_ARG, "sparse_create_csr: null argument");
+        need(m >= 0 && n >= 0 && nnz >= 0 && row_begin >= 0, SLQ_INVALID_DIMS, "sparse_create_csr: bad shape");
+        SLQ_CUDA_CHECK(cudaSetDevice(ctx->device));
+        auto* A = new slq_sparse();
+        A->ctx = ctx;
+        A->m = m;
+        A->n = n;
+        A->nnz = nnz;
+        A->row_begin = row_begin;
+        try {
+            slq::sparse_alloc(ctx, A, with_b != 0);
+            SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            slq::sparse_free(A);
+            delete A;
+            throw;
+        }
+        *out = A;
+        if (row_ptr) *row_ptr = A->rowptr;
+        if (col_idx) *col_idx = A->colidx;
+        if (values) *values = A->vals;
+        if (b) *b = A->b;
+    });
+}
+
+int slq_sparse_set_rhs(slq_sparse* A, const double* b) {
+    return guarded([&] {
+        need(A != nullptr, SLQ_INVALID_ARG, "null matrix");
+        if (!A->b) {
+            SLQ_CUDA_CHECK(cudaMalloc(&A->b, sizeof(double) * (A->m + slq::kSparseRowPad)));
+            SLQ_CUDA_CHECK(cudaMemset(A->b, 0, sizeof(double) * (A->m + slq::kSparseRowPad)));
+        }
+        if (b) SLQ_CUDA_CHECK(cudaMemcpy(A->b, b, sizeof(double) * A->m, cudaMemcpyHostToDevice));
+    });
+}
+
+int slq_sparse_free(slq_sparse* A) {
+    return guarded([&] {
+        if (!A) return;
+        cudaStreamSynchronize(A->ctx->stream);
+        slq::sparse_free(A);
+        delete A;
+    });
+}
+
+int slq_sketch_apply_sparse(slq_ctx* ctx, const slq_sparse* A, int64_t d, int64_t zeta, uint64_t seed, double* Y,
+                            double* Sb) {
+    return guarded([&] {
+        need(ctx && A, SLQ_INVALID_ARG, "sketch_apply_sparse: null handle");
+        const int64_t n = A->n;
+        double* Yaug = static_cast<double*>(ctx->ws.yaug.ensure(sizeof(double) * d * (n + 1)));
+        slq::sketch_apply_sparse_dev(ctx, A, d, zeta, seed, Yaug);
+        slq::allreduce_sum(ctx, Yaug, d * (n + 1));
+        if (Y) SLQ_CUDA_CHECK(cudaMemcpyAsync(Y, Yaug, sizeof(double) * d * n, cudaMemcpyDeviceToHost, ctx->stream));
+        if (Sb) SLQ_CUDA_CHECK(cudaMemcpyAsync(Sb, Yaug + d * n, sizeof(double) * d, cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int slq_spmm_csc_csc(slq_ctx* ctx, int64_t d, int64_t m, const int64_t* s_rows, const double* s_vals,
+                     const int64_t* s_colptr, int64_t n, const int64_t* a_colptr, const int64_t* a_rows,
+                     const double* a_vals, double* Y) {
+    return guarded([&] {
+        need(ctx && s_colptr && a_colptr && Y, SLQ_INVALID_ARG, "spmm_csc_csc: null argument");
+        const int64_t snnz = s_colptr[m];
+        double val = 0.0;
+        int64_t zmax = 1;
+        for (int64_t j = 0; j < m; ++j) zmax = std::max(zmax, s_colptr[j + 1] - s_colptr[j]);
+        for (int64_t e = 0; e < snnz; ++e) {
+            const double a = std::fabs(s_vals[e]);
+            if (e == 0) val = a;
+            else if (a != val) slq::fail(SLQ_UNSUPPORTED, "spmm: device path needs +-v sketch values");
+            if (s_rows[e] < 0 || s_rows[e] >= d) slq::fail(SLQ_INVALID_ARG, "spmm: row index out of range");
+        }
+        slq_sparse* As = nullptr;
+        int st = slq_sparse_upload_csc(ctx, m, n, a_colptr, a_rows, a_vals, nullptr, 0, &As);
+        if (st != SLQ_OK) slq::fail(st, g_last_error);
+        struct Free {
+            slq_sparse* p;
+            ~Free() { slq_sparse_free(p); }
+        } fr{As};
+        slq::DevBuf drows, dvals, dcp, dcomp, dY;
+        int64_t* r = static_cast<int64_t*>(drows.ensure(sizeof(int64_t) * std::max<int64_t>(1, snnz)));
+        double* v = static_cast<double*>(dvals.ensure(sizeof(double) * std::max<int64_t>(1, snnz)));
+        int64_t* cp = static_cast<int64_t*>(dcp.ensure(sizeof(int64_t) * (m + 1)));
+        uint32_t* comp = static_cast<uint32_t*>(dcomp.ensure(sizeof(uint32_t) * std::max<int64_t>(1, snnz)));
+        double* Yd = static_cast<double*>(dY.ensure(sizeof(double) * d * (n + 1)));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(r, s_rows, sizeof(int64_t) * snnz, cudaMemcpyHostToDevice, ctx->stream));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(v, s_vals, sizeof(double) * snnz, cudaMemcpyHostToDevice, ctx->stream));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(cp, s_colptr, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, ctx->stream));
+        if (snnz > 0) {
+            csc_to_compact_kernel<<<static_cast<unsigned>(slq::ceil_div(snnz, 256)), 256, 0, ctx->stream>>>(r, v, snnz, comp);
+            SLQ_LAUNCH_CHECK(ctx);
+        }
+        slq::sketch_apply_sparse_compact_dev(ctx, As, d, comp, cp, zmax, val, Yd);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(Y, Yd, sizeof(double) * d * n, cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int slq_lsqr_sparse(slq_ctx* ctx, const slq_sparse* A, const double* M, const double* b, const double* x0,
+                    const slq_solve_opts* opts_in, double* x_out, slq_report* report, double* residual_estimate,
+                    double* iterates_error, double* residual_true) {
+    return guarded([&] {
+        need(ctx && A && M && x0 && x_out, SLQ_INVALID_ARG, "lsqr_sparse: null argument");
+        need(b != nullptr || A->b != nullptr, SLQ_INVALID_ARG, "lsqr_sparse: no right-hand side");
+        slq_solve_opts opts;
+        if (opts_in) opts = *opts_in;
+        else slq_solve_opts_default(&opts);
+        const int64_t n = A->n, m = A->m;
+        PrecondBufs P = precond_bufs(ctx, n);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(P.M, M, sizeof(double) * n * n, cudaMemcpyHostToDevice, ctx->stream));
+        transpose_square(ctx, P.M, n, P.Mt);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(P.x0, x0, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        slq::DevBuf db, dx;
+        double* bd = nullptr;
+        if (b) {
+            bd = static_cast<double*>(db.ensure(sizeof(double) * (m + slq::kSparseRowPad)));
+            SLQ_CUDA_CHECK(cudaMemsetAsync(bd, 0, sizeof(double) * (m + slq::kSparseRowPad), ctx->stream));
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(bd, b, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream));
+        }
+        double* x = static_cast<double*>(dx.ensure(sizeof(double) * (n + 8)));
+        slq::LsqrOut lo;
+        const auto h0 = std::chrono::steady_clock::now();
+        slq::lsqr_dev(ctx, *slq::make_sparse_op(ctx, A), bd, P.M, P.Mt, P.x0, x, opts, residual_estimate,
+                      iterates_error, residual_true, lo);
+        SLQ_CUDA_CHECK(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        lo.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
+        fill_report(report, lo);
+    });
 }
 
 int slq_time_kernels(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed, int reps,
@@ -762,7 +982,7 @@ int slq_solve_host(slq_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t 
     slq_dense* Ad = nullptr;
     int st = slq_dense_upload(ctx, A, m, n, lda, b, row_begin, &Ad);
     if (st != SLQ_OK) return st;
-    st = run_solve(ctx, Ad, d, zeta, seed, opts, x_out, report, times, residual_estimate);
+    st = run_solve(ctx, dense_operand(ctx, Ad), d, zeta, seed, opts, x_out, report, times, residual_estimate);
     std::string keep = g_last_error;
     slq_dense_free(Ad);
     g_last_error = keep;

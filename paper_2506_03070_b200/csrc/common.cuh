@@ -110,7 +110,23 @@ struct slq_dense {
     bool has_b = false;
 };
 
+// Sparse row block in CSR (device).  Arrays carry slack past their logical
+// end (colidx / vals: +4 entries, rowptr: +2, b: +kSparseRowPad) so bulk
+// copies can round their ranges to 16-byte boundaries.
+struct slq_sparse {
+    slq_ctx* ctx = nullptr;
+    int64_t m = 0, n = 0, nnz = 0;
+    int64_t row_begin = 0;
+    int64_t* rowptr = nullptr;  // m + 1 (+2 slack)
+    int32_t* colidx = nullptr;  // nnz (+4 slack)
+    double* vals = nullptr;     // nnz (+4 slack)
+    double* b = nullptr;        // m (+ slack) right-hand side rows, may be null
+    bool owned = true;
+};
+
 namespace slq {
+
+constexpr int64_t kSparseRowPad = 256;
 
 // Row stride of the device layout: [A | b | zero pad], 32-byte aligned rows.
 inline int64_t dense_ld(int64_t n) { return round_up(n + 1, 4); }

@@ -638,7 +638,7 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
     B.scal = B.hist + maxit + 8;
     B.part = static_cast<double*>(ws.lsqr_part.ensure(sizeof(double) * grid * (n + 1)));
     B.st = static_cast<LsqrState*>(ws.lsqr_state.ensure(sizeof(LsqrState)));
-    B.u = static_cast<double*>(ws.lsqr_u.ensure(sizeof(double) * std::max<int64_t>(1, m)));
+    B.u = static_cast<double*>(ws.lsqr_u.ensure(sizeof(double) * (m + kSparseRowPad)));  // slack for tile copies
 
     LsqrState h{};
     h.eps = opts.eps;

@@ -446,11 +446,6 @@ void generate_sparse_sign_dev(slq_ctx* ctx, int64_t d, int64_t zeta, uint64_t se
 
 namespace {
 
-struct ChunkPlan {
-    int K, KB, cap;
-    int64_t nchunks, ptr_stride, ent_stride;
-};
-
 ChunkPlan plan_chunks(int64_t m, int64_t d, int64_t zeta_max) {
     ChunkPlan p{};
     int zp = 1;
@@ -493,6 +488,34 @@ void launch_gather(slq_ctx* ctx, const GatherArgs& g, int rpt, int64_t nslabs, s
 
 }  // namespace
 
+ChunkCsr build_chunk_csr(slq_ctx* ctx, const uint32_t* compact, const int64_t* colptr_dev, int64_t zeta_max,
+                         int64_t m, int64_t d) {
+    Workspace& ws = ctx->ws;
+    ChunkCsr cc;
+    cc.plan = plan_chunks(m, d, zeta_max);
+    const ChunkPlan& cp = cc.plan;
+    // slack: row-part slices may run past the last chunk
+    cc.ptr = static_cast<uint16_t*>(ws.chunk_ptr.ensure(sizeof(uint16_t) * (cp.ptr_stride * cp.nchunks + d + 64)));
+    cc.ent = static_cast<uint16_t*>(ws.chunk_ent.ensure(sizeof(uint16_t) * cp.ent_stride * cp.nchunks));
+    cc.flag = static_cast<int*>(ws.flags.ensure(4096));
+    SLQ_CUDA_CHECK(cudaMemsetAsync(cc.flag, 0, sizeof(int), ctx->stream));
+    BucketArgs ba{compact, colptr_dev, zeta_max, m, d, cp.K, cp.KB, cp.ptr_stride, cp.ent_stride, cc.ptr, cc.ent,
+                  cp.cap, cc.flag};
+    const size_t bsmem = sizeof(uint32_t) * cp.cap;
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(bucketize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(bsmem)));
+    bucketize_kernel<<<static_cast<unsigned>(cp.nchunks), 1024, bsmem, ctx->stream>>>(ba);
+    SLQ_LAUNCH_CHECK(ctx);
+    return cc;
+}
+
+void check_chunk_csr(slq_ctx* ctx, const ChunkCsr& cc) {
+    int hflag = 0;
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(&hflag, cc.flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (hflag) fail(SLQ_UNSUPPORTED, "sketch_apply: a chunk exceeded 16384 sketch entries");
+}
+
 void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32_t* compact,
                               const int64_t* colptr_dev, int64_t zeta, double val, bool exact,
                               double* Y) {
@@ -504,20 +527,10 @@ void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const
         SLQ_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(double) * d * ncols_out, ctx->stream));
         return;
     }
-    ChunkPlan cp = plan_chunks(m, d, zeta);
-    uint16_t* ptr = ws.chunk_ptr.as<uint16_t>();
-    ptr = static_cast<uint16_t*>(ws.chunk_ptr.ensure(sizeof(uint16_t) * (cp.ptr_stride * cp.nchunks + d + 64)));  // slack: part slices may run past the last chunk
-    uint16_t* ent = static_cast<uint16_t*>(ws.chunk_ent.ensure(sizeof(uint16_t) * cp.ent_stride * cp.nchunks));
-    int* flags = static_cast<int*>(ws.flags.ensure(4096));
-    SLQ_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int), ctx->stream));
-
-    BucketArgs ba{compact, colptr_dev, zeta, m, d, cp.K, cp.KB, cp.ptr_stride, cp.ent_stride, ptr, ent,
-                  cp.cap, flags};
-    const size_t bsmem = sizeof(uint32_t) * cp.cap;
-    SLQ_CUDA_CHECK(cudaFuncSetAttribute(bucketize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(bsmem)));
-    bucketize_kernel<<<static_cast<unsigned>(cp.nchunks), 1024, bsmem, ctx->stream>>>(ba);
-    SLQ_LAUNCH_CHECK(ctx);
+    ChunkCsr cc = build_chunk_csr(ctx, compact, colptr_dev, zeta, m, d);
+    const ChunkPlan& cp = cc.plan;
+    uint16_t* ptr = cc.ptr;
+    uint16_t* ent = cc.ent;
 
     // 4-column slab per CTA, all d rows of the slab in registers (<= 8 rows per thread)
     int rpt = 1;
@@ -553,10 +566,7 @@ void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const
             Yw, nsplit, d, ldw, ncols_out, Y);
         SLQ_LAUNCH_CHECK(ctx);
     }
-    int hflag = 0;
-    SLQ_CUDA_CHECK(cudaMemcpyAsync(&hflag, flags, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-    if (hflag) fail(SLQ_UNSUPPORTED, "sketch_apply: a chunk exceeded 16384 sketch entries");
+    check_chunk_csr(ctx, cc);
 }
 
 void sketch_apply_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed,

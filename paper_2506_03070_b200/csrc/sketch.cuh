@@ -5,6 +5,23 @@
 
 namespace slq {
 
+// Chunk-CSR of a sparse sign sketch (K2's bucketed form): for every chunk of
+// K consecutive sketch columns (= A rows), the entries sorted by (target row
+// r, column k) as u16 (k_local << 1 | negative) with u16 row pointers.
+struct ChunkPlan {
+    int K, KB, cap;
+    int64_t nchunks, ptr_stride, ent_stride;
+};
+struct ChunkCsr {
+    ChunkPlan plan;
+    uint16_t* ptr = nullptr;
+    uint16_t* ent = nullptr;
+    int* flag = nullptr;
+};
+ChunkCsr build_chunk_csr(slq_ctx* ctx, const uint32_t* compact, const int64_t* colptr_dev, int64_t zeta_max,
+                         int64_t m, int64_t d);
+void check_chunk_csr(slq_ctx* ctx, const ChunkCsr& cc);
+
 // K1: sparse-sign generator for global columns [col_begin, col_begin+ncols).
 // Outputs (device pointers, each optional): compact u32 entries, reference
 // CSC (rows64 / vals / colptr), stats[2] (u64 counters, accumulated).

@@ -1,0 +1,24 @@
+// sparse.cuh -- host entry points of the sparse-A (CSR) path.
+#pragma once
+
+#include <memory>
+
+#include "common.cuh"
+#include "lsqr.cuh"
+
+namespace slq {
+
+// allocate the CSR arrays of A (m, n, nnz set by the caller) with bulk-copy slack
+void sparse_alloc(slq_ctx* ctx, slq_sparse* A, bool with_b);
+void sparse_free(slq_sparse* A);
+// fill A's CSR from a host CSC (the reference CscMatrix layout), rows sorted
+void sparse_from_csc(slq_ctx* ctx, slq_sparse* A, const int64_t* colptr, const int64_t* rows, const double* vals);
+// K2s: Y_aug = S [A b] (d x (n+1), column-major), bit-identical to spmm(csc, csc)
+void sketch_apply_sparse_dev(slq_ctx* ctx, const slq_sparse* A, int64_t d, int64_t zeta, uint64_t seed, double* Y);
+// K2s for a caller-given sketch already in compact form (colptr_dev null = uniform zeta)
+void sketch_apply_sparse_compact_dev(slq_ctx* ctx, const slq_sparse* A, int64_t d, const uint32_t* compact,
+                                     const int64_t* colptr_dev, int64_t zeta_max, double val, double* Y);
+// K4s operator for LSQR
+std::unique_ptr<PassOp> make_sparse_op(slq_ctx* ctx, const slq_sparse* A);
+
+}  // namespace slq

@@ -1,0 +1,92 @@
+"""GPU parity of the sparse-A path (BASELINE config C4)
+against the CPU oracle's CSC restatement (itself bit-identical to the
+reference's spmm(csc, csc) / SerialOperator<CscMatrix>, tests/test_oracle.py).
+
+Bars: S A and S b bit-exact (reference accumulation order); LSQR iterates
+within 1e-10 at moderate conditioning, residual histories 1e-9; the
+pipeline's backward error no worse than 2x the reference's at fixed T."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+slq = pytest.importorskip("paper_2506_03070_b200")
+C = oracle.C()
+
+
+def rand_csc(m, n, density, seed, long_rows=0, empty_rows=0):
+    rng = np.random.default_rng(seed)
+    A = sp.random(m, n, density=density, format="lil", random_state=seed, data_rvs=rng.standard_normal)
+    for r in range(long_rows):  # rows longer than one warp pass (64 nnz)
+        A[r, :] = rng.standard_normal(n) * (rng.random(n) < 0.9)
+    for r in range(empty_rows):
+        A[m - 1 - r, :] = 0.0
+    A = A.tocsc()
+    A.sort_indices()
+    A.eliminate_zeros()
+    return slq.CscMatrix(m, n, A.data.astype(np.float64), A.indices.astype(np.int64), A.indptr.astype(np.int64)), A
+
+
+@pytest.mark.parametrize("m,n,d,zeta,density,long_rows", [(3000, 40, 200, 8, 0.05, 0), (5000, 100, 400, 4, 0.02, 3),
+                                                          (2000, 70, 300, 16, 0.3, 5), (1500, 8, 64, 1, 0.1, 0)])
+def test_sparse_apply_bit_exact(m, n, d, zeta, density, long_rows):
+    Acsc, A = rand_csc(m, n, density, m + n, long_rows=long_rows, empty_rows=2)
+    b = np.random.default_rng(1).standard_normal(m)
+    S = slq.generate_sparse_sign(d, m, zeta, 77)
+    Y = slq.apply(S, Acsc)
+    Yo, Sbo = C.sketch_apply_csc(d, zeta, 77, m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, b)
+    assert np.array_equal(Y, Yo)
+    dm = slq.SparseDeviceMatrix.from_csc(Acsc, b)
+    Yd, Sbd = dm.sketch(d, zeta, 77)
+    assert np.array_equal(Yd, Yo) and np.array_equal(Sbd, Sbo)
+
+
+def test_sparse_apply_matches_dense_apply():
+    Acsc, A = rand_csc(4000, 30, 0.1, 5)
+    S = slq.generate_sparse_sign(160, 4000, 8, 3)
+    assert np.array_equal(slq.apply(S, Acsc), slq.apply(S, A.toarray()))
+
+
+def test_sparse_lsqr_vs_oracle():
+    m, n, d, zeta = 6000, 50, 300, 8
+    Acsc, A = rand_csc(m, n, 0.05, 11)
+    Ad = A.toarray()
+    b = np.random.default_rng(2).standard_normal(m)
+    Y, Sb = C.sketch_apply_csc(d, zeta, 5, m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, b)
+    M, Q = C.build_preconditioner(Y)
+    x0 = C.initial_guess(M, Q, Sb)
+    xs = np.linalg.lstsq(Ad, b, rcond=None)[0]
+    for one_sync in (False, True):
+        fn = slq.lsqr_one_sync if one_sync else slq.lsqr
+        x, rep = fn(Acsc, M, b, x0, slq.SolveOptions(eps=0.0, maxit=12, x_star=xs, track_true_residual=True))
+        xo, repo = C.lsqr_csc(m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, M, b, x0, eps=0.0, maxit=12,
+                              one_sync=one_sync, x_star=xs, track_true=True)
+        assert rep.iterations == 12
+        assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
+        assert np.allclose(rep.residual_estimate, repo.residual_estimate, rtol=1e-9)
+        assert np.allclose(rep.residual_true, repo.residual_true, rtol=1e-9)
+        assert np.allclose(rep.iterates_error, repo.iterates_error, rtol=1e-6, atol=1e-12)
+
+
+def test_sparse_solve_pipeline():
+    m, n, d, zeta = 20000, 60, 240, 8
+    Acsc, A = rand_csc(m, n, 0.03, 21)
+    Ad = A.toarray()
+    b = np.random.default_rng(3).standard_normal(m)
+    x, rep, times = slq.solve(Acsc, d, zeta, 9, slq.SolveOptions(eps=0.0, maxit=25), b=b)
+    Y, Sb = C.sketch_apply_csc(d, zeta, 9, m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, b)
+    M, Q = C.build_preconditioner(Y)
+    x0 = C.initial_guess(M, Q, Sb)
+    xo, repo = C.lsqr_csc(m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, M, b, x0, eps=0.0, maxit=25,
+                          one_sync=True)
+
+    def eta(v):
+        r = b - Ad @ v
+        return np.linalg.norm(Ad.T @ r) / (np.linalg.norm(Ad, 2) * np.linalg.norm(r))
+
+    assert rep.iterations == 25
+    assert eta(x) <= max(2 * eta(xo), 1e-14)
+    assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
