@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=16, help="reference runs on m/cpu_sample rows, scaled")
+    ap.add_argument("--config", default="c3", choices=["c3", "c4"],
+                    help="c3: dense 4M x 1000 cond 1e8 (headline); c4: sparse CSR 2^24 x 2000, 50 nnz/row, cond 1e6")
     return ap.parse_args()
 
 
@@ -231,6 +233,107 @@ def reference_sample(args, m_s, T, torch=None):
     return total, {k: float(v) for k, v in ph.items()}, desc, cores, wall
 
 
+# ------------------------------------------------------------ config C4 (sparse)
+
+def run_sparse(args, world, rank, local_rank):
+    """BASELINE configs[3]: sparse CSR A, m=2^24, n=2000, exactly 50 distinct
+    random columns per row (the reference rejection sampler, seed 4), values
+    +-sigma_j with sigma log-spaced in [1e-6, 1] (cond ~1e6), b uniform(-1,1);
+    d = 4n, zeta = 8; one line like the dense one (value = seconds per solve)."""
+    import ctypes as ct
+
+    import torch
+
+    import paper_2506_03070_b200 as slq
+
+    m = args.m if args.m != 4_000_000 else 1 << 24
+    n = args.n if args.n != 1000 else 2000
+    nnz_row, d, zeta = 50, args.dfac * n, args.zeta
+    cond = 1e6
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = tdist
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    part = slq.partition_rows(m, world)
+    r0, r1 = part.begin(rank), part.end(rank)
+    ml = r1 - r0
+    ctx = slq.Context(local_rank)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream.cuda_stream)
+    if world > 1:
+        uid = [slq.Context.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.init_comm(uid[0], rank, world)
+    sigma = np.power(10.0, -np.log10(cond) * np.arange(n) / max(n - 1, 1))
+    t_gen = time.perf_counter()
+    A, _ = slq.SparseDeviceMatrix.create_csr(ml, n, ml * nnz_row, row_begin=r0, with_b=True, ctx=ctx)
+    A.fill_random(nnz_row, 4, sigma)
+    b = np.random.default_rng(1000 + rank).uniform(-1.0, 1.0, ml)
+    A.set_rhs(b)
+    t_gen = time.perf_counter() - t_gen
+    a_norm_f = float(np.sqrt(m * nnz_row * np.mean(sigma ** 2)))  # E||A||_F (an upper bound for ||A||_2)
+    T = args.iters or 40
+
+    def solve(eta=False):
+        return slq.solve(A, d, zeta, 3, slq.SolveOptions(eps=0.0, maxit=T, a_norm_est=a_norm_f if eta else 0.0),
+                         ctx=ctx)
+
+    for _ in range(max(args.warmup, 3)):
+        solve()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(1.5)
+    solve()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.kernel_launches
+    ev0.record(stream)
+    phases = []
+    for _ in range(args.steps):
+        _, rep, ph = solve()
+        phases.append(ph)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    sec = ev0.elapsed_time(ev1) * 1e-3 / args.steps
+    if dist is not None:
+        t = torch.tensor([sec], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+    ph = {k: float(np.mean([p[k] for p in phases])) for k in phases[0]}
+    _, rep_eta, _ = solve(eta=True)
+    nnz = ml * nnz_row
+    pass_bytes = 12.0 * nnz + 8.0 * (ml + 1) + 16.0 * ml
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    it_s = ph["lsqr_per_iteration"]
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC + " [config C4 sparse]", "value": sec, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": sec * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device generator: 50 distinct random columns/row, seed 4; b uniform)",
+            "config": {"workload": f"C4: sparse CSR m={m} n={n} nnz/row={nnz_row} cond~1e6, d={d} zeta={zeta}, "
+                                   f"{T} LSQR iterations", "m": m, "n": n, "nnz": m * nnz_row, "d": d, "zeta": zeta,
+                       "lsqr_iterations": T, "parallelism": f"rows/{world}" if world > 1 else "1 GPU"},
+            "eta_F_final": rep_eta.backward_error, "phases_s": ph,
+            "roofline": {"bound": "hbm", "kernel": "sparse LSQR iteration (K4s + K5)",
+                         "achieved": pass_bytes / it_s / 1e9 if it_s else None, "peak": peak, "unit": "GB/s",
+                         "frac": pass_bytes / it_s / 1e9 / peak if it_s else None, "traffic": None,
+                         "algorithmic_bytes_per_iteration": pass_bytes},
+            "gpu_launches": int(ctx.kernel_launches - launches0), "clocks": ck, "generation_s": t_gen}))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------ main
 
 def main():
@@ -238,6 +341,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config == "c4" and args.impl == "ours":
+        return run_sparse(args, world, rank, local_rank)
     n, d, zeta = args.n, args.dfac * args.n, args.zeta
     config = {"workload": f"C3: dense m={args.m} n={n} cond={args.cond:g} rho={args.rho}, sparse-sign d={d} "
                           f"zeta={zeta}, LSQR to eta<={args.eta:g}",

@@ -150,6 +150,11 @@ int slq_sparse_create_csr(slq_ctx* ctx, int64_t m, int64_t n, int64_t nnz, int64
                           slq_sparse** out, int64_t** row_ptr, int32_t** col_idx, double** values,
                           double** b);
 int slq_sparse_set_rhs(slq_sparse* A, const double* b_host);
+/* Benchmark harness: fills A (created with
+ * nnz = m * nnz_per_row) with nnz_per_row distinct random columns per row,
+ * drawn by the reference's rejection sampler keyed by global row id, values
+ * +-col_scale[col] (host array of n, NULL = +-1). */
+int slq_sparse_fill_random(slq_sparse* A, int64_t nnz_per_row, uint64_t seed, const double* col_scale);
 int slq_sparse_free(slq_sparse* A);
 
 /* sketch.hpp:298 + :304 for a sparse operand: Y = S A (d x n, column-major)

@@ -588,6 +588,11 @@ class SparseDeviceMatrix:
     def set_rhs(self, b):
         _check(C.lib.slq_sparse_set_rhs(self.handle, _d(_vec(b))))
 
+    def fill_random(self, nnz_per_row, seed, col_scale=None):
+        """Benchmark harness (config C4): nnz_per_row distinct random columns per row."""
+        cs = _vec(col_scale) if col_scale is not None else None
+        _check(C.lib.slq_sparse_fill_random(self.handle, nnz_per_row, seed & (2**64 - 1), _d(cs)))
+
     def free(self):
         if self.handle:
             C.lib.slq_sparse_free(self.handle)

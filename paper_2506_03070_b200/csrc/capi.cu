@@ -845,6 +845,22 @@ int slq_sparse_create_csr(slq_ctx* ctx, int64_t m, int64_t n, int64_t nnz, int64
     });
 }
 
+int slq_sparse_fill_random(slq_sparse* A, int64_t nnz_per_row, uint64_t seed, const double* col_scale) {
+    return guarded([&] {
+        need(A != nullptr, SLQ_INVALID_ARG, "null matrix");
+        need(A->nnz == A->m * nnz_per_row, SLQ_DIMENSION_MISMATCH, "sparse_fill_random: nnz != m * nnz_per_row");
+        slq_ctx* ctx = A->ctx;
+        slq::DevBuf sc;
+        double* dsc = nullptr;
+        if (col_scale) {
+            dsc = static_cast<double*>(sc.ensure(sizeof(double) * std::max<int64_t>(1, A->n)));
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(dsc, col_scale, sizeof(double) * A->n, cudaMemcpyHostToDevice, ctx->stream));
+        }
+        slq::generate_sparse_rows_dev(ctx, A->n, nnz_per_row, seed, A->row_begin, A->m, dsc, A->rowptr, A->colidx,
+                                      A->vals);
+    });
+}
+
 int slq_sparse_set_rhs(slq_sparse* A, const double* b) {
     return guarded([&] {
         need(A != nullptr, SLQ_INVALID_ARG, "null matrix");

@@ -198,6 +198,30 @@ __global__ void gen_generic_kernel(GenArgs a) {
     }
 }
 
+// Synthetic sparse rows for the C4 benchmark harness: row i
+// (global id g) gets nnz distinct columns of [0, n) drawn by the reference's
+// rejection sampler from substream (seed, 2g) -- sorted -- and values
+// +-scale[col] with signs from substream (seed, 2g+1).
+__global__ void sparse_rows_kernel(int64_t n, int64_t nnz, uint64_t seed_mixed, uint64_t thresh, int64_t row_begin,
+                                   int64_t m, const double* scale, int64_t* rowptr, int32_t* colidx, double* vals,
+                                   int64_t* work) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i > m) return;
+    rowptr[i] = i * nnz;
+    if (i == m) return;
+    const uint64_t g = static_cast<uint64_t>(row_begin + i);
+    int64_t* cols = work + i * nnz;
+    unsigned long long rounds = 0;
+    replay_column(cols, nnz, static_cast<uint64_t>(n), thresh, stream_state(seed_mixed, 2 * g), &rounds);
+    SeqRng vr{stream_state(seed_mixed, 2 * g + 1)};
+    for (int64_t t = 0; t < nnz; ++t) {
+        const int64_t c = cols[t];
+        colidx[i * nnz + t] = static_cast<int32_t>(c);
+        const double sg = (vr.next() & 1u) ? 1.0 : -1.0;
+        vals[i * nnz + t] = scale ? sg * scale[c] : sg;
+    }
+}
+
 // ------------------------------------------------------------- K2 bucketize
 
 struct BucketArgs {
@@ -487,6 +511,17 @@ void launch_gather(slq_ctx* ctx, const GatherArgs& g, int rpt, int64_t nslabs, s
 }
 
 }  // namespace
+
+void generate_sparse_rows_dev(slq_ctx* ctx, int64_t n, int64_t nnz, uint64_t seed, int64_t row_begin, int64_t m,
+                              const double* scale, int64_t* rowptr, int32_t* colidx, double* vals) {
+    if (nnz < 1 || nnz > n) fail(SLQ_INVALID_SPARSITY, "sparse rows: need 1 <= nnz per row <= n");
+    DevBuf work;
+    int64_t* w = static_cast<int64_t*>(work.ensure(sizeof(int64_t) * std::max<int64_t>(1, m * nnz)));
+    sparse_rows_kernel<<<static_cast<unsigned>(ceil_div(m + 1, 128)), 128, 0, ctx->stream>>>(
+        n, nnz, mix64(seed), lemire_thresh(static_cast<uint64_t>(n)), row_begin, m, scale, rowptr, colidx, vals, w);
+    SLQ_LAUNCH_CHECK(ctx);
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+}
 
 ChunkCsr build_chunk_csr(slq_ctx* ctx, const uint32_t* compact, const int64_t* colptr_dev, int64_t zeta_max,
                          int64_t m, int64_t d) {

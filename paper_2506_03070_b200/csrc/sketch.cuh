@@ -30,6 +30,10 @@ void generate_sparse_sign_dev(slq_ctx* ctx, int64_t d, int64_t zeta, uint64_t se
                               int64_t* rows64, double* vals, int64_t* colptr,
                               unsigned long long* stats);
 
+// C4 benchmark harness: CSR rows with nnz distinct random columns each (see sketch.cu)
+void generate_sparse_rows_dev(slq_ctx* ctx, int64_t n, int64_t nnz, uint64_t seed, int64_t row_begin, int64_t m,
+                              const double* scale, int64_t* rowptr, int32_t* colidx, double* vals);
+
 // K2: Y_aug = S [A b] for the rows of A (S keyed by global row id).  Writes
 // d x (n+1) column-major into Y (ldy = d).  exact => single split in the
 // reference's accumulation order.
