@@ -32,7 +32,7 @@ namespace slq {
 
 namespace {
 
-constexpr int kPanelThreads = 512;
+constexpr int kPanelThreads = 1024;
 constexpr int kNbMax = 32;
 constexpr int kWs = kNbMax + 1;  // padded row stride of the panel slice (bank-conflict free columns)
 
@@ -156,13 +156,13 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
     const double rank_tol = *a.rank_tol;
     int nred = 0;
 
-    // Row ownership is fixed for the whole panel: warp w owns local rows w, w+16, ...
+    // Row ownership is fixed for the whole panel: warp w owns local rows w, w+kWarps, ...
     // (filtered to the rows below the current diagonal).  Every per-row step of a
     // column is then warp-local and only the two reductions need block barriers.
     double sig = 0.0;  // partial sigma of the current column (valid in every lane)
     {
         const int ib0 = static_cast<int>(a.k0 - row0 + 1 > 0 ? a.k0 - row0 + 1 : 0);
-        for (int il = wid + 16 * lane; il < nrows; il += 16 * 32)
+        for (int il = wid + kWarps * lane; il < nrows; il += kWarps * 32)
             if (il >= ib0) sig += w[il * kWs] * w[il * kWs];
         for (int o = 16; o > 0; o >>= 1) sig += __shfl_xor_sync(0xffffffffu, sig, o);
     }
@@ -172,14 +172,14 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
         const int lk = static_cast<int>(gk - row0);   // local index of row gk (may be outside)
         const bool owner = lk >= 0 && lk < nrows;
         const int ib = lk + 1 > 0 ? lk + 1 : 0;       // first local row strictly below gk
-        const int i0 = wid + 16 * ((ib - wid + 15 > 0 ? ib - wid + 15 : 0) / 16);  // first owned row >= ib
+        const int i0 = wid + kWarps * ((ib - wid + kWarps - 1 > 0 ? ib - wid + kWarps - 1 : 0) / kWarps);  // first owned row >= ib
 
         // (a) sigma = sum_{i>gk} w_ik^2, x0 = w[gk][kk]: block then cluster reduction
         if (lane == 0) red[wid][0] = sig;
         __syncthreads();
         if (wid == 0) {
             double t = (lane < kWarps) ? red[lane][0] : 0.0;
-            for (int o = 8; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
             if (lane == 0) {
                 mine[0][0] = t;
                 mine[0][1] = owner ? w[lk * kWs + kk] : 0.0;
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
         const double v0 = x0 - beta;
         const double tau = (beta - x0) / beta;
         // (b) scale the reflector below the diagonal (each warp its own rows); R diagonal = beta
-        for (int il = i0 + 16 * lane; il < nrows; il += 16 * 32) w[il * kWs + kk] /= v0;
+        for (int il = i0 + kWarps * lane; il < nrows; il += kWarps * 32) w[il * kWs + kk] /= v0;
         __syncwarp();
         if (owner && tid == 0) w[lk * kWs + kk] = beta;
 
@@ -208,9 +208,9 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
             double acc0 = 0.0, acc1 = 0.0;
             if (lane < kb) {
                 int il = i0;
-                for (; il + 16 < nrows; il += 32) {
+                for (; il + kWarps < nrows; il += 2 * kWarps) {
                     acc0 += w[il * kWs + lane] * w[il * kWs + kk];
-                    acc1 += w[(il + 16) * kWs + lane] * w[(il + 16) * kWs + kk];
+                    acc1 += w[(il + kWarps) * kWs + lane] * w[(il + kWarps) * kWs + kk];
                 }
                 if (il < nrows) acc0 += w[il * kWs + lane] * w[il * kWs + kk];
             }
@@ -234,12 +234,12 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
             if (jj > kk && jj < kb) {
                 const double sj = tot[jj] * tau;
                 int il = i0;
-                for (; il + 16 < nrows; il += 32) {
+                for (; il + kWarps < nrows; il += 2 * kWarps) {
                     const double n0 = w[il * kWs + jj] - sj * w[il * kWs + kk];
-                    const double n1 = w[(il + 16) * kWs + jj] - sj * w[(il + 16) * kWs + kk];
+                    const double n1 = w[(il + kWarps) * kWs + jj] - sj * w[(il + kWarps) * kWs + kk];
                     w[il * kWs + jj] = n0;
-                    w[(il + 16) * kWs + jj] = n1;
-                    if (jj == kk + 1) sig += (il != lk1 ? n0 * n0 : 0.0) + (il + 16 != lk1 ? n1 * n1 : 0.0);
+                    w[(il + kWarps) * kWs + jj] = n1;
+                    if (jj == kk + 1) sig += (il != lk1 ? n0 * n0 : 0.0) + (il + kWarps != lk1 ? n1 * n1 : 0.0);
                 }
                 if (il < nrows) {
                     const double n0 = w[il * kWs + jj] - sj * w[il * kWs + kk];
@@ -250,17 +250,28 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
             }
             sig = __shfl_sync(0xffffffffu, sig, (kk + 1) & 31);
         }
-        // compact-WY: T[0:kk, kk] = -tau T[0:kk, 0:kk] (V^T v_kk);  T[kk][kk] = tau
+        // keep V^T v_kk and tau for the compact-WY factor (built after the loop,
+        // off the per-column critical path)
         if (rank == 0) {
-            if (tid < kk) {
-                double t = 0.0;
-                for (int b2 = tid; b2 < kk; ++b2) t += Ts[tid][b2] * tot[b2];
-                Ts[tid][kk] = -tau * t;
-            }
+            if (tid < kk) Ts[tid][kk] = tot[tid];
             if (tid == 0) {
                 Ts[kk][kk] = tau;
                 a.tau[gk] = tau;
             }
+        }
+    }
+    __syncthreads();
+    // compact-WY: T[0:kk, kk] = -tau_kk T[0:kk, 0:kk] (V^T v_kk), column by column
+    // (one warp; the upper part of Ts holds the dots until overwritten)
+    if (rank == 0 && wid == 0) {
+        for (int kk = 1; kk < kb; ++kk) {
+            double t = 0.0;
+            if (lane < kk)
+                for (int b2 = lane; b2 < kk; ++b2) t += Ts[lane][b2] * Ts[b2][kk];
+            // Ts[lane][b2] for b2 < kk are final T entries; Ts[b2][kk] are still the dots
+            __syncwarp();
+            if (lane < kk) Ts[lane][kk] = -Ts[kk][kk] * t;
+            __syncwarp();
         }
     }
     __syncthreads();
@@ -447,32 +458,134 @@ __global__ void check_diag_kernel(const double* R, int64_t n, int* err) {
     if (i < n && R[i * n + i] == 0.0) atomicMin(err, static_cast<int>(i));
 }
 
-// M = R^-1 (upper, column-major) and Mt (row-major copy: Mt[i*n+j] = M(i,j)).
-// One warp per column j: x = e_j, back-substitution in column-axpy form with
-// x staged in shared memory (triangular.hpp:14-33 computes the same entries
-// by dot-product back-substitution).
-__global__ void __launch_bounds__(128) tri_inverse_kernel(const double* R, int64_t n, double* M,
-                                                          double* Mt) {
-    extern __shared__ double xs[];  // [4][n]
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t j = static_cast<int64_t>(blockIdx.x) * 4 + wid;
-    if (j >= n) return;
-    double* x = xs + wid * n;
-    for (int64_t i = lane; i <= j; i += 32) x[i] = (i == j) ? 1.0 : 0.0;
+// ------------------------------------------------ blocked triangular inverse
+//
+// M = R^-1 by recursive doubling: the 32 x 32 diagonal blocks are inverted
+// exactly as triangular.hpp:14-33 does (column back-substitution, ascending
+// k dot products), then level by level two neighbouring inverted blocks are
+// merged:  M12 = -M11 (R12 M22)  -- two FP64 tensor-core (DMMA) GEMMs per
+// level for all merges of the level at once.
+
+constexpr int kInvB = 32;
+
+// one warp per diagonal block; lane j computes column j of the block inverse
+__global__ void __launch_bounds__(64) diag_block_inverse_kernel(const double* R, int64_t n, double* M) {
+    __shared__ double Rs[2][kInvB][kInvB + 1];
+    __shared__ double Ms[2][kInvB][kInvB + 1];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t b0 = (static_cast<int64_t>(blockIdx.x) * 2 + w) * kInvB;
+    if (b0 >= n) return;
+    const int bs = static_cast<int>(min(static_cast<int64_t>(kInvB), n - b0));
+    for (int j = 0; j < bs; ++j)
+        if (lane < bs) Rs[w][lane][j] = R[(b0 + j) * n + b0 + lane];
     __syncwarp();
-    for (int64_t i = j; i >= 0; --i) {
-        const double xi = x[i] / R[i * n + i];
-        __syncwarp();
-        if (lane == 0) x[i] = xi;
-        const double* ri = R + i * n;
-        for (int64_t l = lane; l < i; l += 32) x[l] -= xi * ri[l];
-        __syncwarp();
+    const int j = lane;
+    if (j < bs) {
+        for (int i = 0; i < bs; ++i) Ms[w][i][j] = 0.0;
+        Ms[w][j][j] = 1.0 / Rs[w][j][j];
+        for (int i = j - 1; i >= 0; --i) {
+            double sum = 0.0;
+            for (int k = i + 1; k <= j; ++k) sum += Rs[w][i][k] * Ms[w][k][j];
+            Ms[w][i][j] = -sum / Rs[w][i][i];
+        }
     }
-    for (int64_t i = lane; i < n; i += 32) {
-        const double v = (i <= j) ? x[i] : 0.0;
-        M[j * n + i] = v;
-        if (Mt) Mt[i * n + j] = v;
+    __syncwarp();
+    for (int jj = 0; jj < bs; ++jj)
+        if (lane < bs) M[(b0 + jj) * n + b0 + lane] = Ms[w][lane][jj];
+}
+
+// C[z] = alpha * A[z] * B[z] for a batch of merges; operands are sub-blocks of
+// n x n column-major matrices addressed by (row, col) offsets per batch entry.
+struct GemmBatch {
+    const double* A;
+    const double* B;
+    double* C;
+    int64_t ld;
+    double alpha;
+    int64_t base;   // first row/col of merge 0
+    int64_t step;   // distance between merges (2 * half)
+    int64_t half;   // size of the left block (rows of M11, cols of R12 / C)
+    int64_t nmax;   // n: clip sizes at the matrix edge
+    int mode;       // 0: T = R12 * M22   (A = R rows [a, a+half) cols [b, e); B = M22)
+                    // 1: M12 = -M11 * T (A = M11; B = T)
+};
+
+// 64 x 64 output tile per CTA, 8 warps (each 32 x 16 = 4 x 2 DMMA tiles), K in steps of 16 via smem
+__global__ void __launch_bounds__(256) merge_gemm_kernel(GemmBatch g) {
+    __shared__ double As[64][17];
+    __shared__ double Bs[16][65];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lr = lane & 3, lg = lane >> 2;
+    const int64_t a = g.base + static_cast<int64_t>(blockIdx.z) * g.step;  // merge start
+    const int64_t b = a + g.half;                                           // right block start
+    if (b >= g.nmax) return;
+    const int64_t e = min(g.nmax, b + g.half);                              // right block end
+    // C is half x (e - b); K dimension: mode 0 -> (e - b) (cols of R12 = rows of M22);
+    //                                   mode 1 -> half (cols of M11 = rows of T)
+    const int64_t P = g.half, Qn = e - b, K = (g.mode == 0) ? (e - b) : g.half;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64, c0 = static_cast<int64_t>(blockIdx.x) * 64;
+    if (r0 >= P || c0 >= Qn) return;
+    // operand origins (column-major, ld)
+    const double* Ab;
+    const double* Bb;
+    if (g.mode == 0) {
+        Ab = g.A + b * g.ld + a;      // R[a:b, b:e]
+        Bb = g.B + b * g.ld + b;      // M[b:e, b:e]
+    } else {
+        Ab = g.A + a * g.ld + a;      // M[a:b, a:b]
+        Bb = g.B + b * g.ld;          // T stored at rows [0, half), cols [b, e) of the scratch (ld)
     }
+    double acc[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int wr = (warp >> 2) * 32, wc = (warp & 3) * 16;
+    for (int64_t k0 = 0; k0 < K; k0 += 16) {
+        for (int t = tid; t < 64 * 16; t += 256) {
+            const int i = t % 64, k = t / 64;
+            const int64_t gi = r0 + i, gk = k0 + k;
+            As[i][k] = (gi < P && gk < K) ? Ab[gk * g.ld + gi] : 0.0;
+        }
+        for (int t = tid; t < 16 * 64; t += 256) {
+            const int k = t % 16, j = t / 16;
+            const int64_t gk = k0 + k, gj = c0 + j;
+            Bs[k][j] = (gk < K && gj < Qn) ? Bb[gj * g.ld + gk] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double af = As[wr + i * 8 + lg][ks * 4 + lr];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const double bf = Bs[ks * 4 + lr][wc + j * 8 + lg];
+                    dmma(acc[i][j][0], acc[i][j][1], af, bf);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    double* Cb = (g.mode == 0) ? g.C + b * g.ld : g.C + b * g.ld + a;  // mode 0: scratch T rows [0,half); mode 1: M[a:b, b:e]
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t gi = r0 + wr + i * 8 + lg, gj = c0 + wc + j * 8 + 2 * lr + h;
+                if (gi < P && gj < Qn) Cb[gj * g.ld + gi] = g.alpha * acc[i][j][h];
+            }
+}
+
+__global__ void zero_lower_blocks_kernel(double* M, int64_t n) {
+    // M starts as the block-diagonal inverse; everything off the diagonal
+    // blocks is written by the merges (upper) or must be zero (lower)
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= n * n) return;
+    const int64_t j = e / n, i = e - j * n;
+    if (i / kInvB != j / kInvB) M[e] = 0.0;
 }
 
 // y = M v with M upper (row-major copy Mt): warp per row i.
@@ -613,11 +726,41 @@ void tri_inverse_dev(slq_ctx* ctx, const double* R, int64_t n, double* M, double
     SLQ_CUDA_CHECK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     if (herr != big) fail(SLQ_SINGULAR_TRIANGULAR, "tri_inverse: zero diagonal at " + std::to_string(herr));
-    const size_t smem = 4 * n * sizeof(double);
-    if (smem > 227 * 1024) fail(SLQ_UNSUPPORTED, "tri_inverse: n too large");
-    SLQ_CUDA_CHECK(cudaFuncSetAttribute(tri_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
-    tri_inverse_kernel<<<static_cast<unsigned>(ceil_div(n, 4)), 128, smem, ctx->stream>>>(R, n, M, Mt);
+    if (n == 0) return;
+    zero_lower_blocks_kernel<<<static_cast<unsigned>(ceil_div(n * n, 256)), 256, 0, ctx->stream>>>(M, n);
+    SLQ_LAUNCH_CHECK(ctx);
+    const int64_t nblk = ceil_div(n, kInvB);
+    diag_block_inverse_kernel<<<static_cast<unsigned>(ceil_div(nblk, 2)), 64, 0, ctx->stream>>>(R, n, M);
+    SLQ_LAUNCH_CHECK(ctx);
+    // merges: block size h = 32, 64, ...: M[a:b, b:e] = -M[a:b, a:b] (R[a:b, b:e] M[b:e, b:e])
+    double* T = static_cast<double*>(ctx->ws.qr_q.ensure(sizeof(double) * n * n));  // scratch, ld = n
+    for (int64_t h = kInvB; h < n; h *= 2) {
+        const int64_t nmerge = ceil_div(n, 2 * h);
+        const unsigned tiles = static_cast<unsigned>(ceil_div(h, 64));
+        GemmBatch g0{R, M, T, n, 1.0, 0, 2 * h, h, n, 0};
+        merge_gemm_kernel<<<dim3(tiles, tiles, static_cast<unsigned>(nmerge)), 256, 0, ctx->stream>>>(g0);
+        SLQ_LAUNCH_CHECK(ctx);
+        GemmBatch g1{M, T, M, n, -1.0, 0, 2 * h, h, n, 1};
+        merge_gemm_kernel<<<dim3(tiles, tiles, static_cast<unsigned>(nmerge)), 256, 0, ctx->stream>>>(g1);
+        SLQ_LAUNCH_CHECK(ctx);
+    }
+    if (Mt) transpose_dev(ctx, M, n, Mt);
+}
+
+__global__ void transpose_sq_kernel(const double* M, int64_t n, double* Mt) {
+    __shared__ double tile[32][33];
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32, r0 = static_cast<int64_t>(blockIdx.y) * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int k = ty; k < 32; k += 8)
+        if (c0 + k < n && r0 + tx < n) tile[k][tx] = M[(c0 + k) * n + r0 + tx];
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8)
+        if (r0 + k < n && c0 + tx < n) Mt[(r0 + k) * n + c0 + tx] = tile[tx][k];
+}
+
+void transpose_dev(slq_ctx* ctx, const double* M, int64_t n, double* Mt) {
+    dim3 g(static_cast<unsigned>(ceil_div(n, 32)), static_cast<unsigned>(ceil_div(n, 32)));
+    transpose_sq_kernel<<<g, dim3(32, 8), 0, ctx->stream>>>(M, n, Mt);
     SLQ_LAUNCH_CHECK(ctx);
 }
 

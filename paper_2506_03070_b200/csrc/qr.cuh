@@ -15,6 +15,9 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
 // M = R^-1 (column-major) and optionally Mt (row-major copy).
 void tri_inverse_dev(slq_ctx* ctx, const double* R, int64_t n, double* M, double* Mt);
 
+// Mt = M^T (n x n, column-major in and out).
+void transpose_dev(slq_ctx* ctx, const double* M, int64_t n, double* Mt);
+
 // y = M v for upper-triangular M given as its row-major copy Mt.
 void trmv_upper_dev(slq_ctx* ctx, const double* Mt, int64_t n, const double* v, double* y);
 // y = M^T v for upper-triangular M given column-major.
