@@ -288,6 +288,212 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
     cl.sync();
 }
 
+// ------------------------------------------ register-resident panel (default)
+//
+// Same reflectors as panel_kernel, one cluster reduction per column instead of
+// two.  For column k with diagonal row g the reduction carries, for every
+// panel column j, the pair
+//     G_j = sum_{i>g} w_ij w_ik      (dot products below the diagonal)
+//     R_j = w_gj                     (the diagonal row, contributed by rank 0)
+// from which sigma = G_k, x0 = R_k and, with v_i = w_ik / v0,
+//     s_j = R_j + G_j / v0  =  w_gj + sum_{i>g} v_i w_ij      (qr.hpp:51-53)
+// (for j < k the same expression is v_j^T v_k, the compact-WY input).  The
+// partial G of the NEXT column is accumulated while the current reflector is
+// applied, so each column costs one block barrier plus one DSMEM exchange.
+// The panel slice lives in registers: thread (warp w, lane j) owns column j
+// of local rows w + 16 s, s < RS.
+constexpr int kRegPanelThreads = 512;
+constexpr int kRegWarps = kRegPanelThreads / 32;
+
+template <int RS>
+__global__ void __launch_bounds__(kRegPanelThreads, 1) panel_reg_kernel(PanelArgs a) {
+    extern __shared__ __align__(16) double w[];  // [rpc][kWs] staging for the coalesced load / store
+    __shared__ double red[kRegWarps][32];
+    __shared__ double rrow[32];
+    __shared__ __align__(16) double inbox[2][16][64];
+    __shared__ double Ts[kNbMax][kNbMax + 1];
+    __shared__ uint64_t mbar[2];
+    cg::cluster_group cl = cg::this_cluster();
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 2; ++q) {
+            const unsigned ad = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[q]));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(ad) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const unsigned rank = cl.block_rank(), nr = cl.num_blocks();
+    const bool r0 = rank == 0;
+    const int kb = a.kb;
+    const int64_t row0 = a.k0 + static_cast<int64_t>(rank) * a.rpc;
+    const int nrows = static_cast<int>(a.d - row0 < a.rpc ? (a.d - row0 > 0 ? a.d - row0 : 0) : a.rpc);
+
+    // coalesced load of the slice (warp per column), transposed through shared memory
+    for (int jj = wid; jj < kb; jj += kRegWarps) {
+        const double* col = a.Y + (a.k0 + jj) * a.ldy + row0;
+#pragma unroll 4
+        for (int il = lane; il < nrows; il += 32) w[il * kWs + jj] = col[il];
+    }
+    __syncthreads();
+    double v[RS];
+#pragma unroll
+    for (int s = 0; s < RS; ++s) {
+        const int il = wid + kRegWarps * s;
+        v[s] = (il < nrows && lane < kb) ? w[il * kWs + lane] : 0.0;
+    }
+    cl.sync();  // every CTA's mbarriers exist before anyone arrives remotely
+    const double rank_tol = *a.rank_tol;
+
+    // partial G for column 0 (rows strictly below the panel's first diagonal row)
+    double g = 0.0;
+#pragma unroll
+    for (int s = 0; s < RS; ++s) {
+        const int il = wid + kRegWarps * s;
+        const double vk = __shfl_sync(0xffffffffu, v[s], 0);
+        if (il < nrows && (!r0 || il > 0)) g = fma(v[s], vk, g);
+    }
+
+    for (int kk = 0; kk < kb; ++kk) {
+        const int p = kk & 1;
+        const unsigned phase = static_cast<unsigned>((kk >> 1) & 1);
+        red[wid][lane] = g;
+        if (r0 && wid == (kk & (kRegWarps - 1))) rrow[lane] = (kk < kRegWarps) ? v[0] : v[1];
+        __syncthreads();
+        const unsigned bar = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[p]));
+        if (wid == 0) {
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+#pragma unroll
+            for (int q = 0; q < kRegWarps; q += 4) {
+                t0 += red[q][lane];
+                t1 += red[q + 1][lane];
+                t2 += red[q + 2][lane];
+                t3 += red[q + 3][lane];
+            }
+            const double gsum = (t0 + t1) + (t2 + t3);
+            const double rj = r0 ? rrow[lane] : 0.0;
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                             "r"(static_cast<unsigned>(nr * 64 * sizeof(double)))
+                             : "memory");
+            const unsigned slot = static_cast<unsigned>(__cvta_generic_to_shared(&inbox[p][rank][2 * lane]));
+            for (unsigned q = 0; q < nr; ++q) {
+                unsigned rslot, rbar;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rslot) : "r"(slot), "r"(q));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rbar) : "r"(bar), "r"(q));
+                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(rslot),
+                             "d"(gsum), "d"(rj), "r"(rbar)
+                             : "memory");
+            }
+        }
+        {
+            unsigned ok = 0;
+            do {
+                asm volatile(
+                    "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
+                    " selp.u32 %0, 1, 0, P;\n}\n"
+                    : "=r"(ok)
+                    : "r"(bar), "r"(phase)
+                    : "memory");
+            } while (!ok);
+        }
+        // every thread sums the inbox itself (rank order): no second barrier.  The
+        // buffer is safe to reuse two columns later: a peer can only push column
+        // kk+2 after this CTA pushed kk+1, i.e. after all its warps passed here.
+        double G = 0.0, R = 0.0;
+        for (unsigned q = 0; q < nr; ++q) {
+            const double2 pr = *reinterpret_cast<const double2*>(&inbox[p][q][2 * lane]);
+            G += pr.x;
+            R += pr.y;
+        }
+        const double sigma = __shfl_sync(0xffffffffu, G, kk), x0 = __shfl_sync(0xffffffffu, R, kk);
+        const double normx = sqrt(x0 * x0 + sigma);
+        if (normx < rank_tol || normx == 0.0) {
+            if (r0 && tid == 0) atomicCAS(a.err, 0, static_cast<int>(1 + a.k0 + kk));
+            cl.sync();
+            return;
+        }
+        const double beta = (x0 > 0.0) ? -normx : normx;
+        const double v0 = x0 - beta;
+        const double tau = (beta - x0) / beta;
+        const double rv0 = 1.0 / v0;
+        const double sdot = R + G * rv0;  // s_j (j > kk) or v_j^T v_kk (j < kk)
+        const double sj = (lane > kk && lane < kb) ? sdot * tau : 0.0;
+        const double cj = sj * rv0;       // w_ij -= tau s_j v_i = cj w_ik
+        if (r0 && wid == 0) {
+            if (lane < kk) Ts[lane][kk] = sdot;
+            if (lane == 0) {
+                Ts[kk][kk] = tau;
+                a.tau[a.k0 + kk] = tau;
+            }
+        }
+        // apply H_kk to this thread's column and accumulate the next column's
+        // partial G.  Rows past the slice are zero and stay zero, so only rank
+        // 0's first two slots (rows < 32: finished rows of R, the diagonal row)
+        // need guards.
+        g = 0.0;
+        const int kn = kk + 1 < 32 ? kk + 1 : 31;
+        const bool isk = lane == kk;
+#pragma unroll
+        for (int s = 0; s < RS; ++s) {
+            const int il = wid + kRegWarps * s;
+            const double wk = __shfl_sync(0xffffffffu, v[s], kk);
+            double nv = isk ? wk * rv0 : fma(-cj, wk, v[s]);
+            bool acc = true;
+            if (s < 2 && r0) {
+                if (il < kk) nv = v[s];
+                else if (il == kk) nv = isk ? beta : v[s] - sj;
+                acc = il > kk + 1;
+            }
+            v[s] = nv;
+            const double wn = __shfl_sync(0xffffffffu, nv, kn);
+            if (acc) g = fma(nv, wn, g);
+        }
+    }
+    __syncthreads();
+    // compact-WY T by recursive doubling (dlarft): T[a:b, b:e] = -T11 (V1^T V2) T22,
+    // levels h = 1, 2, 4, ...; Ts holds tau on the diagonal and the dots v_i^T v_j
+    // above it until each block is overwritten.
+    if (r0) {
+        double* P = &w[0];  // [32][kWs] scratch (the slice is back in registers)
+        for (int h = 1; h < kb; h *= 2) {
+            const int e = tid;
+            const int m = e / (h * h), i = (e / h) % h, j = e % h;
+            const int a0 = 2 * h * m, b0 = a0 + h;
+            const bool live = e < 16 * h && b0 + j < kb;
+            if (live) {
+                double t = 0.0;
+                for (int k = 0; k <= j; ++k) t = fma(Ts[a0 + i][b0 + k], Ts[b0 + k][b0 + j], t);
+                P[(a0 + i) * kWs + b0 + j] = t;
+            }
+            __syncthreads();
+            if (live) {
+                double t = 0.0;
+                for (int k = i; k < h; ++k) t = fma(Ts[a0 + i][a0 + k], P[(a0 + k) * kWs + b0 + j], t);
+                Ts[a0 + i][b0 + j] = -t;
+            }
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < RS; ++s) {
+        const int il = wid + kRegWarps * s;
+        if (il < nrows && lane < kb) w[il * kWs + lane] = v[s];
+    }
+    __syncthreads();
+    for (int jj = wid; jj < kb; jj += kRegWarps) {
+        double* col = a.Y + (a.k0 + jj) * a.ldy + row0;
+#pragma unroll 4
+        for (int il = lane; il < nrows; il += 32) col[il] = w[il * kWs + jj];
+    }
+    if (r0)
+        for (int e = tid; e < kNbMax * kNbMax; e += kRegPanelThreads) {
+            const int i = e % kNbMax, j = e / kNbMax;
+            a.T[j * kNbMax + i] = (i < kb && j < kb && i <= j) ? Ts[i][j] : 0.0;
+        }
+    cl.sync();
+}
+
 // --------------------------------------------------- trailing update (DMMA)
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -637,6 +843,67 @@ void launch_panel(slq_ctx* ctx, const PanelArgs& pa, int cl) {
     ctx->launches++;
 }
 
+template <int RS>
+void launch_panel_reg_rs(slq_ctx* ctx, const PanelArgs& pa, int cl) {
+    const size_t smem = static_cast<size_t>(pa.rpc) * kWs * sizeof(double);
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(panel_reg_kernel<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    if (cl > 8)
+        SLQ_CUDA_CHECK(cudaFuncSetAttribute(panel_reg_kernel<RS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl, 1, 1);
+    cfg.blockDim = dim3(kRegPanelThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SLQ_CUDA_CHECK(cudaLaunchKernelEx(&cfg, panel_reg_kernel<RS>, pa));
+    ctx->launches++;
+}
+
+void launch_panel_reg(slq_ctx* ctx, const PanelArgs& pa, int cl, int rs) {
+    switch (rs) {
+        case 2: launch_panel_reg_rs<2>(ctx, pa, cl); break;
+        case 4: launch_panel_reg_rs<4>(ctx, pa, cl); break;
+        case 8: launch_panel_reg_rs<8>(ctx, pa, cl); break;
+        case 16: launch_panel_reg_rs<16>(ctx, pa, cl); break;
+        default: launch_panel_reg_rs<32>(ctx, pa, cl); break;
+    }
+}
+
+// largest cluster the register panel may use (16 needs a GPC with 16 free SMs)
+int max_panel_cluster() {
+    static int cached = 0;
+    if (cached) return cached;
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(panel_reg_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    const size_t smem = static_cast<size_t>(256) * kWs * sizeof(double);
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(panel_reg_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16, 1, 1);
+    cfg.blockDim = dim3(kRegPanelThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 16;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, panel_reg_kernel<16>, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        nclusters = 0;
+    }
+    cached = nclusters > 0 ? 16 : 8;
+    return cached;
+}
+
 void launch_update(slq_ctx* ctx, const UpdArgs& u) {
     if (u.c_end <= u.c_begin || u.r_end <= u.k0) return;
     const unsigned ncb = static_cast<unsigned>(ceil_div(u.c_end - u.c_begin, kCB));
@@ -680,14 +947,26 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
         const int64_t k0 = p * kNbMax;
         const int kb = static_cast<int>(std::min<int64_t>(kNbMax, n - k0));
         const int64_t rows = d - k0;
+        // register panel: <= 256 rows per CTA when the cluster allows, <= 512 at most
+        const int clmax = max_panel_cluster();
         int cl = 1;
-        const int64_t max_rows_cta = (200 * 1024) / (kWs * 8);  // 775 rows per CTA
-        while (ceil_div(rows, cl) > max_rows_cta && cl < 16) cl *= 2;
-        if (ceil_div(rows, cl) > max_rows_cta) fail(SLQ_UNSUPPORTED, "householder_qr: sketch too tall for the panel kernel");
-        // prefer more CTAs for tall panels: lowers per-column latency of the local work
-        while (cl < 8 && ceil_div(rows, cl) > 256) cl *= 2;
-        PanelArgs pa{Yaug, ldy, d, k0, kb, ceil_div(rows, cl), rank_tol, tau, T + p * kNbMax * kNbMax, err};
-        launch_panel(ctx, pa, cl);
+        while (ceil_div(rows, cl) > 256 && cl < clmax) cl *= 2;
+        if (ceil_div(rows, cl) <= kRegWarps * 32) {
+            const int64_t rpc = ceil_div(rows, cl);
+            int rs = 2;
+            while (rs * kRegWarps < rpc) rs *= 2;
+            PanelArgs pa{Yaug, ldy, d, k0, kb, rpc, rank_tol, tau, T + p * kNbMax * kNbMax, err};
+            launch_panel_reg(ctx, pa, cl, rs);
+        } else {
+            // very tall sketches: shared-memory panel (two reductions per column)
+            cl = 1;
+            const int64_t max_rows_cta = (200 * 1024) / (kWs * 8);  // 775 rows per CTA
+            while (ceil_div(rows, cl) > max_rows_cta && cl < 16) cl *= 2;
+            if (ceil_div(rows, cl) > max_rows_cta)
+                fail(SLQ_UNSUPPORTED, "householder_qr: sketch too tall for the panel kernel");
+            PanelArgs pa{Yaug, ldy, d, k0, kb, ceil_div(rows, cl), rank_tol, tau, T + p * kNbMax * kNbMax, err};
+            launch_panel(ctx, pa, cl);
+        }
         UpdArgs u{Yaug, ldy, k0, kb, T + p * kNbMax * kNbMax, Yaug, ldy, k0 + kb, ncols, d, 1};
         launch_update(ctx, u);
     }
