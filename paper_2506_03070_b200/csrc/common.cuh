@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -37,6 +38,12 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// Diagnostic switches (environment variables set to a non-empty value other than "0").
+inline bool slq_env_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return v && v[0] && !(v[0] == '0' && v[1] == 0);
+}
 
 // Device buffer with RAII; grow-only reuse via ensure().
 struct DevBuf {
