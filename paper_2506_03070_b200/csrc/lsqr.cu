@@ -621,7 +621,7 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
     // with an evict-first policy: the per-iteration triangular applies then
     // hit L2 instead of HBM.
     bool l2_window = false;
-    {
+    if (!slq_env_flag("SLQ_NO_L2_WINDOW")) {
         const double* lo = std::min(M, Mt);
         const size_t bytes = (std::max(M, Mt) - lo == n * n) ? 2 * n * n * sizeof(double) : n * n * sizeof(double);
         static bool limit_set = false;

@@ -583,38 +583,57 @@ __global__ void __launch_bounds__(256) update_w_kernel(UpdArgs u, double* Wpart)
     W[a * kCB + ct1 * 8 + 2 * lr + 1] = acc[1][1];
 }
 
-// U2: W = sum_rb Wpart[rb][cb];  W2 = T^T W (or T W);  C_rb -= V_rb W2
-__global__ void __launch_bounds__(256) update_apply_kernel(UpdArgs u, const double* Wpart) {
-    extern __shared__ __align__(16) double sm[];
-    double* Vs = sm;
-    double* Cs = sm + kNbMax * kLdT;
-    double* W = Cs + kCB * kLdT;             // [kNbMax][kCB + 1]
-    double* W2 = W + kNbMax * (kCB + 1);     // [kNbMax][kCB + 1]
-    double* Ts = W2 + kNbMax * (kCB + 1);    // [kNbMax][kNbMax + 1]
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int lr = lane & 3, lg = lane >> 2;
-    const int64_t r0 = u.k0 + static_cast<int64_t>(blockIdx.y) * kRB;
-    const int64_t c0 = u.c_begin + static_cast<int64_t>(blockIdx.x) * kCB;
-    const int nrb = gridDim.y;
+// U2: W = sum_rb Wpart[rb][cb] (fixed order);  W2[cb] = T^T W (or T W).
+// One CTA per column block, so the partials are summed once, not once per
+// row block of the apply.
+__global__ void __launch_bounds__(256) update_reduce_kernel(UpdArgs u, const double* Wpart, int nrb, double* W2g) {
+    __shared__ double W[kNbMax][kCB + 1];
+    __shared__ double Ts[kNbMax][kNbMax + 1];
+    const int tid = threadIdx.x;
+    const int ncb = gridDim.x;
     for (int e = tid; e < kNbMax * kCB; e += 256) {
-        double acc = 0.0;
-        for (int rb = 0; rb < nrb; ++rb) acc += Wpart[(static_cast<int64_t>(rb) * gridDim.x + blockIdx.x) * (kNbMax * kCB) + e];
-        W[(e / kCB) * (kCB + 1) + e % kCB] = acc;
+        const double* src = Wpart + static_cast<int64_t>(blockIdx.x) * (kNbMax * kCB) + e;
+        const int64_t step = static_cast<int64_t>(ncb) * (kNbMax * kCB);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int rb = 0;
+        for (; rb + 4 <= nrb; rb += 4) {
+            a0 += src[(rb + 0) * step];
+            a1 += src[(rb + 1) * step];
+            a2 += src[(rb + 2) * step];
+            a3 += src[(rb + 3) * step];
+        }
+        for (; rb < nrb; ++rb) a0 += src[rb * step];
+        W[e / kCB][e % kCB] = (a0 + a1) + (a2 + a3);
     }
-    for (int e = tid; e < kNbMax * kNbMax; e += 256) Ts[(e % kNbMax) * (kNbMax + 1) + e / kNbMax] = u.T[e];  // Ts[i][j] = T(i,j)
-    stage_v(u, r0, Vs);
-    stage_c(u, r0, c0, Cs);
+    for (int e = tid; e < kNbMax * kNbMax; e += 256) Ts[e % kNbMax][e / kNbMax] = u.T[e];  // Ts[i][j] = T(i,j)
     __syncthreads();
+    double* out = W2g + static_cast<int64_t>(blockIdx.x) * (kNbMax * kCB);
     for (int e = tid; e < kNbMax * kCB; e += 256) {
         const int a = e / kCB, c = e % kCB;
         double acc = 0.0;
         if (u.transT) {
-            for (int b = 0; b <= a; ++b) acc += Ts[b * (kNbMax + 1) + a] * W[b * (kCB + 1) + c];
+            for (int b = 0; b <= a; ++b) acc += Ts[b][a] * W[b][c];
         } else {
-            for (int b = a; b < kNbMax; ++b) acc += Ts[a * (kNbMax + 1) + b] * W[b * (kCB + 1) + c];
+            for (int b = a; b < kNbMax; ++b) acc += Ts[a][b] * W[b][c];
         }
-        W2[a * (kCB + 1) + c] = acc;
+        out[e] = acc;
     }
+}
+
+// U3: C_rb -= V_rb W2[cb]
+__global__ void __launch_bounds__(256) update_apply_kernel(UpdArgs u, const double* W2g) {
+    extern __shared__ __align__(16) double sm[];
+    double* Vs = sm;
+    double* Cs = sm + kNbMax * kLdT;
+    double* W2 = Cs + kCB * kLdT;             // [kNbMax][kCB + 1]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lr = lane & 3, lg = lane >> 2;
+    const int64_t r0 = u.k0 + static_cast<int64_t>(blockIdx.y) * kRB;
+    const int64_t c0 = u.c_begin + static_cast<int64_t>(blockIdx.x) * kCB;
+    const double* w2 = W2g + static_cast<int64_t>(blockIdx.x) * (kNbMax * kCB);
+    for (int e = tid; e < kNbMax * kCB; e += 256) W2[(e / kCB) * (kCB + 1) + e % kCB] = w2[e];
+    stage_v(u, r0, Vs);
+    stage_c(u, r0, c0, Cs);
     __syncthreads();
     // output tiles: (kRB/8) x (kCB/8) = 16 x 4 = 64; warp w owns 8 (two row tiles x four c tiles)
 #pragma unroll
@@ -908,14 +927,17 @@ void launch_update(slq_ctx* ctx, const UpdArgs& u) {
     if (u.c_end <= u.c_begin || u.r_end <= u.k0) return;
     const unsigned ncb = static_cast<unsigned>(ceil_div(u.c_end - u.c_begin, kCB));
     const unsigned nrb = static_cast<unsigned>(ceil_div(u.r_end - u.k0, kRB));
-    double* Wpart = static_cast<double*>(ctx->ws.qr_w.ensure(sizeof(double) * kNbMax * kCB * ncb * nrb));
+    double* Wpart = static_cast<double*>(ctx->ws.qr_w.ensure(sizeof(double) * kNbMax * kCB * ncb * (nrb + 1)));
+    double* W2 = Wpart + static_cast<int64_t>(kNbMax) * kCB * ncb * nrb;
     const size_t sm1 = sizeof(double) * (kNbMax + kCB) * kLdT;
-    const size_t sm2 = sm1 + sizeof(double) * (2 * kNbMax * (kCB + 1) + kNbMax * (kNbMax + 1));
+    const size_t sm2 = sm1 + sizeof(double) * kNbMax * (kCB + 1);
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(update_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm1)));
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(update_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2)));
     update_w_kernel<<<dim3(ncb, nrb), 256, sm1, ctx->stream>>>(u, Wpart);
     SLQ_LAUNCH_CHECK(ctx);
-    update_apply_kernel<<<dim3(ncb, nrb), 256, sm2, ctx->stream>>>(u, Wpart);
+    update_reduce_kernel<<<ncb, 256, 0, ctx->stream>>>(u, Wpart, static_cast<int>(nrb), W2);
+    SLQ_LAUNCH_CHECK(ctx);
+    update_apply_kernel<<<dim3(ncb, nrb), 256, sm2, ctx->stream>>>(u, W2);
     SLQ_LAUNCH_CHECK(ctx);
 }
 

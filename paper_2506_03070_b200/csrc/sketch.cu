@@ -239,7 +239,10 @@ struct BucketArgs {
     uint16_t* ent_out;
     int cap;                         // smem key capacity (power of 2)
     int* overflow;
+    int slots;                       // 1: entries as gather_kernel slots (see below)
 };
+
+__device__ __forceinline__ int gslot(int k, int h);
 
 __global__ void __launch_bounds__(1024) bucketize_kernel(BucketArgs a) {
     extern __shared__ uint32_t keys[];
@@ -291,7 +294,12 @@ __global__ void __launch_bounds__(1024) bucketize_kernel(BucketArgs a) {
     uint16_t* ptr = a.ptr_out + c * a.ptr_stride;
     const uint32_t lowmask = (1u << sh) - 1u;
     for (int i = tid; i < N; i += T) {
-        ent[i] = static_cast<uint16_t>(keys[i] & lowmask);
+        const uint32_t kv = keys[i] & lowmask;  // k_local << 1 | neg
+        // slots: byte offset of the entry's first 16-byte half in the A stage
+        // (the second is at offset ^ 16) with the sign in bit 0, so the
+        // gather decodes an entry with a few logic ops
+        ent[i] = a.slots ? static_cast<uint16_t>((gslot(static_cast<int>(kv >> 1), 0) << 4) | (kv & 1u))
+                         : static_cast<uint16_t>(kv);
         const int64_t r = keys[i] >> sh;
         const int64_t rp = (i == 0) ? -1 : static_cast<int64_t>(keys[i - 1] >> sh);
         for (int64_t rr = rp + 1; rr <= r; ++rr) ptr[rr] = static_cast<uint16_t>(i);
@@ -328,7 +336,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // 16-byte half h of A-slab row k (4 columns = 32 bytes) lives at slot
 // 2k + (h ^ ((k >> 2) & 1)): the first halves of random rows then spread over
 // all eight 16-byte bank groups (row parity x bit 2 of k), as do the second.
-__device__ __forceinline__ int gslot(int k, int h) { return 2 * k + (h ^ ((k >> 2) & 1)); }
+__device__ __forceinline__ int gslot(int k, int h) { return 2 * k + (h ^ ((k >> 2) & 1)); }  // gslot(k,1) == gslot(k,0)^1
 
 __device__ __forceinline__ void stage_chunk(const GatherArgs& g, int64_t col0, int64_t c, double* As, uint16_t* Ps,
                                             uint16_t* Es) {
@@ -376,6 +384,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
     auto Ps = [&](int s) { return reinterpret_cast<uint16_t*>(smem + s * st_bytes + a_bytes); };
     auto Es = [&](int s) { return reinterpret_cast<uint16_t*>(smem + s * st_bytes + a_bytes + p_bytes); };
 
+    const uint64_t vbits = static_cast<uint64_t>(__double_as_longlong(g.val));
     double y[RPT][4];
 #pragma unroll
     for (int q = 0; q < RPT; ++q)
@@ -390,7 +399,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
         cp_commit();
         cp_wait<1>();
         __syncthreads();
-        const double* A_s = As(s);
+        const unsigned char* A_b = reinterpret_cast<const unsigned char*>(As(s));
         const uint16_t* P_s = Ps(s);
         const uint16_t* E_s = Es(s);
 #pragma unroll
@@ -400,10 +409,10 @@ __global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
                 const int e0 = P_s[r], e1 = P_s[r + 1];
                 for (int e = e0; e < e1; ++e) {
                     const unsigned en = E_s[e];
-                    const int k = static_cast<int>(en >> 1);
-                    const double v = (en & 1u) ? -g.val : g.val;
-                    const double2 lo = *reinterpret_cast<const double2*>(A_s + 2 * gslot(k, 0));
-                    const double2 hi = *reinterpret_cast<const double2*>(A_s + 2 * gslot(k, 1));
+                    const unsigned o0 = en & 0xFFF0u;
+                    const double v = __longlong_as_double(static_cast<long long>(vbits ^ (static_cast<uint64_t>(en) << 63)));
+                    const double2 lo = *reinterpret_cast<const double2*>(A_b + o0);
+                    const double2 hi = *reinterpret_cast<const double2*>(A_b + (o0 ^ 16u));
                     y[q][0] = acc_step<EXACT>(y[q][0], v, lo.x);
                     y[q][1] = acc_step<EXACT>(y[q][1], v, lo.y);
                     y[q][2] = acc_step<EXACT>(y[q][2], v, hi.x);
@@ -904,7 +913,7 @@ void generate_sparse_rows_dev(slq_ctx* ctx, int64_t n, int64_t nnz, uint64_t see
 }
 
 ChunkCsr build_chunk_csr(slq_ctx* ctx, const uint32_t* compact, const int64_t* colptr_dev, int64_t zeta_max,
-                         int64_t m, int64_t d) {
+                         int64_t m, int64_t d, bool gather_slots) {
     Workspace& ws = ctx->ws;
     ChunkCsr cc;
     cc.plan = plan_chunks(m, d, zeta_max);
@@ -915,7 +924,7 @@ ChunkCsr build_chunk_csr(slq_ctx* ctx, const uint32_t* compact, const int64_t* c
     cc.flag = static_cast<int*>(ws.flags.ensure(4096));
     SLQ_CUDA_CHECK(cudaMemsetAsync(cc.flag, 0, sizeof(int), ctx->stream));
     BucketArgs ba{compact, colptr_dev, zeta_max, m, d, cp.K, cp.KB, cp.ptr_stride, cp.ent_stride, cc.ptr, cc.ent,
-                  cp.cap, cc.flag};
+                  cp.cap, cc.flag, gather_slots ? 1 : 0};
     const size_t bsmem = sizeof(uint32_t) * cp.cap;
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(bucketize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(bsmem)));
@@ -946,7 +955,7 @@ void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const
     // d = 4n, slower than the register-row gather (one entry per warp
     // instruction vs 32): opt-in for experiments only
     if (slq_env_flag("SLQ_SLAB_GATHER") && sketch_apply_slab(ctx, A, d, compact, colptr_dev, zeta, val, exact, Y)) return;
-    ChunkCsr cc = build_chunk_csr(ctx, compact, colptr_dev, zeta, m, d);
+    ChunkCsr cc = build_chunk_csr(ctx, compact, colptr_dev, zeta, m, d, true);
     const ChunkPlan& cp = cc.plan;
     uint16_t* ptr = cc.ptr;
     uint16_t* ent = cc.ent;

@@ -337,18 +337,34 @@ __global__ void __launch_bounds__(288, 1) sparse_pass_kernel(SPassArgs a) {
     double ssq = 0.0;
     const double* ubase = a.u_in ? a.u_in : a.b;
     if (warp == W) {
-        if (lane == 0) {
-            for (int64_t k = 0; k < nt; ++k) {
-                const int s = static_cast<int>(k % a.S);
-                const int64_t r = k / a.S;
-                if (r > 0) mbar_wait(&empty[s], static_cast<unsigned>((r - 1) & 1));
+        // producer: the tile bounds (two row pointers each) are prefetched 32
+        // tiles at a time by the warp's lanes, so issuing a tile's copies never
+        // waits on a dependent global load
+        int s = -1;
+        unsigned ph = 1;
+        int64_t pre_lo = 0, pre_hi = 0;
+        for (int64_t k = 0; k < nt; ++k) {
+            if ((k & 31) == 0) {
+                const int64_t kk = k + lane;
+                if (kk < nt) {
+                    const int64_t r0 = (t0 + kk) * a.R;
+                    pre_lo = a.rowptr[r0];
+                    pre_hi = a.rowptr[min(a.m, r0 + a.R)];
+                }
+            }
+            const int64_t lo = __shfl_sync(0xffffffffu, pre_lo, static_cast<int>(k & 31));
+            const int64_t hi = __shfl_sync(0xffffffffu, pre_hi, static_cast<int>(k & 31));
+            if (++s == a.S) {
+                s = 0;
+                ph ^= 1u;
+            }
+            if (lane == 0) {
+                if (k >= a.S) mbar_wait(&empty[s], ph);
                 const int64_t row0 = (t0 + k) * a.R;
-                const int64_t row1 = min(a.m, row0 + a.R);
-                const int64_t base = a.rowptr[row0] & ~int64_t(3);
-                const int64_t cnt = ((a.rowptr[row1] - base) + 3) & ~int64_t(3);
+                const int64_t base = lo & ~int64_t(3);
+                const int64_t cnt = ((hi - base) + 3) & ~int64_t(3);
                 unsigned char* st = smem + s * st_bytes;
-                const unsigned bytes =
-                    static_cast<unsigned>(cnt * 8 + cnt * 4 + st_rp + st_u);
+                const unsigned bytes = static_cast<unsigned>(cnt * 8 + cnt * 4 + st_rp + st_u);
                 mbar_expect_tx(&full[s], bytes);
                 if (cnt > 0) {
                     bulk_g2s(st, a.vals + base, static_cast<unsigned>(cnt * 8), &full[s]);
@@ -357,14 +373,19 @@ __global__ void __launch_bounds__(288, 1) sparse_pass_kernel(SPassArgs a) {
                 bulk_g2s(st + st_vals + st_cols, a.rowptr + row0, static_cast<unsigned>(st_rp), &full[s]);
                 bulk_g2s(st + st_vals + st_cols + st_rp, ubase + row0, static_cast<unsigned>(st_u), &full[s]);
             }
+            __syncwarp();
         }
-        __syncwarp();
     } else {
         const double c = a.coef ? *a.coef : a.c_fixed;
         double* zw = z_s + static_cast<int64_t>(warp) * n;
+        int s = -1;
+        unsigned ph = 1;
         for (int64_t k = 0; k < nt; ++k) {
-            const int s = static_cast<int>(k % a.S);
-            mbar_wait(&full[s], static_cast<unsigned>((k / a.S) & 1));
+            if (++s == a.S) {
+                s = 0;
+                ph ^= 1u;
+            }
+            mbar_wait(&full[s], ph ^ 1u);
             const unsigned char* st = smem + s * st_bytes;
             const double* sv = reinterpret_cast<const double*>(st);
             const int32_t* sc = reinterpret_cast<const int32_t*>(st + st_vals);
@@ -373,32 +394,45 @@ __global__ void __launch_bounds__(288, 1) sparse_pass_kernel(SPassArgs a) {
             const int64_t row0 = (t0 + k) * a.R;
             const int rows = static_cast<int>(min(static_cast<int64_t>(a.R), a.m - row0));
             const int64_t base = srp[0] & ~int64_t(3);
-            for (int i = warp; i < rows; i += W) {
-                const int b0 = static_cast<int>(srp[i] - base), b1 = static_cast<int>(srp[i + 1] - base);
-                int32_t cc[2];
-                double vv[2];
+            // four rows per warp step, eight lanes per row for A p (three
+            // independent reduction trees in flight instead of one), then the
+            // rows' A^T u_hat scatter one row at a time with all lanes (rows
+            // may share columns; a row's columns are distinct, so lanes never
+            // collide inside one scatter)
+            const int g = lane >> 3, sub = lane & 7;
+            for (int i0 = warp * 4; i0 < rows; i0 += 4 * W) {
+                const int i = i0 + g;
+                const bool rv = i < rows;
+                const int b0 = rv ? static_cast<int>(srp[i] - base) : 0;
+                const int b1 = rv ? static_cast<int>(srp[i + 1] - base) : 0;
                 double acc = 0.0;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int t = b0 + lane + 32 * h;
-                    const bool ok = t < b1;
-                    cc[h] = ok ? sc[t] : 0;
-                    vv[h] = ok ? sv[t] : 0.0;
-                    acc = fma(vv[h], p_s[cc[h]], acc);
+                for (int t = b0 + sub; t < b1; t += 8) acc = fma(sv[t], p_s[sc[t]], acc);
+                acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+                acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+                acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                const double uh = rv ? __dadd_rn(acc, __dmul_rn(c, su[i])) : 0.0;
+                if (rv && sub == 0) {
+                    if (a.u_out) a.u_out[row0 + i] = uh;
+                    ssq = fma(uh, uh, ssq);
                 }
-                for (int t = b0 + 64 + lane; t < b1; t += 32) acc = fma(sv[t], p_s[sc[t]], acc);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                const double uh = __dadd_rn(acc, __dmul_rn(c, su[i]));
-                if (lane == 0 && a.u_out) a.u_out[row0 + i] = uh;
-                ssq = fma(uh, uh, ssq);
                 if (a.want_z) {
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-                        if (b0 + lane + 32 * h < b1) zw[cc[h]] = fma(vv[h], uh, zw[cc[h]]);
-                    for (int t = b0 + 64 + lane; t < b1; t += 32) zw[sc[t]] = fma(sv[t], uh, zw[sc[t]]);
+                    const int ng = rows - i0 < 4 ? rows - i0 : 4;
+                    for (int gg = 0; gg < ng; ++gg) {
+                        const double ug = __shfl_sync(0xffffffffu, uh, gg * 8);
+                        const int c0 = __shfl_sync(0xffffffffu, b0, gg * 8), c1 = __shfl_sync(0xffffffffu, b1, gg * 8);
+                        // first 64 entries with both loads issued before the
+                        // read-modify-writes (a row's columns are distinct)
+                        const int ta = c0 + lane, tb = c0 + 32 + lane;
+                        const bool oka = ta < c1, okb = tb < c1;
+                        const int ca = oka ? sc[ta] : 0, cb = okb ? sc[tb] : 0;
+                        const double va = oka ? sv[ta] : 0.0, vb = okb ? sv[tb] : 0.0;
+                        const double za = oka ? zw[ca] : 0.0, zb = okb ? zw[cb] : 0.0;
+                        if (oka) zw[ca] = fma(va, ug, za);
+                        if (okb) zw[cb] = fma(vb, ug, zb);
+                        for (int t = c0 + 64 + lane; t < c1; t += 32) zw[sc[t]] = fma(sv[t], ug, zw[sc[t]]);
+                        __syncwarp();
+                    }
                 }
-                __syncwarp();
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
@@ -406,6 +440,8 @@ __global__ void __launch_bounds__(288, 1) sparse_pass_kernel(SPassArgs a) {
     }
     __syncthreads();
     double* red = reinterpret_cast<double*>(smem);  // stage memory is free now
+    ssq += __shfl_xor_sync(0xffffffffu, ssq, 8);     // lanes 0, 8, 16, 24 hold the row-group sums
+    ssq += __shfl_xor_sync(0xffffffffu, ssq, 16);
     if (warp < W && lane == 0) red[warp] = ssq;
     __syncthreads();
     double* outp = a.part + static_cast<int64_t>(blockIdx.x) * (n + 1);
@@ -509,7 +545,7 @@ void sketch_apply_sparse_compact_dev(slq_ctx* ctx, const slq_sparse* A, int64_t 
         SLQ_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(double) * d * (n + 1), ctx->stream));
         return;
     }
-    ChunkCsr cc = build_chunk_csr(ctx, compact, colptr_dev, zeta_max, m, d);
+    ChunkCsr cc = build_chunk_csr(ctx, compact, colptr_dev, zeta_max, m, d, false);
     // S^T rows (entries of each Y row in ascending k)
     DevBuf srp, scan_tmp;
     int64_t* srow_ptr = static_cast<int64_t*>(srp.ensure(sizeof(int64_t) * (d + 1)));
