@@ -375,6 +375,9 @@ int slq_ctx_destroy(slq_ctx* ctx) {
         cudaStreamSynchronize(ctx->stream);
         slq::comm_destroy(ctx);
         if (ctx->lsqr_exec) cudaGraphExecDestroy(ctx->lsqr_exec);
+        if (ctx->lsqr_hdone) cudaFreeHost(ctx->lsqr_hdone);
+        for (cudaEvent_t e : ctx->lsqr_ev)
+            if (e) cudaEventDestroy(e);
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
         delete ctx;
     });

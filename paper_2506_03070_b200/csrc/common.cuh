@@ -104,6 +104,8 @@ struct slq_ctx {
     // cached LSQR iteration graph (rebuilt when any captured pointer / size changes)
     cudaGraphExec_t lsqr_exec = nullptr;
     std::vector<uint64_t> lsqr_key;
+    int* lsqr_hdone = nullptr;            // pinned done-flag mirror (2 ints)
+    cudaEvent_t lsqr_ev[2] = {nullptr, nullptr};
 };
 
 struct slq_dense {

@@ -759,12 +759,23 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
             }
         }
         cudaGraphExec_t exec = use_graph ? ctx->lsqr_exec : nullptr;
-        int* hdone = nullptr;
-        SLQ_CUDA_CHECK(cudaMallocHost(&hdone, 2 * sizeof(int)));
+        // pinned done-flag mirror and batch events live in the context (a
+        // cudaMallocHost per solve costs milliseconds of host time during
+        // which the device can idle)
+        if (!ctx->lsqr_hdone) {
+            SLQ_CUDA_CHECK(cudaMallocHost(&ctx->lsqr_hdone, 2 * sizeof(int)));
+            for (int i = 0; i < 2; ++i) SLQ_CUDA_CHECK(cudaEventCreate(&ctx->lsqr_ev[i]));
+        }
+        int* hdone = ctx->lsqr_hdone;
         hdone[0] = hdone[1] = 0;
-        cudaEvent_t ev[2];
-        SLQ_CUDA_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-        SLQ_CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+        cudaEvent_t* ev = ctx->lsqr_ev;
+        static const bool trace = slq_env_flag("SLQ_TRACE");
+        cudaEvent_t tb[16];
+        int ntb = 0;
+        if (trace) {
+            SLQ_CUDA_CHECK(cudaEventCreate(&tb[0]));
+            SLQ_CUDA_CHECK(cudaEventRecord(tb[ntb++], ctx->stream));
+        }
         int64_t launched = 0;
         int64_t k = 0;
         while (launched < maxit) {
@@ -775,6 +786,10 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
                 for (int b = 0; b < kBatch; ++b) enqueue_iteration();
             }
             launched += kBatch;
+            if (trace && ntb < 16) {
+                SLQ_CUDA_CHECK(cudaEventCreate(&tb[ntb]));
+                SLQ_CUDA_CHECK(cudaEventRecord(tb[ntb++], ctx->stream));
+            }
             SLQ_CUDA_CHECK(cudaMemcpyAsync(&hdone[k & 1], done_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
             SLQ_CUDA_CHECK(cudaEventRecord(ev[k & 1], ctx->stream));
             if (k > 0) {
@@ -784,9 +799,18 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
             ++k;
         }
         SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-        cudaEventDestroy(ev[0]);
-        cudaEventDestroy(ev[1]);
-        cudaFreeHost(hdone);
+        if (trace) {
+            float t0 = 0.f;
+            SLQ_CUDA_CHECK(cudaEventElapsedTime(&t0, e0, tb[0]));
+            std::fprintf(stderr, "[slq] lsqr: init %.3f ms; batches (8 it):", t0);
+            for (int i = 1; i < ntb; ++i) {
+                float t = 0.f;
+                SLQ_CUDA_CHECK(cudaEventElapsedTime(&t, tb[i - 1], tb[i]));
+                std::fprintf(stderr, " %.3f", t);
+            }
+            std::fprintf(stderr, " ms\n");
+            for (int i = 0; i < ntb; ++i) cudaEventDestroy(tb[i]);
+        }
     }
     SLQ_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
     if (l2_window) {

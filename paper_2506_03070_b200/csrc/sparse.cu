@@ -152,16 +152,6 @@ __global__ void csr_sort_rows(const int64_t* rowptr, int64_t m, int32_t* colidx,
     }
 }
 
-__global__ void max_tile_nnz_kernel(const int64_t* rowptr, int64_t m, int R, unsigned long long* out) {
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t r0 = t * R;
-    if (r0 >= m) return;
-    const int64_t r1 = min(m, r0 + R);
-    const int64_t base = rowptr[r0] & ~int64_t(3);
-    const int64_t cnt = ((rowptr[r1] - base) + 3) & ~int64_t(3);
-    atomicMax(out, static_cast<unsigned long long>(cnt));
-}
-
 // ------------------------------------------------- S^T CSR from chunk-CSR
 
 // warp per sketch row r: lane l handles chunks l, l+32, ...
@@ -282,8 +272,22 @@ __global__ void __launch_bounds__(512) sparse_gather_kernel(SGatherArgs g) {
 }
 
 // ------------------------------------------------------------ K4s pass
+//
+// One sweep over the CSR rows computes u_hat = A p + c u, ||u_hat||^2 and
+// z = A^T u_hat -- the sparse twin of the dense fused pass (lsqr.hpp:115-127
+// with SerialOperator<CscMatrix>).  A's values and column indices go straight
+// from HBM to registers (each row read by 32 lanes, coalesced; the next row
+// quad is loaded while the current one is processed), so shared memory only
+// holds p and one private z copy per warp.  Per quad of 4 rows lane l holds
+// entries l and l+32 of each row; the four dot products are reduced together
+// (6 double shuffles instead of 20); the scatter z[col] += v u_hat then runs
+// row by row -- a row's columns are distinct, so lanes never collide, and
+// rows are ordered by __syncwarp.  Rows longer than 64 entries take a slow
+// tail loop.  Deterministic: fixed row -> warp assignment and fixed orders.
 
 using namespace ptx;
+
+constexpr int kSpMaxWarps = 16;
 
 struct SPassArgs {
     const int64_t* rowptr;
@@ -299,161 +303,176 @@ struct SPassArgs {
     double* part;         // [grid][n+1]
     int want_z;
     const int* skip;
-    int R, S, W;          // rows per tile, stages, consumer warps (= z copies)
-    int64_t cap;          // nnz capacity of a stage (multiple of 4)
 };
 
-__global__ void __launch_bounds__(288, 1) sparse_pass_kernel(SPassArgs a) {
-    extern __shared__ __align__(128) unsigned char smem[];
+struct SpQuad {
+    double v[8];    // entry lane (+32) of row g at [2g] ([2g+1]); garbage where not live
+    int c[8];
+    double u;       // u of row (lane >> 3)
+    unsigned cnt;   // row lengths, 8 bits each (255 = 255 or more: slow tail)
+};
+
+__device__ __forceinline__ int sp_cnt(unsigned pk, int g) { return static_cast<int>((pk >> (8 * g)) & 255u); }
+
+// Loads are unconditional (out-of-row slots read entry 0, always allocated)
+// so none of them is waited on here; liveness is applied at use.
+__device__ __forceinline__ void sp_load_quad(const SPassArgs& a, const double* ubase, int64_t r0, int64_t r_end,
+                                             int64_t rp, int lane, SpQuad& q) {
+    q.cnt = 0;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        const int64_t lo = __shfl_sync(0xffffffffu, rp, g);
+        const int64_t hi = __shfl_sync(0xffffffffu, rp, g + 1);
+        const int64_t len = r0 + g < r_end ? hi - lo : 0;
+        const int cnt = static_cast<int>(len < 255 ? len : 255);
+        q.cnt |= static_cast<unsigned>(cnt) << (8 * g);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int t = lane + 32 * j;
+            const int64_t idx = t < cnt ? lo + t : 0;
+            q.c[2 * g + j] = __ldcs(a.colidx + idx);
+            q.v[2 * g + j] = __ldcs(a.vals + idx);
+        }
+    }
+    const int64_t ru = r0 + (lane >> 3);
+    q.u = ubase[ru < r_end ? ru : r_end - 1];
+}
+
+struct SpCtx {
+    int64_t R0, R1, nq;
+    int W, lane;
+    double c;
+    const double* p_s;
+    double* zw;
+    const double* ubase;
+};
+
+// Process quad q (held in `cur`) and start loading quad q + 2W into `fill`.
+__device__ __forceinline__ void sp_step(const SPassArgs& a, const SpCtx& x, int64_t q, SpQuad& cur, SpQuad& fill,
+                                        int64_t& rp_next, double& ssq) {
+    const int lane = x.lane, W = x.W;
+    if (q + 2 * W < x.nq) sp_load_quad(a, x.ubase, x.R0 + 4 * (q + 2 * W), x.R1, rp_next, lane, fill);
+    {
+        const int64_t r = x.R0 + 4 * (q + 3 * W) + (lane < 5 ? lane : 4);
+        rp_next = __ldcs(a.rowptr + (r < x.R1 ? r : x.R1));
+    }
+    // ---- A p for the four rows
+    double acc[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        const int cg = sp_cnt(cur.cnt, g);
+        const bool oka = lane < cg, okb = lane + 32 < cg;
+        if (!oka) cur.v[2 * g] = 0.0, cur.c[2 * g] = 0;
+        if (!okb) cur.v[2 * g + 1] = 0.0, cur.c[2 * g + 1] = 0;
+        acc[g] = fma(cur.v[2 * g + 1], x.p_s[cur.c[2 * g + 1]], cur.v[2 * g] * x.p_s[cur.c[2 * g]]);
+        if (cg > 64) {  // warp-uniform slow tail (rows longer than 64 entries)
+            const int64_t r = x.R0 + 4 * q + g;
+            const int64_t e = a.rowptr[r + 1];
+            for (int64_t t = a.rowptr[r] + 64 + lane; t < e; t += 32) acc[g] = fma(a.vals[t], x.p_s[a.colidx[t]], acc[g]);
+        }
+    }
+    // four-way warp reduction: lane group g ends with row g's sum
+    const bool h16 = lane & 16, h8 = lane & 8;
+    double k0 = h16 ? acc[2] : acc[0], k1 = h16 ? acc[3] : acc[1];
+    k0 += __shfl_xor_sync(0xffffffffu, h16 ? acc[0] : acc[2], 16);
+    k1 += __shfl_xor_sync(0xffffffffu, h16 ? acc[1] : acc[3], 16);
+    double kk = h8 ? k1 : k0;
+    kk += __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
+    kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+    kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+    kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+    const int64_t rme = x.R0 + 4 * q + (lane >> 3);
+    const double uh = (rme < x.R1) ? __dadd_rn(kk, __dmul_rn(x.c, cur.u)) : 0.0;
+    if ((lane & 7) == 0 && rme < x.R1) {
+        if (a.u_out) a.u_out[rme] = uh;
+        ssq = fma(uh, uh, ssq);
+    }
+    // ---- z += A^T u_hat, row by row
+    if (a.want_z) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const double ug = __shfl_sync(0xffffffffu, uh, 8 * g);
+            const int cg = sp_cnt(cur.cnt, g);
+            const bool oka = lane < cg, okb = lane + 32 < cg;
+            const double za = oka ? x.zw[cur.c[2 * g]] : 0.0;
+            const double zb = okb ? x.zw[cur.c[2 * g + 1]] : 0.0;
+            if (oka) x.zw[cur.c[2 * g]] = fma(cur.v[2 * g], ug, za);
+            if (okb) x.zw[cur.c[2 * g + 1]] = fma(cur.v[2 * g + 1], ug, zb);
+            if (cg > 64) {
+                const int64_t r = x.R0 + 4 * q + g;
+                const int64_t e = a.rowptr[r + 1];
+                for (int64_t t = a.rowptr[r] + 64 + lane; t < e; t += 32) {
+                    const int cc = a.colidx[t];
+                    x.zw[cc] = fma(a.vals[t], ug, x.zw[cc]);
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(32 * kSpMaxWarps, 1) sparse_pass_kernel(SPassArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
     if (a.skip && *a.skip) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int W = a.W;
+    const int W = blockDim.x >> 5;
     const int64_t n = a.n;
-    // layout: stages [S] x {vals cap f64 | cols cap i32 | rowptr R+2 i64 | u R f64}, p[n], z[W][n], bars
-    const size_t st_vals = static_cast<size_t>(a.cap) * 8, st_cols = static_cast<size_t>(a.cap) * 4;
-    const size_t st_rp = static_cast<size_t>(a.R + 2) * 8, st_u = static_cast<size_t>(a.R) * 8;
-    const size_t st_bytes = st_vals + st_cols + st_rp + st_u;
-    double* p_s = reinterpret_cast<double*>(smem + a.S * st_bytes);
+    double* p_s = reinterpret_cast<double*>(smem);
     double* z_s = p_s + n;
-    uint64_t* full = reinterpret_cast<uint64_t*>(z_s + static_cast<int64_t>(W) * n);
-    uint64_t* empty = full + a.S;
-
-    const int64_t ntiles = (a.m + a.R - 1) / a.R;
-    const int64_t t0 = blockIdx.x * ntiles / gridDim.x;
-    const int64_t t1 = (blockIdx.x + 1) * ntiles / gridDim.x;
-    const int64_t nt = t1 - t0;
-
-    if (tid == 0) {
-        for (int s = 0; s < a.S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], W);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
     for (int64_t j = tid; j < n; j += blockDim.x) p_s[j] = a.p[j];
     for (int64_t j = tid; j < static_cast<int64_t>(W) * n; j += blockDim.x) z_s[j] = 0.0;
     __syncthreads();
 
-    double ssq = 0.0;
+    const int64_t R0 = blockIdx.x * a.m / gridDim.x, R1 = (blockIdx.x + 1) * a.m / gridDim.x;
+    const int64_t nq = (R1 - R0 + 3) / 4;
+    const double c = a.coef ? *a.coef : a.c_fixed;
     const double* ubase = a.u_in ? a.u_in : a.b;
-    if (warp == W) {
-        // producer: the tile bounds (two row pointers each) are prefetched 32
-        // tiles at a time by the warp's lanes, so issuing a tile's copies never
-        // waits on a dependent global load
-        int s = -1;
-        unsigned ph = 1;
-        int64_t pre_lo = 0, pre_hi = 0;
-        for (int64_t k = 0; k < nt; ++k) {
-            if ((k & 31) == 0) {
-                const int64_t kk = k + lane;
-                if (kk < nt) {
-                    const int64_t r0 = (t0 + kk) * a.R;
-                    pre_lo = a.rowptr[r0];
-                    pre_hi = a.rowptr[min(a.m, r0 + a.R)];
-                }
-            }
-            const int64_t lo = __shfl_sync(0xffffffffu, pre_lo, static_cast<int>(k & 31));
-            const int64_t hi = __shfl_sync(0xffffffffu, pre_hi, static_cast<int>(k & 31));
-            if (++s == a.S) {
-                s = 0;
-                ph ^= 1u;
-            }
-            if (lane == 0) {
-                if (k >= a.S) mbar_wait(&empty[s], ph);
-                const int64_t row0 = (t0 + k) * a.R;
-                const int64_t base = lo & ~int64_t(3);
-                const int64_t cnt = ((hi - base) + 3) & ~int64_t(3);
-                unsigned char* st = smem + s * st_bytes;
-                const unsigned bytes = static_cast<unsigned>(cnt * 8 + cnt * 4 + st_rp + st_u);
-                mbar_expect_tx(&full[s], bytes);
-                if (cnt > 0) {
-                    bulk_g2s(st, a.vals + base, static_cast<unsigned>(cnt * 8), &full[s]);
-                    bulk_g2s(st + st_vals, a.colidx + base, static_cast<unsigned>(cnt * 4), &full[s]);
-                }
-                bulk_g2s(st + st_vals + st_cols, a.rowptr + row0, static_cast<unsigned>(st_rp), &full[s]);
-                bulk_g2s(st + st_vals + st_cols + st_rp, ubase + row0, static_cast<unsigned>(st_u), &full[s]);
-            }
-            __syncwarp();
-        }
-    } else {
-        const double c = a.coef ? *a.coef : a.c_fixed;
-        double* zw = z_s + static_cast<int64_t>(warp) * n;
-        int s = -1;
-        unsigned ph = 1;
-        for (int64_t k = 0; k < nt; ++k) {
-            if (++s == a.S) {
-                s = 0;
-                ph ^= 1u;
-            }
-            mbar_wait(&full[s], ph ^ 1u);
-            const unsigned char* st = smem + s * st_bytes;
-            const double* sv = reinterpret_cast<const double*>(st);
-            const int32_t* sc = reinterpret_cast<const int32_t*>(st + st_vals);
-            const int64_t* srp = reinterpret_cast<const int64_t*>(st + st_vals + st_cols);
-            const double* su = reinterpret_cast<const double*>(st + st_vals + st_cols + st_rp);
-            const int64_t row0 = (t0 + k) * a.R;
-            const int rows = static_cast<int>(min(static_cast<int64_t>(a.R), a.m - row0));
-            const int64_t base = srp[0] & ~int64_t(3);
-            // four rows per warp step, eight lanes per row for A p (three
-            // independent reduction trees in flight instead of one), then the
-            // rows' A^T u_hat scatter one row at a time with all lanes (rows
-            // may share columns; a row's columns are distinct, so lanes never
-            // collide inside one scatter)
-            const int g = lane >> 3, sub = lane & 7;
-            for (int i0 = warp * 4; i0 < rows; i0 += 4 * W) {
-                const int i = i0 + g;
-                const bool rv = i < rows;
-                const int b0 = rv ? static_cast<int>(srp[i] - base) : 0;
-                const int b1 = rv ? static_cast<int>(srp[i + 1] - base) : 0;
-                double acc = 0.0;
-                for (int t = b0 + sub; t < b1; t += 8) acc = fma(sv[t], p_s[sc[t]], acc);
-                acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-                acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-                acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-                const double uh = rv ? __dadd_rn(acc, __dmul_rn(c, su[i])) : 0.0;
-                if (rv && sub == 0) {
-                    if (a.u_out) a.u_out[row0 + i] = uh;
-                    ssq = fma(uh, uh, ssq);
-                }
-                if (a.want_z) {
-                    const int ng = rows - i0 < 4 ? rows - i0 : 4;
-                    for (int gg = 0; gg < ng; ++gg) {
-                        const double ug = __shfl_sync(0xffffffffu, uh, gg * 8);
-                        const int c0 = __shfl_sync(0xffffffffu, b0, gg * 8), c1 = __shfl_sync(0xffffffffu, b1, gg * 8);
-                        // first 64 entries with both loads issued before the
-                        // read-modify-writes (a row's columns are distinct)
-                        const int ta = c0 + lane, tb = c0 + 32 + lane;
-                        const bool oka = ta < c1, okb = tb < c1;
-                        const int ca = oka ? sc[ta] : 0, cb = okb ? sc[tb] : 0;
-                        const double va = oka ? sv[ta] : 0.0, vb = okb ? sv[tb] : 0.0;
-                        const double za = oka ? zw[ca] : 0.0, zb = okb ? zw[cb] : 0.0;
-                        if (oka) zw[ca] = fma(va, ug, za);
-                        if (okb) zw[cb] = fma(vb, ug, zb);
-                        for (int t = c0 + 64 + lane; t < c1; t += 32) zw[sc[t]] = fma(sv[t], ug, zw[sc[t]]);
-                        __syncwarp();
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-        }
+    double* zw = z_s + static_cast<int64_t>(warp) * n;
+    double ssq = 0.0;
+
+    auto rp_load = [&](int64_t q) -> int64_t {  // lanes 0..4: rowptr of the quad's rows (unconditional load)
+        const int64_t r = R0 + 4 * q + (lane < 5 ? lane : 4);
+        return __ldcs(a.rowptr + (r < R1 ? r : R1));
+    };
+    // three quads in flight per warp (the one being processed and the next
+    // two); the loop is unrolled by three so the buffers rotate by name
+    int64_t q = warp;
+    SpQuad qa, qb, qc;
+    int64_t rp_next = 0;
+    if (q < nq) {
+        const int64_t rpa = rp_load(q), rpb = rp_load(q + W);
+        sp_load_quad(a, ubase, R0 + 4 * q, R1, rpa, lane, qa);
+        sp_load_quad(a, ubase, R0 + 4 * (q + W), R1, rpb, lane, qb);
+        rp_next = rp_load(q + 2 * W);
     }
-    __syncthreads();
-    double* red = reinterpret_cast<double*>(smem);  // stage memory is free now
-    ssq += __shfl_xor_sync(0xffffffffu, ssq, 8);     // lanes 0, 8, 16, 24 hold the row-group sums
+    SpCtx x{R0, R1, nq, W, lane, c, p_s, zw, ubase};
+    while (q < nq) {
+        sp_step(a, x, q, qa, qc, rp_next, ssq);
+        q += W;
+        if (q >= nq) break;
+        sp_step(a, x, q, qb, qa, rp_next, ssq);
+        q += W;
+        if (q >= nq) break;
+        sp_step(a, x, q, qc, qb, rp_next, ssq);
+        q += W;
+    }
+    // ssq: lanes 0, 8, 16, 24 hold partial sums
+    ssq += __shfl_xor_sync(0xffffffffu, ssq, 8);
     ssq += __shfl_xor_sync(0xffffffffu, ssq, 16);
-    if (warp < W && lane == 0) red[warp] = ssq;
+    __syncthreads();
+    double* red = p_s;  // p is no longer needed
+    if (lane == 0) red[warp] = ssq;
     __syncthreads();
     double* outp = a.part + static_cast<int64_t>(blockIdx.x) * (n + 1);
     if (a.want_z)
         for (int64_t j = tid; j < n; j += blockDim.x) {
             double s = 0.0;
-            for (int q = 0; q < W; ++q) s += z_s[static_cast<int64_t>(q) * n + j];
+            for (int w = 0; w < W; ++w) s += z_s[static_cast<int64_t>(w) * n + j];
             outp[j] = s;
         }
     if (tid == 0) {
         double s = 0.0;
-        for (int q = 0; q < W; ++q) s += red[q];
+        for (int w = 0; w < W; ++w) s += red[w];
         outp[n] = s;
     }
 }
@@ -584,32 +603,14 @@ public:
     SparseOp(slq_ctx* ctx, const slq_sparse* A) : A_(A) {
         m = A->m;
         n = A->n;
-        // z copies (one per consumer warp) + p in shared memory; stages take the rest
+        // p + one z copy per warp in shared memory
         const int64_t zrow = n * static_cast<int64_t>(sizeof(double));
-        W_ = static_cast<int>(std::min<int64_t>(8, (150 * 1024) / std::max<int64_t>(zrow, 1) - 1));
+        const int64_t budget = 220 * 1024;
+        W_ = static_cast<int>(std::min<int64_t>(kSpMaxWarps, budget / std::max<int64_t>(zrow, 1) - 1));
         if (W_ < 1) fail(SLQ_UNSUPPORTED, "sparse lsqr: n too large for shared-memory z copies");
-        R_ = 32;
-        S_ = 3;
-        // stage capacity = max nnz of a tile (16-byte-rounded range)
-        DevBuf mx;
-        unsigned long long* dmx = static_cast<unsigned long long*>(mx.ensure(8));
-        SLQ_CUDA_CHECK(cudaMemsetAsync(dmx, 0, 8, ctx->stream));
-        const int64_t ntiles = ceil_div(std::max<int64_t>(m, 1), R_);
-        if (m > 0) {
-            max_tile_nnz_kernel<<<static_cast<unsigned>(ceil_div(ntiles, 256)), 256, 0, ctx->stream>>>(A->rowptr, m, R_,
-                                                                                                    dmx);
-            SLQ_LAUNCH_CHECK(ctx);
-        }
-        unsigned long long h = 0;
-        SLQ_CUDA_CHECK(cudaMemcpyAsync(&h, dmx, 8, cudaMemcpyDeviceToHost, ctx->stream));
-        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-        cap_ = std::max<int64_t>(4, static_cast<int64_t>(h));
-        const size_t fixed = static_cast<size_t>(zrow) * (W_ + 1) + 2 * S_ * sizeof(uint64_t) + 64;
-        auto stage = [&](int64_t cap) { return static_cast<size_t>(cap * 12 + (R_ + 2) * 8 + R_ * 8); };
-        while (fixed + S_ * stage(cap_) > 227 * 1024 && S_ > 2) --S_;
-        smem_ = fixed + S_ * stage(cap_);
-        if (smem_ > 227 * 1024) fail(SLQ_UNSUPPORTED, "sparse lsqr: row tile too dense for shared memory");
-        grid_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, ntiles)));
+        smem_ = static_cast<size_t>(zrow) * (W_ + 1);
+        if (smem_ < static_cast<size_t>(W_) * sizeof(double)) smem_ = static_cast<size_t>(W_) * sizeof(double);
+        grid_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, ceil_div(std::max<int64_t>(m, 1), 4 * W_))));
         SLQ_CUDA_CHECK(cudaFuncSetAttribute(sparse_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem_)));
     }
@@ -617,21 +618,20 @@ public:
     void pass(slq_ctx* ctx, const PassCall& c) const override {
         if (!c.u_in && !A_->b) fail(SLQ_INVALID_ARG, "sparse lsqr: no right-hand side");
         SPassArgs a{A_->rowptr, A_->colidx, A_->vals, A_->b, m, n, c.p, c.u_in, c.u_out, c.coef, c.c_fixed,
-                    c.part, c.want_z, c.skip, R_, S_, W_, cap_};
-        sparse_pass_kernel<<<grid_, 32 * (W_ + 1), smem_, ctx->stream>>>(a);
+                    c.part, c.want_z, c.skip};
+        sparse_pass_kernel<<<grid_, 32 * W_, smem_, ctx->stream>>>(a);
         SLQ_LAUNCH_CHECK(ctx);
     }
     std::vector<uint64_t> key() const override {
         return {2, reinterpret_cast<uint64_t>(A_->rowptr), reinterpret_cast<uint64_t>(A_->colidx),
                 reinterpret_cast<uint64_t>(A_->vals), reinterpret_cast<uint64_t>(A_->b), static_cast<uint64_t>(m),
-                static_cast<uint64_t>(n), static_cast<uint64_t>(cap_), static_cast<uint64_t>(grid_)};
+                static_cast<uint64_t>(n), static_cast<uint64_t>(W_), static_cast<uint64_t>(grid_)};
     }
     double pass_bytes() const override { return 12.0 * A_->nnz + 8.0 * (m + 1) + 16.0 * m; }
 
 private:
     const slq_sparse* A_;
-    int W_ = 8, R_ = 32, S_ = 3, grid_ = 1;
-    int64_t cap_ = 4;
+    int W_ = 8, grid_ = 1;
     size_t smem_ = 0;
 };
 
