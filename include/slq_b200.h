@@ -37,7 +37,9 @@ typedef enum {
     SLQ_NCCL = 7,
     SLQ_OOM = 8,
     SLQ_UNSUPPORTED = 9,
-    SLQ_INVALID_ARG = 10
+    SLQ_INVALID_ARG = 10,
+    SLQ_INVALID_DISTORTION = 11, /* InvalidDistortion errors.hpp:39 */
+    SLQ_DIVERGENCE = 12          /* Divergence        errors.hpp:64 */
 } slq_status;
 
 typedef enum { SLQ_TERM_TOLERANCE = 0, SLQ_TERM_MAXITER = 1, SLQ_TERM_BREAKDOWN = 2 } slq_termination;
@@ -246,6 +248,38 @@ int slq_lsqr(slq_ctx* ctx, const slq_dense* A, const double* M, const double* b,
 int slq_lsqr_sparse(slq_ctx* ctx, const slq_sparse* A, const double* M, const double* b, const double* x0,
                     const slq_solve_opts* opts, double* x_out, slq_report* report,
                     double* residual_estimate, double* iterates_error, double* residual_true);
+
+/* -------------------------------------------------- gradient family --- */
+
+typedef struct {
+    double alpha;   /* gradient.hpp:20-24 GradientParams */
+    double beta;
+    double eta_hat;
+} slq_gradient_params;
+
+/* gradient.hpp:27-34 hbm_params: alpha = (1-eta^2)^2, beta = eta^2.
+ * SLQ_INVALID_DISTORTION unless 0 <= eta_hat < 1. */
+int slq_hbm_params(double eta_hat, slq_gradient_params* out);
+/* gradient.hpp:37-48 gd_params: alpha = (1-eta^2)^2 / (1+eta^2), beta = 0. */
+int slq_gd_params(double eta_hat, slq_gradient_params* out);
+
+/* gradient.hpp:56-115 gradient_descent_hbm over a device matrix (arguments as
+ * slq_lsqr; opts->one_sync / backward_tol / on_bidiag are ignored).  Heavy
+ * ball x_t = x_{t-1} + alpha M M^T A^T r_{t-1} + beta (x_{t-1} - x_{t-2});
+ * stops when ||M^T A^T r|| <= eps times its first value.  One HBM pass over A
+ * per iteration (r_t and A^T r_t from the same sweep) and one n-vector
+ * allreduce with a communicator.  SLQ_DIVERGENCE when ||M^T A^T r|| grows by
+ * 1e6 (gradient.hpp:82-85). */
+int slq_gradient_descent_hbm(slq_ctx* ctx, const slq_dense* A, const double* M, const double* b,
+                             const double* x0, const slq_gradient_params* params,
+                             const slq_solve_opts* opts, double* x_out, slq_report* report,
+                             double* residual_estimate, double* iterates_error, double* residual_true);
+/* gradient.hpp:117-122 -- the CscMatrix overload, over a sparse operand. */
+int slq_gradient_descent_hbm_sparse(slq_ctx* ctx, const slq_sparse* A, const double* M, const double* b,
+                                    const double* x0, const slq_gradient_params* params,
+                                    const slq_solve_opts* opts, double* x_out, slq_report* report,
+                                    double* residual_estimate, double* iterates_error,
+                                    double* residual_true);
 
 /* ---------------------------------------------------- whole pipeline --- */
 

@@ -41,6 +41,8 @@ STATUS = {
     3: "DimensionMismatch",
     4: "RankDeficient",
     5: "SingularTriangular",
+    11: "InvalidDistortion",
+    12: "Divergence",
     8: "OOM",
     99: "Error",
 }
@@ -164,6 +166,13 @@ class COracle(_Base):
         L.orc_lsqr.argtypes = [_dp, _i64, _i64, _dp, _dp, _dp, ct.c_double, ct.c_long, ct.c_int,
                                _dp, ct.c_int, _dp, ct.POINTER(_OrcReport), _dp, _dp, _dp]
         L.orc_partition_rows.argtypes = [_i64, ct.c_int, _ip]
+        L.orc_hbm_params.argtypes = [ct.c_double, _dp, _dp]
+        L.orc_gd_params.argtypes = [ct.c_double, _dp, _dp]
+        L.orc_gd_hbm.argtypes = [_dp, _i64, _i64, _dp, _dp, _dp, ct.c_double, ct.c_double, ct.c_double, ct.c_long,
+                                 _dp, ct.c_int, _dp, ct.POINTER(_OrcReport), _dp, _dp, _dp]
+        L.orc_gd_hbm_csc.argtypes = [_i64, _i64, _ip, _dp, _ip, _dp, _dp, _dp, ct.c_double, ct.c_double,
+                                     ct.c_double, ct.c_long, _dp, ct.c_int, _dp, ct.POINTER(_OrcReport), _dp, _dp,
+                                     _dp]
         L.orc_gen_dense.argtypes = [_i64, _i64, ct.c_double, _u64, _dp]
         L.orc_gen_rhs.argtypes = [_dp, _i64, _i64, ct.c_double, _u64, _dp, _dp]
 
@@ -323,6 +332,37 @@ class COracle(_Base):
         return x, Report(rep.iterations, TERMINATION[rep.termination], est[: rep.n_estimate].copy(),
                          err[: rep.n_err].copy(), tru[: rep.n_true].copy())
 
+    # gradient.hpp
+    def gradient_params(self, eta, hbm=True):
+        a, b = np.zeros(1), np.zeros(1)
+        self._check((self.lib.orc_hbm_params if hbm else self.lib.orc_gd_params)(eta, _d(a), _d(b)))
+        return float(a[0]), float(b[0])
+
+    def gd_hbm(self, A, M, b, x0, alpha, beta, eps=1e-10, maxit=100, x_star=None, track_true=False):
+        A, M = _f(A), _f(M)
+        m, n = A.shape
+        x = np.zeros(n)
+        rep = _OrcReport()
+        est, err, tru = np.zeros(maxit + 1), np.zeros(maxit + 2), np.zeros(maxit + 2)
+        xs = _col(x_star) if x_star is not None else None
+        self._check(self.lib.orc_gd_hbm(_d(A), m, n, _d(M), _d(_col(b)), _d(_col(x0)), alpha, beta, eps, maxit,
+                                        _d(xs), int(track_true), _d(x), ct.byref(rep), _d(est), _d(err), _d(tru)))
+        return x, Report(rep.iterations, TERMINATION[rep.termination], est[: rep.n_estimate].copy(),
+                         err[: rep.n_err].copy(), tru[: rep.n_true].copy())
+
+    def gd_hbm_csc(self, m, n, arows, avals, acolptr, M, b, x0, alpha, beta, eps=1e-10, maxit=100, x_star=None,
+                   track_true=False):
+        M = _f(M)
+        x = np.zeros(n)
+        rep = _OrcReport()
+        est, err, tru = np.zeros(maxit + 1), np.zeros(maxit + 2), np.zeros(maxit + 2)
+        xs = _col(x_star) if x_star is not None else None
+        self._check(self.lib.orc_gd_hbm_csc(m, n, _i(arows), _d(avals), _i(acolptr), _d(M), _d(_col(b)),
+                                            _d(_col(x0)), alpha, beta, eps, maxit, _d(xs), int(track_true), _d(x),
+                                            ct.byref(rep), _d(est), _d(err), _d(tru)))
+        return x, Report(rep.iterations, TERMINATION[rep.termination], est[: rep.n_estimate].copy(),
+                         err[: rep.n_err].copy(), tru[: rep.n_true].copy())
+
     # distsim.hpp
     def partition_rows(self, m, p):
         out = np.zeros(p + 1, np.int64)
@@ -367,6 +407,10 @@ class RefOracle(_Base):
         L.ref_lsqr.argtypes = [_dp, _i64, _i64, _dp, _dp, _dp, ct.c_double, _i64, ct.c_int, _dp,
                                ct.c_int, ct.c_int, _dp, ct.POINTER(_RefReport), _dp, _dp, _dp]
         L.ref_partition_rows.argtypes = [_i64, ct.c_int, _ip]
+        L.ref_gradient_params.argtypes = [ct.c_double, ct.c_int, _dp]
+        L.ref_gradient_descent_hbm.argtypes = [ct.c_int, _dp, _i64, _i64, _ip, _dp, _ip, _dp, _dp, _dp, ct.c_double,
+                                               ct.c_double, ct.c_double, _i64, _dp, ct.c_int, ct.c_int, _dp,
+                                               ct.POINTER(_RefReport), _dp, _dp, _dp]
         L.ref_lsqr_csc.argtypes = [_i64, _i64, _ip, _dp, _ip, _dp, _dp, _dp, ct.c_double, _i64, ct.c_int, _dp,
                                    ct.c_int, ct.c_int, _dp, ct.POINTER(_RefReport), _dp, _dp, _dp]
         L.ref_dist_generate_sparse_sign.argtypes = [_i64, _i64, _i64, _u64, ct.c_int, _ip, _dp, _ip]
@@ -462,6 +506,33 @@ class RefOracle(_Base):
         out = np.zeros(p + 1, np.int64)
         self._check(self.lib.ref_partition_rows(m, p, _i(out)))
         return out
+
+    def gradient_params(self, eta, hbm=True):
+        out = np.zeros(2)
+        self._check(self.lib.ref_gradient_params(eta, int(hbm), _d(out)))
+        return float(out[0]), float(out[1])
+
+    def gd_hbm(self, A, M, b, x0, alpha, beta, eps=1e-10, maxit=100, x_star=None, track_true=False, workers=0,
+               csc=None):
+        """gradient.hpp:56-126; csc = (m, n, rows, vals, colptr) selects the CscMatrix overload."""
+        M = _f(M)
+        if csc is not None:
+            m, n, rows, vals, colptr = csc
+            Ad = None
+        else:
+            Ad = _f(A)
+            (m, n), rows, vals, colptr = Ad.shape, None, None, None
+        x = np.zeros(n)
+        rep = _RefReport()
+        est, err, tru = np.zeros(maxit + 1), np.zeros(maxit + 2), np.zeros(maxit + 2)
+        xs = _col(x_star) if x_star is not None else None
+        self._check(self.lib.ref_gradient_descent_hbm(int(csc is not None), _d(Ad), m, n, _i(rows), _d(vals),
+                                                      _i(colptr), _d(M), _d(_col(b)), _d(_col(x0)), alpha, beta,
+                                                      eps, maxit, _d(xs), int(track_true), workers, _d(x),
+                                                      ct.byref(rep), _d(est), _d(err), _d(tru)))
+        return x, Report(rep.iterations, TERMINATION[rep.termination], est[: rep.n_estimate].copy(),
+                         err[: rep.n_err].copy(), tru[: rep.n_true].copy(), rep.sync_count,
+                         rep.broadcasts, rep.init_reductions, rep.init_broadcasts, rep.wall_time)
 
     def sketch_apply_csc(self, d, zeta, seed, m, n, arows, avals, acolptr):
         Y = np.zeros((d, n), order="F")

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "sketchlsq/distsim.hpp"
+#include "sketchlsq/gradient.hpp"
 #include "sketchlsq/lsqr.hpp"
 #include "sketchlsq/preconditioner.hpp"
 #include "sketchlsq/problems.hpp"
@@ -36,6 +37,8 @@ int map_exc() {
     catch (const DimensionMismatch& e) { g_err = e.what(); return 3; }
     catch (const RankDeficient& e) { g_err = e.what(); return 4; }
     catch (const SingularTriangular& e) { g_err = e.what(); return 5; }
+    catch (const InvalidDistortion& e) { g_err = e.what(); return 11; }
+    catch (const Divergence& e) { g_err = e.what(); return 12; }
     catch (const std::exception& e) { g_err = e.what(); return 99; }
 }
 
@@ -269,6 +272,60 @@ int ref_lsqr_csc(int64_t m, int64_t n, const int64_t* rows, const double* vals, 
             DistributedVector db = distribute(bv, pool);
             auto op = dist_operator(dA);
             res = one_sync ? lsqr_one_sync(op, P, db, xv, o) : lsqr(op, P, db, xv, o);
+        }
+        std::memcpy(x_out, res.first.data(), sizeof(double) * n);
+        fill(res.second, rep, est, err, tru);
+        return 0;
+    } catch (...) { return map_exc(); }
+}
+
+// gradient.hpp:27-48 hbm_params / gd_params (out: alpha, beta)
+int ref_gradient_params(double eta, int hbm, double* out) {
+    try {
+        const GradientParams g = hbm ? hbm_params(eta) : gd_params(eta);
+        out[0] = g.alpha;
+        out[1] = g.beta;
+        return 0;
+    } catch (...) { return map_exc(); }
+}
+
+// gradient.hpp:56-126 gradient_descent_hbm, dense (csc == 0: A column-major m x n)
+// or CSC (rows / vals / colptr), serial operator or WorkerPool(workers).
+int ref_gradient_descent_hbm(int csc, const double* A, int64_t m, int64_t n, const int64_t* rows, const double* vals,
+                             const int64_t* colptr, const double* M, const double* b, const double* x0, double alpha,
+                             double beta, double eps, int64_t maxit, const double* x_star, int track_true, int workers,
+                             double* x_out, ref_report* rep, double* est, double* err, double* tru) {
+    try {
+        Preconditioner P;
+        P.M = wrap(M, n, n);
+        Vector bv(b, b + m), xv(x0, x0 + n), xs;
+        SolveOptions o;
+        o.eps = eps;
+        o.maxit = maxit;
+        if (x_star) {
+            xs.assign(x_star, x_star + n);
+            o.x_star = &xs;
+        }
+        o.track_true_residual = track_true != 0;
+        const GradientParams gp{alpha, beta, 0.0};
+        std::pair<Vector, SolveReport> res;
+        auto run = [&](const auto& Am) {
+            if (workers <= 0) return gradient_descent_hbm(Am, P, bv, xv, gp, o);
+            WorkerPool pool(workers);
+            auto dA = distribute(Am, pool);
+            DistributedVector db = distribute(bv, pool);
+            auto op = dist_operator(dA);
+            return gradient_descent_hbm(op, P, db, xv, gp, o);
+        };
+        if (csc) {
+            CscMatrix Ac(m, n);
+            const int64_t nnz = colptr[n];
+            Ac.row_indices.assign(rows, rows + nnz);
+            Ac.values.assign(vals, vals + nnz);
+            Ac.col_pointers.assign(colptr, colptr + n + 1);
+            res = run(Ac);
+        } else {
+            res = run(wrap(A, m, n));
         }
         std::memcpy(x_out, res.first.data(), sizeof(double) * n);
         fill(res.second, rep, est, err, tru);

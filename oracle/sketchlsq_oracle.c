@@ -27,6 +27,8 @@
 #define E_RANK_DEFICIENT 4
 #define E_SINGULAR_TRIANGULAR 5
 #define E_OOM 8
+#define E_INVALID_DISTORTION 11
+#define E_DIVERGENCE 12
 
 typedef int64_t idx;
 
@@ -540,6 +542,101 @@ int orc_lsqr_csc(idx m, idx n, const idx* rows, const double* vals, const idx* c
     orc_op op = {m, n, 1, NULL, rows, vals, colptr};
     return lsqr_op(&op, M, b, x0, eps, maxit, one_sync, x_star, track_true, x_out, rep, est_hist,
                    err_hist, true_hist);
+}
+
+/* ------------------------------------------------- gradient family */
+
+/* gradient.hpp:27-48 hbm_params / gd_step_size: alpha, beta from eta_hat. */
+int orc_hbm_params(double eta, double* alpha, double* beta) {
+    if (!(eta >= 0.0 && eta < 1.0)) return E_INVALID_DISTORTION;
+    const double e2 = eta * eta;
+    *alpha = (1.0 - e2) * (1.0 - e2);
+    *beta = e2;
+    return OK;
+}
+int orc_gd_params(double eta, double* alpha, double* beta) {
+    if (!(eta >= 0.0 && eta < 1.0)) return E_INVALID_DISTORTION;
+    const double e2 = eta * eta;
+    *alpha = (1.0 - e2) * (1.0 - e2) / (1.0 + e2);
+    *beta = 0.0;
+    return OK;
+}
+
+/* gradient.hpp:56-115 gradient_descent_hbm (heavy ball; beta = 0 is plain
+ * gradient descent) over the serial operator:
+ *   h = M^T A^T r_{t-1}; metric = ||h||; Divergence if metric > 1e6 metric_1;
+ *   x_t = (1+beta) x_{t-1} - beta x_{t-2} + alpha M h; r_t = b - A x_t;
+ *   stop when metric <= eps metric_1. */
+static int gd_op(const orc_op* op, const double* M, const double* b, const double* x0, double alpha,
+                 double beta, double eps, long maxit, const double* x_star, int track_true, double* x_out,
+                 orc_lsqr_report* rep, double* est_hist, double* err_hist, double* true_hist) {
+    const idx m = op->m, n = op->n;
+    memset(rep, 0, sizeof(*rep));
+    double* r = (double*)malloc(sizeof(double) * (size_t)m);
+    double* wm = (double*)malloc(sizeof(double) * (size_t)m);
+    double* xp = (double*)malloc(sizeof(double) * (size_t)n);
+    double* xn = (double*)malloc(sizeof(double) * (size_t)n);
+    double* tn = (double*)malloc(sizeof(double) * (size_t)n);
+    double* h = (double*)malloc(sizeof(double) * (size_t)n);
+    double* g = (double*)malloc(sizeof(double) * (size_t)n);
+    double* wn = (double*)malloc(sizeof(double) * (size_t)n);
+    if (!r || !wm || !xp || !xn || !tn || !h || !g || !wn) return E_OOM;
+    double* x = x_out;
+    memcpy(x, x0, sizeof(double) * (size_t)n);
+    memcpy(xp, x0, sizeof(double) * (size_t)n);
+    op_matvec(op, x, wm);
+    for (idx i = 0; i < m; ++i) r[i] = b[i] + (-1.0) * wm[i];
+    record(op, m, n, b, x, x_star, track_true, err_hist, true_hist, rep, wm, wn);
+    int status = OK;
+    double metric0 = -1.0;
+    rep->termination = TERM_MAXITER;
+    rep->iterations = maxit;
+    for (long t = 1; t <= maxit; ++t) {
+        op_rmatvec(op, r, tn);
+        orc_tri_upper_rmatvec(M, n, tn, h);
+        const double metric = norm2(h, n);
+        if (metric0 < 0.0) metric0 = metric;
+        if (metric > 1e6 * metric0) { status = E_DIVERGENCE; break; }
+        orc_tri_upper_matvec(M, n, h, g);
+        for (idx j = 0; j < n; ++j) {
+            double v = x[j];
+            v *= 1.0 + beta;          /* scal(1 + beta, x_next) */
+            v += -beta * xp[j];       /* axpy(-beta, x_prev, x_next) */
+            v += alpha * g[j];        /* axpy(alpha, g, x_next) */
+            xn[j] = v;
+        }
+        memcpy(xp, x, sizeof(double) * (size_t)n);
+        memcpy(x, xn, sizeof(double) * (size_t)n);
+        op_matvec(op, x, wm);
+        for (idx i = 0; i < m; ++i) r[i] = b[i] + (-1.0) * wm[i];
+        est_hist[rep->n_estimate++] = metric;
+        record(op, m, n, b, x, x_star, track_true, err_hist, true_hist, rep, wm, wn);
+        if (metric <= eps * metric0) {
+            rep->termination = TERM_TOLERANCE;
+            rep->iterations = t;
+            break;
+        }
+    }
+    free(r); free(wm); free(xp); free(xn); free(tn); free(h); free(g); free(wn);
+    return status;
+}
+
+int orc_gd_hbm(const double* A, idx m, idx n, const double* M, const double* b, const double* x0, double alpha,
+               double beta, double eps, long maxit, const double* x_star, int track_true, double* x_out,
+               orc_lsqr_report* rep, double* est_hist, double* err_hist, double* true_hist) {
+    orc_op op = {m, n, 0, A, NULL, NULL, NULL};
+    return gd_op(&op, M, b, x0, alpha, beta, eps, maxit, x_star, track_true, x_out, rep, est_hist, err_hist,
+                 true_hist);
+}
+
+/* gradient.hpp:117-122 -- CscMatrix overload */
+int orc_gd_hbm_csc(idx m, idx n, const idx* rows, const double* vals, const idx* colptr, const double* M,
+                   const double* b, const double* x0, double alpha, double beta, double eps, long maxit,
+                   const double* x_star, int track_true, double* x_out, orc_lsqr_report* rep,
+                   double* est_hist, double* err_hist, double* true_hist) {
+    orc_op op = {m, n, 1, NULL, rows, vals, colptr};
+    return gd_op(&op, M, b, x0, alpha, beta, eps, maxit, x_star, track_true, x_out, rep, est_hist, err_hist,
+                 true_hist);
 }
 
 /* ----------------------------------------------------- partitioning */

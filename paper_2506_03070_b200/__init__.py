@@ -12,9 +12,12 @@ from .api import (  # noqa: F401
     CudaError,
     DeviceMatrix,
     DimensionMismatch,
+    Divergence,
     Error,
+    GradientParams,
     InvalidArgument,
     InvalidDims,
+    InvalidDistortion,
     InvalidSparsity,
     NcclError,
     OutOfMemory,
@@ -36,7 +39,11 @@ from .api import (  # noqa: F401
     apply_Mt,
     build_preconditioner,
     default_context,
+    gd_params,
+    gd_step_size,
     generate_sparse_sign,
+    gradient_descent_hbm,
+    hbm_params,
     householder_qr,
     initial_guess,
     lsqr,

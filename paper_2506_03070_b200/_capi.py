@@ -65,6 +65,10 @@ class Report(ct.Structure):
     ]
 
 
+class GradientParams(ct.Structure):
+    _fields_ = [("alpha", ct.c_double), ("beta", ct.c_double), ("eta_hat", ct.c_double)]
+
+
 class PhaseTimes(ct.Structure):
     _fields_ = [
         ("generate", ct.c_double),
@@ -125,6 +129,12 @@ _SIGS = {
     "slq_lsqr_sparse": (ct.c_int, [vp, vp, dp, dp, dp, ct.POINTER(SolveOpts), dp, ct.POINTER(Report), dp, dp, dp]),
     "slq_solve_sparse": (ct.c_int, [vp, vp, i64, i64, u64, ct.POINTER(SolveOpts), dp, ct.POINTER(Report),
                                     ct.POINTER(PhaseTimes), dp]),
+    "slq_hbm_params": (ct.c_int, [ct.c_double, ct.POINTER(GradientParams)]),
+    "slq_gd_params": (ct.c_int, [ct.c_double, ct.POINTER(GradientParams)]),
+    "slq_gradient_descent_hbm": (ct.c_int, [vp, vp, dp, dp, dp, ct.POINTER(GradientParams), ct.POINTER(SolveOpts), dp,
+                                            ct.POINTER(Report), dp, dp, dp]),
+    "slq_gradient_descent_hbm_sparse": (ct.c_int, [vp, vp, dp, dp, dp, ct.POINTER(GradientParams),
+                                                   ct.POINTER(SolveOpts), dp, ct.POINTER(Report), dp, dp, dp]),
     "slq_time_kernels": (ct.c_int, [vp, vp, i64, i64, u64, ct.c_int, dp]),
     "slq_solve_host": (ct.c_int, [vp, dp, i64, i64, i64, dp, i64, i64, i64, u64, ct.POINTER(SolveOpts), dp,
                                   ct.POINTER(Report), ct.POINTER(PhaseTimes), dp]),

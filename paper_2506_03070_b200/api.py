@@ -45,6 +45,14 @@ class InvalidDims(Error):
     """errors.hpp:46"""
 
 
+class InvalidDistortion(Error):
+    """errors.hpp:39"""
+
+
+class Divergence(Error):
+    """errors.hpp:64"""
+
+
 class CudaError(Error):
     pass
 
@@ -76,6 +84,8 @@ _STATUS = {
     8: OutOfMemory,
     9: Unsupported,
     10: InvalidArgument,
+    11: InvalidDistortion,
+    12: Divergence,
 }
 
 
@@ -726,6 +736,77 @@ def lsqr(A, P, b, x0, opts: SolveOptions | None = None, ctx=None):
 def lsqr_one_sync(A, P, b, x0, opts: SolveOptions | None = None, ctx=None):
     """lsqr.hpp:185-189 / :203-212 -- one reduction per iteration."""
     return _lsqr(A, P, b, x0, opts, True, ctx)
+
+
+# --------------------------------------------------------- gradient family
+
+
+@dataclass
+class GradientParams:
+    """gradient.hpp:20-24"""
+
+    alpha: float = 1.0
+    beta: float = 0.0
+    eta_hat: float = 0.0
+
+
+def hbm_params(eta_hat: float) -> GradientParams:
+    """gradient.hpp:27-34: alpha = (1 - eta^2)^2, beta = eta^2 (rate sqrt(beta))."""
+    g = C.GradientParams()
+    _check(C.lib.slq_hbm_params(float(eta_hat), ct.byref(g)))
+    return GradientParams(g.alpha, g.beta, g.eta_hat)
+
+
+def gd_params(eta_hat: float) -> GradientParams:
+    """gradient.hpp:46-48: plain gradient descent, alpha = gd_step_size(eta_hat), beta = 0."""
+    g = C.GradientParams()
+    _check(C.lib.slq_gd_params(float(eta_hat), ct.byref(g)))
+    return GradientParams(g.alpha, g.beta, g.eta_hat)
+
+
+def gd_step_size(eta_hat: float) -> float:
+    """gradient.hpp:37-44"""
+    return gd_params(eta_hat).alpha
+
+
+def gradient_descent_hbm(A, P, b, x0, params: GradientParams, opts: SolveOptions | None = None, ctx=None):
+    """gradient.hpp:56-126 -- heavy-ball (beta > 0) / gradient descent (beta = 0)
+    on the preconditioned problem; one HBM pass over A per iteration.  Raises
+    Divergence when ||M^T A^T r|| grows by 1e6 over its first value."""
+    ctx = _ctx(ctx)
+    sparse = isinstance(A, (CscMatrix, SparseDeviceMatrix))
+    if isinstance(A, CscMatrix):
+        bb = _vec(b)
+        if bb.size != A.rows:
+            raise DimensionMismatch("rmatvec(csc): length mismatch")
+        dm, bb = SparseDeviceMatrix.from_csc(A, bb, ctx=ctx), None
+    elif isinstance(A, (DeviceMatrix, SparseDeviceMatrix)):
+        dm = A
+        bb = _vec(b) if b is not None else None
+    else:
+        A = _f64(A)
+        bb = _vec(b)
+        if bb.size != A.shape[0]:
+            raise DimensionMismatch("rmatvec: length mismatch")
+        dm, bb = DeviceMatrix.from_numpy(A, bb, ctx=ctx), None
+    n = dm.n
+    M = _f64(P.M if isinstance(P, Preconditioner) else P)
+    if M.shape != (n, n):
+        raise DimensionMismatch("tri_upper_matvec")
+    x0 = _vec(x0)
+    if x0.size != n:
+        raise DimensionMismatch("matvec: x has wrong length")
+    co, keep = _opts(opts, False, n)
+    maxit = max(int(co.maxit), 0)
+    est, err, tru = np.zeros(maxit + 2), np.zeros(maxit + 2), np.zeros(maxit + 2)
+    x = np.zeros(n)
+    rep = C.Report()
+    gp = C.GradientParams(float(params.alpha), float(params.beta), float(params.eta_hat))
+    fn = C.lib.slq_gradient_descent_hbm_sparse if sparse else C.lib.slq_gradient_descent_hbm
+    _check(fn(ctx.handle, dm.handle, _d(M), _d(bb), _d(x0), ct.byref(gp), ct.byref(co), _d(x), ct.byref(rep),
+              _d(est), _d(err), _d(tru)))
+    del keep
+    return x, _report(rep, est, err, tru)
 
 
 # ------------------------------------------------------------ distributed

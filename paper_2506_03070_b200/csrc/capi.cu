@@ -338,6 +338,40 @@ int run_solve(slq_ctx* ctx, const Operand& A, int64_t d, int64_t zeta, uint64_t 
 
 }  // namespace
 
+namespace {
+
+// shared body of the dense / sparse gradient_descent_hbm entry points
+template <class MakeOp>
+void gd_common(slq_ctx* ctx, int64_t m, int64_t n, const double* M, const double* b, const double* x0,
+               const slq_gradient_params* params, const slq_solve_opts* opts_in, double* x_out, slq_report* report,
+               double* residual_estimate, double* iterates_error, double* residual_true, int64_t b_pad,
+               MakeOp make_op) {
+    slq_solve_opts opts;
+    if (opts_in) opts = *opts_in;
+    else slq_solve_opts_default(&opts);
+    PrecondBufs P = precond_bufs(ctx, n);
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(P.M, M, sizeof(double) * n * n, cudaMemcpyHostToDevice, ctx->stream));
+    transpose_square(ctx, P.M, n, P.Mt);
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(P.x0, x0, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    slq::DevBuf db, dx;
+    double* bd = nullptr;
+    if (b) {
+        bd = static_cast<double*>(db.ensure(sizeof(double) * (m + b_pad)));
+        if (b_pad) SLQ_CUDA_CHECK(cudaMemsetAsync(bd, 0, sizeof(double) * (m + b_pad), ctx->stream));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(bd, b, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    double* x = static_cast<double*>(dx.ensure(sizeof(double) * (n + 8)));
+    slq::LsqrOut lo;
+    const auto h0 = std::chrono::steady_clock::now();
+    slq::gd_dev(ctx, *make_op(), bd, P.M, P.Mt, P.x0, params->alpha, params->beta, x, opts, residual_estimate,
+                iterates_error, residual_true, lo);
+    SLQ_CUDA_CHECK(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    lo.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
+    fill_report(report, lo);
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* slq_last_error(void) { return g_last_error.c_str(); }
@@ -968,6 +1002,48 @@ int slq_lsqr_sparse(slq_ctx* ctx, const slq_sparse* A, const double* M, const do
         SLQ_CUDA_CHECK(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
         lo.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
         fill_report(report, lo);
+    });
+}
+
+int slq_hbm_params(double eta, slq_gradient_params* out) {
+    return guarded([&] {
+        need(out != nullptr, SLQ_INVALID_ARG, "hbm_params: null output");
+        need(eta >= 0.0 && eta < 1.0, SLQ_INVALID_DISTORTION, "hbm_params: need 0 <= eta_hat < 1");
+        const double e2 = eta * eta;
+        *out = slq_gradient_params{(1.0 - e2) * (1.0 - e2), e2, eta};
+    });
+}
+
+int slq_gd_params(double eta, slq_gradient_params* out) {
+    return guarded([&] {
+        need(out != nullptr, SLQ_INVALID_ARG, "gd_params: null output");
+        need(eta >= 0.0 && eta < 1.0, SLQ_INVALID_DISTORTION, "gd_step_size: need 0 <= eta_hat < 1");
+        const double e2 = eta * eta;
+        *out = slq_gradient_params{(1.0 - e2) * (1.0 - e2) / (1.0 + e2), 0.0, eta};
+    });
+}
+
+int slq_gradient_descent_hbm(slq_ctx* ctx, const slq_dense* A, const double* M, const double* b, const double* x0,
+                             const slq_gradient_params* params, const slq_solve_opts* opts, double* x_out,
+                             slq_report* report, double* residual_estimate, double* iterates_error,
+                             double* residual_true) {
+    return guarded([&] {
+        need(ctx && A && M && x0 && x_out && params, SLQ_INVALID_ARG, "gradient_descent_hbm: null argument");
+        need(b != nullptr || A->has_b, SLQ_INVALID_ARG, "gradient_descent_hbm: no right-hand side");
+        gd_common(ctx, A->m, A->n, M, b, x0, params, opts, x_out, report, residual_estimate, iterates_error,
+                  residual_true, 0, [&] { return slq::make_dense_op(ctx, A); });
+    });
+}
+
+int slq_gradient_descent_hbm_sparse(slq_ctx* ctx, const slq_sparse* A, const double* M, const double* b,
+                                    const double* x0, const slq_gradient_params* params, const slq_solve_opts* opts,
+                                    double* x_out, slq_report* report, double* residual_estimate,
+                                    double* iterates_error, double* residual_true) {
+    return guarded([&] {
+        need(ctx && A && M && x0 && x_out && params, SLQ_INVALID_ARG, "gradient_descent_hbm_sparse: null argument");
+        need(b != nullptr || A->b != nullptr, SLQ_INVALID_ARG, "gradient_descent_hbm_sparse: no right-hand side");
+        gd_common(ctx, A->m, A->n, M, b, x0, params, opts, x_out, report, residual_estimate, iterates_error,
+                  residual_true, slq::kSparseRowPad, [&] { return slq::make_sparse_op(ctx, A); });
     });
 }
 

@@ -844,6 +844,260 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
         for (size_t i = 0; i < htrue.size(); ++i) true_hist[i] = htrue[i];
 }
 
+// ------------------------------------------------ gradient family (K6)
+//
+// gradient.hpp:56-115 gradient_descent_hbm.  One fused pass per iteration:
+// the reference's r_t = b - A x_t (matvec) and the next iteration's A^T r_t
+// (rmatvec) come from the same sweep over A (u_hat = A x - b, z = A^T u_hat),
+// so an iteration reads A once instead of twice.  Per iteration:
+//   pass(x) -> z = -A^T r          (K4, + one n-vector allreduce on NCCL)
+//   gd_h:  h = M^T A^T r, ||h||^2 partials; t <- t+1
+//   gd_x:  metric = ||h|| (fixed-order sum), Divergence check, g = M h,
+//          x_t = (1+beta) x_{t-1} - beta x_{t-2} + alpha g  (the reference's
+//          scal/axpy sequence, unfused roundings), tolerance check.
+// Device state carries the stop decision, so batches of iterations are
+// enqueued without host round trips.
+
+namespace {
+
+struct GdState {
+    int64_t t;        // iterations completed
+    int64_t iters;
+    int done, term, diverged, active;
+    double metric0;
+    double eps;
+    int64_t maxit;
+};
+
+__global__ void __launch_bounds__(256) gd_h_kernel(const double* M, int64_t n, const double* z, double* h,
+                                                   double* part, GdState* st) {
+    __shared__ double red[8];
+    if (st->done) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->active = 0;
+        return;
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * 8 + w;
+    double hi = 0.0;
+    if (i < n) {
+        // h_i = sum_{j <= i} M(j, i) (-z_j): column i of column-major M
+        const double* col = M + i * n;
+        double acc = 0.0;
+        for (int64_t j = lane; j <= i; j += 32) acc = fma(col[j], -z[j], acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        hi = acc;
+        if (lane == 0) h[i] = hi;
+    }
+    if (lane == 0) red[w] = (i < n) ? hi * hi : 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int q = 0; q < 8; ++q) s += red[q];
+        part[blockIdx.x] = s;
+        if (blockIdx.x == 0) {
+            st->active = 1;
+            st->t += 1;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) gd_x_kernel(const double* Mt, int64_t n, const double* h, const double* part,
+                                                   int np, double alpha, double beta, double* x, double* xp,
+                                                   double* hist, GdState* st) {
+    __shared__ double s_metric;
+    if (!st->active) return;
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int q = 0; q < np; ++q) s += part[q];
+        s_metric = sqrt(s);
+    }
+    __syncthreads();
+    const double metric = s_metric;
+    const int64_t t = st->t;
+    const double metric0 = (t == 1) ? metric : st->metric0;
+    const bool diverged = metric > 1e6 * metric0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * 8 + w;
+    if (!diverged && i < n) {
+        // g_i = sum_{j >= i} M(i, j) h_j: row i of M (row-major copy)
+        const double* row = Mt + i * n;
+        double acc = 0.0;
+        for (int64_t j = i + lane; j < n; j += 32) acc = fma(row[j], h[j], acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            double v = __dmul_rn(x[i], 1.0 + beta);     // scal(1 + beta, x_next)
+            v = __dadd_rn(v, __dmul_rn(-beta, xp[i]));  // axpy(-beta, x_prev, x_next)
+            v = __dadd_rn(v, __dmul_rn(alpha, acc));    // axpy(alpha, g, x_next)
+            xp[i] = x[i];
+            x[i] = v;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (t == 1) st->metric0 = metric;
+        if (diverged) {
+            st->diverged = 1;
+            st->done = 1;
+            st->iters = t - 1;
+            return;
+        }
+        hist[t - 1] = metric;
+        if (metric <= st->eps * metric0) {
+            st->done = 1;
+            st->term = SLQ_TERM_TOLERANCE;
+            st->iters = t;
+        } else if (t >= st->maxit) {
+            st->done = 1;
+            st->term = SLQ_TERM_MAXITER;
+            st->iters = t;
+        }
+    }
+}
+
+__global__ void copy_vec_kernel(const double* src, double* a, double* b, int64_t n) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = b[i] = src[i];
+}
+
+}  // namespace
+
+void gd_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* M, const double* Mt,
+            const double* x0, double alpha, double beta, double* x, const slq_solve_opts& opts, double* est_hist,
+            double* err_hist, double* true_hist, LsqrOut& out) {
+    const int64_t m = op.m, n = op.n;
+    (void)m;
+    const int64_t maxit = std::max<int64_t>(0, opts.maxit);
+    Workspace& ws = ctx->ws;
+    const int grid = op.grid();
+    const int vgrid = static_cast<int>(std::max<int64_t>(1, ceil_div(n, 8)));
+    const size_t nvec = static_cast<size_t>(n + 8);
+    double* vecs = static_cast<double*>(ws.lsqr_vec.ensure(sizeof(double) * (nvec * 4 + vgrid + maxit + 16)));
+    double* xp = vecs;
+    double* h = vecs + nvec;
+    double* zt = vecs + 2 * nvec;  // n + 1
+    double* tmp = vecs + 3 * nvec;
+    double* vpart = vecs + 4 * nvec;
+    double* hist = vpart + vgrid;
+    double* scal = hist + maxit + 8;
+    double* part = static_cast<double*>(ws.lsqr_part.ensure(sizeof(double) * grid * (n + 1)));
+    GdState* st = static_cast<GdState*>(ws.lsqr_state.ensure(std::max(sizeof(GdState), size_t(256))));
+    GdState hs0{};
+    hs0.eps = opts.eps;
+    hs0.maxit = maxit;
+    hs0.term = SLQ_TERM_MAXITER;
+    hs0.done = maxit == 0;
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(st, &hs0, sizeof(hs0), cudaMemcpyHostToDevice, ctx->stream));
+    copy_vec_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, ctx->stream>>>(x0, x, xp, n);
+    SLQ_LAUNCH_CHECK(ctx);
+
+    cudaEvent_t e0, e1;
+    SLQ_CUDA_CHECK(cudaEventCreate(&e0));
+    SLQ_CUDA_CHECK(cudaEventCreate(&e1));
+    SLQ_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+
+    const bool instrument = opts.x_star || opts.track_true_residual;
+    std::vector<double> herr, htrue;
+    DevBuf xsbuf;
+    double* d_xstar = nullptr;
+    if (opts.x_star) {
+        d_xstar = static_cast<double*>(xsbuf.ensure(sizeof(double) * n));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(d_xstar, opts.x_star, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    auto norm_pass = [&](const double* q, double c) {  // ||A q + c b|| (instrumentation, lsqr.hpp:26-37)
+        op.pass(ctx, PassCall{q, b_dev, nullptr, nullptr, c, part, 0, nullptr});
+        sum_strided_kernel<<<1, 32, 0, ctx->stream>>>(part + n, grid, n + 1, scal);
+        SLQ_LAUNCH_CHECK(ctx);
+        allreduce_sum(ctx, scal, 1);
+        sqrt_to_kernel<<<1, 32, 0, ctx->stream>>>(scal, scal + 1);
+        SLQ_LAUNCH_CHECK(ctx);
+        double v;
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(&v, scal + 1, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        return v;
+    };
+    auto record = [&]() {
+        if (opts.x_star) {
+            sub_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, ctx->stream>>>(d_xstar, x, tmp, n);
+            SLQ_LAUNCH_CHECK(ctx);
+            herr.push_back(norm_pass(tmp, 0.0));
+        }
+        if (opts.track_true_residual) htrue.push_back(norm_pass(x, -1.0));
+    };
+    if (instrument) record();
+
+    int64_t allreduces = 0;
+    auto enqueue_iteration = [&]() {
+        op.pass(ctx, PassCall{x, b_dev, nullptr, nullptr, -1.0, part, 1, &st->done});
+        reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 32)), 256, 0, ctx->stream>>>(part, grid, n + 1,
+                                                                                                zt, &st->done);
+        SLQ_LAUNCH_CHECK(ctx);
+        allreduce_sum(ctx, zt, n + 1);
+        if (ctx->comm) ++allreduces;
+        gd_h_kernel<<<vgrid, 256, 0, ctx->stream>>>(M, n, zt, h, vpart, st);
+        SLQ_LAUNCH_CHECK(ctx);
+        gd_x_kernel<<<vgrid, 256, 0, ctx->stream>>>(Mt, n, h, vpart, vgrid, alpha, beta, x, xp, hist, st);
+        SLQ_LAUNCH_CHECK(ctx);
+    };
+    GdState hs{};
+    if (instrument) {
+        for (int64_t t = 1; t <= maxit; ++t) {
+            enqueue_iteration();
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+            SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            if (hs.diverged) break;
+            record();
+            if (hs.done) break;
+        }
+    } else {
+        // batches of 8 iterations; the host checks the device stop flag of
+        // the previous batch while the current one runs
+        constexpr int kBatch = 8;
+        if (!ctx->lsqr_hdone) {
+            SLQ_CUDA_CHECK(cudaMallocHost(&ctx->lsqr_hdone, 2 * sizeof(int)));
+            for (int i = 0; i < 2; ++i) SLQ_CUDA_CHECK(cudaEventCreate(&ctx->lsqr_ev[i]));
+        }
+        int* hdone = ctx->lsqr_hdone;
+        hdone[0] = hdone[1] = 0;
+        int64_t launched = 0, k = 0;
+        while (launched < maxit) {
+            for (int b = 0; b < kBatch; ++b) enqueue_iteration();
+            launched += kBatch;
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(&hdone[k & 1], &st->done, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+            SLQ_CUDA_CHECK(cudaEventRecord(ctx->lsqr_ev[k & 1], ctx->stream));
+            if (k > 0) {
+                SLQ_CUDA_CHECK(cudaEventSynchronize(ctx->lsqr_ev[(k - 1) & 1]));
+                if (hdone[(k - 1) & 1]) break;
+            }
+            ++k;
+        }
+    }
+    SLQ_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    float ms = 0.f;
+    SLQ_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (hs.diverged)
+        fail(SLQ_DIVERGENCE, "gradient_descent_hbm: ||M^T A^T r|| grew by 1e6; eta_hat likely underestimates the "
+                             "true distortion");
+    out.iterations = hs.done ? hs.iters : maxit;
+    out.termination = hs.done ? hs.term : SLQ_TERM_MAXITER;
+    out.n_estimate = out.iterations;
+    if (est_hist && out.n_estimate > 0)
+        SLQ_CUDA_CHECK(cudaMemcpy(est_hist, hist, sizeof(double) * out.n_estimate, cudaMemcpyDeviceToHost));
+    out.allreduces = ctx->comm ? (instrument ? allreduces : out.iterations) : 0;
+    out.init_allreduces = 0;
+    out.seconds = ms * 1e-3;
+    out.n_err = static_cast<int64_t>(herr.size());
+    out.n_true = static_cast<int64_t>(htrue.size());
+    if (err_hist)
+        for (size_t i = 0; i < herr.size(); ++i) err_hist[i] = herr[i];
+    if (true_hist)
+        for (size_t i = 0; i < htrue.size(); ++i) true_hist[i] = htrue[i];
+}
+
 double time_fused_pass(slq_ctx* ctx, const PassOp& op, int reps) {
     // Average device time of one K4 launch (steady-state iteration form),
     // CUDA events on the launching stream.

@@ -53,6 +53,12 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
               const double* x0, double* x, const slq_solve_opts& opts, double* est_hist,
               double* err_hist, double* true_hist, LsqrOut& out);
 
+// gradient.hpp:56-115 gradient_descent_hbm (alpha, beta from hbm_params /
+// gd_params); one fused pass per iteration.  Throws SLQ_DIVERGENCE.
+void gd_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* M, const double* Mt,
+            const double* x0, double alpha, double beta, double* x, const slq_solve_opts& opts, double* est_hist,
+            double* err_hist, double* true_hist, LsqrOut& out);
+
 // Average seconds per fused-pass launch (K4), timed with CUDA events.
 double time_fused_pass(slq_ctx* ctx, const PassOp& op, int reps);
 

@@ -36,4 +36,5 @@ def golden():
         "rng": dict(np.load(os.path.join(g, "rng.npz"))),
         "sketch": dict(np.load(os.path.join(g, "sketch.npz"))),
         "pipeline": dict(np.load(os.path.join(g, "pipeline.npz"))),
+        "gradient": dict(np.load(os.path.join(g, "gradient.npz"))),
     }

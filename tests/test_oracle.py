@@ -131,3 +131,48 @@ def test_restatement_matches_reference_random(seed):
     Y1, S1 = C.sketch_apply(40, 4, s, A, b)
     Y2, S2 = R.sketch_apply(40, 4, s, A, b)
     assert np.array_equal(Y1, Y2) and np.array_equal(S1, S2)
+
+
+def test_gradient_golden(golden):
+    """gradient.hpp:27-126 (hbm_params / gd_params / gradient_descent_hbm)
+    restated in C, bit-identical to the compiled reference's fixtures."""
+    p, g = golden["pipeline"], golden["gradient"]
+    meta = golden["meta"]["gradient"]
+    assert C.gradient_params(meta["eta"], True) == tuple(meta["hbm"])
+    assert C.gradient_params(meta["eta"], False) == tuple(meta["gd"])
+    a, b = meta["hbm"]
+    x, rep = C.gd_hbm(p["A"], p["M"], p["b"], p["x0"], a, b, eps=0.0, maxit=meta["maxit"], x_star=p["x_star"],
+                      track_true=True)
+    assert np.array_equal(x, g["x_hbm"]) and rep.iterations == meta["maxit"]
+    assert np.array_equal(rep.residual_estimate, g["est_hbm"])
+    assert np.array_equal(rep.iterates_error, g["err_hbm"])
+    assert np.array_equal(rep.residual_true, g["true_hbm"])
+    a, b = meta["gd"]
+    x, rep = C.gd_hbm(p["A"], p["M"], p["b"], p["x0"], a, b, eps=0.0, maxit=meta["maxit"])
+    assert np.array_equal(x, g["x_gd"]) and np.array_equal(rep.residual_estimate, g["est_gd"])
+    a, b = meta["hbm"]
+    x, rep = C.gd_hbm(p["A"], p["M"], p["b"], p["x0"], a, b, eps=meta["tol_run"]["eps"], maxit=200)
+    assert np.array_equal(x, g["x_ht"])
+    assert rep.iterations == meta["tol_run"]["iterations"] and rep.termination == meta["tol_run"]["termination"]
+
+
+def test_gradient_edge_cases():
+    # hbm_params / gd_step_size domain (test_solvers.cpp:187-206)
+    assert C.gradient_params(0.5, True) == (0.5625, 0.25)
+    assert C.gradient_params(0.0, False) == (1.0, 0.0)
+    assert abs(C.gradient_params(0.5, False)[0] - 0.45) <= 1e-15
+    for eta, hbm in ((1.0, True), (1.5, False), (-0.1, True)):
+        with pytest.raises(oracle.OracleError) as e:
+            C.gradient_params(eta, hbm)
+        assert e.value.kind == "InvalidDistortion"
+    # perfectly preconditioned gradient step solves in one iteration (test_solvers.cpp:208-222)
+    rng = np.random.default_rng(19)
+    Qa, _ = np.linalg.qr(rng.standard_normal((50, 8)))
+    xs = rng.standard_normal(8)
+    x, rep = C.gd_hbm(Qa, np.eye(8), Qa @ xs, np.zeros(8), 1.0, 0.0, maxit=3, x_star=xs)
+    assert rep.iterates_error[1] <= 1e-12 * rep.iterates_error[0]
+    # a step size far too large diverges (Divergence, gradient.hpp:82-85)
+    A = rng.standard_normal((40, 5))
+    with pytest.raises(oracle.OracleError) as e:
+        C.gd_hbm(A, np.eye(5), rng.standard_normal(40), np.zeros(5), 10.0, 0.0, eps=0.0, maxit=200)
+    assert e.value.kind == "Divergence"

@@ -100,13 +100,29 @@ def main() -> None:
                 "seed_S": 93, "rho": 0.5, "maxit": 12,
                 "tol_run": {"iterations": rep_tol.iterations, "termination": rep_tol.termination}}
 
+    # Gradient family on the same problem (gradient.hpp:27-126): heavy ball
+    # with hbm_params(eta) and plain descent with gd_params(eta), eta = sqrt(n/d)
+    eta = float(np.sqrt(n / d))
+    a_h, b_h = R.gradient_params(eta, True)
+    a_g, b_g = R.gradient_params(eta, False)
+    x_hbm, rep_hbm = R.gd_hbm(A, M, b, x0, a_h, b_h, eps=0.0, maxit=15, x_star=xs, track_true=True)
+    x_gd, rep_gd = R.gd_hbm(A, M, b, x0, a_g, b_g, eps=0.0, maxit=15)
+    x_ht, rep_ht = R.gd_hbm(A, M, b, x0, a_h, b_h, eps=1e-8, maxit=200)
+    np.savez_compressed(
+        os.path.join(OUT, "gradient.npz"), x_hbm=x_hbm, est_hbm=rep_hbm.residual_estimate,
+        err_hbm=rep_hbm.iterates_error, true_hbm=rep_hbm.residual_true, x_gd=x_gd, est_gd=rep_gd.residual_estimate,
+        x_ht=x_ht, est_ht=rep_ht.residual_estimate,
+    )
+    gradient = {"eta": eta, "hbm": [a_h, b_h], "gd": [a_g, b_g], "maxit": 15,
+                "tol_run": {"eps": 1e-8, "iterations": rep_ht.iterations, "termination": rep_ht.termination}}
+
     # Distributed (distsim.hpp) partition + bit-identity across p
     parts = {str(p): R.partition_rows(333, p).tolist() for p in (1, 2, 4, 8)}
     parts.update({"4000000/8": R.partition_rows(4_000_000, 8).tolist(),
                   "1048576/3": R.partition_rows(1 << 20, 3).tolist()})
 
     meta.update({"sketch_cases": cases, "stats_cases": stats, "pipeline": pipeline,
-                 "partition_rows": parts})
+                 "gradient": gradient, "partition_rows": parts})
     with open(os.path.join(OUT, "golden.json"), "w") as f:
         json.dump(meta, f, indent=1)
     print("wrote", sorted(os.listdir(OUT)))
