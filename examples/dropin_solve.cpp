@@ -48,5 +48,22 @@ int main() {
     } catch (const InvalidSparsity& e) {
         std::printf("InvalidSparsity ok\n");
     }
-    return eta < 1e-10 ? 0 : 1;
+    // the gradient family (gradient.hpp) on the same preconditioner
+    SolveOptions gopts;
+    gopts.eps = 1e-10;
+    gopts.maxit = 400;
+    auto [xh, rh] = gradient_descent_hbm(A, P, b, x0, hbm_params(std::sqrt(double(n) / double(d))), gopts);
+    double dx = 0, xn = 0;
+    for (index_t j = 0; j < n; ++j) {
+        dx += (xh[j] - x[j]) * (xh[j] - x[j]);
+        xn += x[j] * x[j];
+    }
+    std::printf("hbm iterations=%ld termination=%s |x_hbm - x_lsqr|/|x|=%.3e\n", rh.iterations,
+                to_string(rh.termination).c_str(), std::sqrt(dx / xn));
+    try {
+        hbm_params(1.0);
+    } catch (const InvalidDistortion& e) {
+        std::printf("InvalidDistortion ok\n");
+    }
+    return (eta < 1e-10 && std::sqrt(dx / xn) < 1e-8) ? 0 : 1;
 }

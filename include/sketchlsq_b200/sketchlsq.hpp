@@ -12,7 +12,7 @@
 // exception types) run on the B200.  Types mirror dense_matrix.hpp:18-50,
 // csc_matrix.hpp:19-60, sketch.hpp:20-68, qr.hpp:15-18,
 // preconditioner.hpp:15-30, lsqr.hpp:14-22, solve_report.hpp:11-49,
-// distsim.hpp:21-42.  Define SKETCHLSQ_B200_NAMESPACE to place the mirror in
+// gradient.hpp:20-126, distsim.hpp:21-42.  Define SKETCHLSQ_B200_NAMESPACE to place the mirror in
 // another namespace (default: sketchlsq, i.e. a true drop-in).
 #pragma once
 
@@ -44,6 +44,8 @@ struct SingularTriangular : Error { using Error::Error; };
 struct DimensionMismatch : Error { using Error::Error; };
 struct InvalidSparsity : Error { using Error::Error; };
 struct InvalidDims : Error { using Error::Error; };
+struct InvalidDistortion : Error { using Error::Error; };
+struct Divergence : Error { using Error::Error; };
 struct DeviceError : Error { using Error::Error; };
 
 namespace b200 {
@@ -57,6 +59,8 @@ inline void check(int st) {
         case SLQ_DIMENSION_MISMATCH: throw DimensionMismatch(msg);
         case SLQ_RANK_DEFICIENT: throw RankDeficient(msg);
         case SLQ_SINGULAR_TRIANGULAR: throw SingularTriangular(msg);
+        case SLQ_INVALID_DISTORTION: throw InvalidDistortion(msg);
+        case SLQ_DIVERGENCE: throw Divergence(msg);
         default: throw DeviceError(msg);
     }
 }
@@ -363,6 +367,60 @@ inline std::pair<Vector, SolveReport> lsqr(const DenseMatrix& A, const Precondit
 inline std::pair<Vector, SolveReport> lsqr_one_sync(const DenseMatrix& A, const Preconditioner& P, const Vector& b,
                                                     const Vector& x0, const SolveOptions& opts = {}) {
     return detail::lsqr_device(A, P, b, x0, opts, true);
+}
+
+// gradient.hpp:20-48
+struct GradientParams {
+    double alpha = 1.0;
+    double beta = 0.0;
+    double eta_hat = 0.0;
+};
+inline GradientParams hbm_params(double eta_hat) {
+    slq_gradient_params g;
+    b200::check(slq_hbm_params(eta_hat, &g));
+    return GradientParams{g.alpha, g.beta, g.eta_hat};
+}
+inline GradientParams gd_params(double eta_hat) {
+    slq_gradient_params g;
+    b200::check(slq_gd_params(eta_hat, &g));
+    return GradientParams{g.alpha, g.beta, g.eta_hat};
+}
+inline double gd_step_size(double eta_hat) { return gd_params(eta_hat).alpha; }
+
+// gradient.hpp:56-126 (DenseMatrix overload): one device pass over A per iteration
+inline std::pair<Vector, SolveReport> gradient_descent_hbm(const DenseMatrix& A, const Preconditioner& P,
+                                                           const Vector& b, const Vector& x0,
+                                                           const GradientParams& params,
+                                                           const SolveOptions& o = {}) {
+    const index_t m = A.rows(), n = A.cols();
+    if (static_cast<index_t>(b.size()) != m) throw DimensionMismatch("rmatvec: length mismatch");
+    if (static_cast<index_t>(x0.size()) != n) throw DimensionMismatch("matvec: length mismatch");
+    if (P.M.rows() != n) throw DimensionMismatch("tri_upper_matvec");
+    slq_dense* dA = nullptr;
+    b200::check(slq_dense_upload(b200::ctx(), A.data().data(), m, n, m > 0 ? m : 1, b.data(), 0, &dA));
+    slq_solve_opts so;
+    slq_solve_opts_default(&so);
+    so.eps = o.eps;
+    so.maxit = o.maxit;
+    so.x_star = o.x_star ? o.x_star->data() : nullptr;
+    so.track_true_residual = o.track_true_residual ? 1 : 0;
+    const slq_gradient_params gp{params.alpha, params.beta, params.eta_hat};
+    const std::size_t cap = static_cast<std::size_t>(o.maxit > 0 ? o.maxit : 0) + 2;
+    Vector x(static_cast<std::size_t>(n)), est(cap), err(cap), tru(cap);
+    slq_report r;
+    const int st = slq_gradient_descent_hbm(b200::ctx(), dA, P.M.data().data(), nullptr, x0.data(), &gp, &so,
+                                            x.data(), &r, est.data(), err.data(), tru.data());
+    slq_dense_free(dA);
+    b200::check(st);
+    SolveReport rep;
+    rep.residual_estimate.assign(est.begin(), est.begin() + r.n_estimate);
+    rep.iterates_error.assign(err.begin(), err.begin() + r.n_err);
+    rep.residual_true.assign(tru.begin(), tru.begin() + r.n_true);
+    rep.iterations = static_cast<long>(r.iterations);
+    rep.termination = static_cast<Termination>(r.termination);
+    rep.sync_count = static_cast<long>(r.sync_count);
+    rep.wall_time = r.wall_time;
+    return {std::move(x), std::move(rep)};
 }
 
 // distsim.hpp:21-42

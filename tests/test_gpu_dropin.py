@@ -18,3 +18,4 @@ def test_cpp_dropin_example_runs_on_gpu():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "termination=" in out.stdout and "InvalidSparsity ok" in out.stdout
+    assert "hbm iterations=" in out.stdout and "InvalidDistortion ok" in out.stdout
