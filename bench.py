@@ -326,7 +326,7 @@ def run_sparse(args, world, rank, local_rank):
             "eta_F_final": rep_eta.backward_error, "phases_s": ph,
             "roofline": {"bound": "hbm", "kernel": "sparse LSQR iteration (K4s + K5)",
                          "achieved": pass_bytes / it_s / 1e9 if it_s else None, "peak": peak, "unit": "GB/s",
-                         "frac": pass_bytes / it_s / 1e9 / peak if it_s else None, "traffic": None,
+                         "frac": pass_bytes / it_s / 1e9 / peak if it_s else None, "traffic": _sparse_traffic(m, n, world),
                          "algorithmic_bytes_per_iteration": pass_bytes},
             "gpu_launches": int(ctx.kernel_launches - launches0), "clocks": ck, "generation_s": t_gen}))
     if dist is not None:
@@ -335,6 +335,18 @@ def run_sparse(args, world, rank, local_rank):
 
 
 # ------------------------------------------------------------ main
+
+def _sparse_traffic(m, n, world):
+    """DRAM bytes per sparse pass launch from the committed ncu capture
+    (profiles/ncu_summary.json), scaled to this rank's rows; None if absent."""
+    try:
+        sp = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json"))).get("sparse_pass_kernel", {})
+        if sp.get("n") != n or not sp.get("m"):
+            return None
+        return (sp["dram_bytes_read"] + sp["dram_bytes_write"]) * (m / world) / sp["m"]
+    except Exception:
+        return None
+
 
 def main():
     args = parse()
@@ -466,7 +478,10 @@ def main():
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("fused_pass", {}).get("dram_bytes_per_launch")
+            fp = json.load(open(prof)).get("fused_pass", {})
+            traffic = fp.get("dram_bytes_per_launch")
+            if traffic is not None and fp.get("m") and fp.get("n") == n and fp["m"] != ml:
+                traffic = traffic * ml / fp["m"]  # per-row traffic is size-independent; this rank's rows
         except Exception:
             traffic = None
     iter_bytes = 8.0 * ml * n + 16.0 * ml + 8.0 * n * n

@@ -1074,14 +1074,28 @@ int slq_time_kernels(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, 
 int slq_solve_host(slq_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
                    int64_t row_begin, int64_t d, int64_t zeta, uint64_t seed, const slq_solve_opts* opts,
                    double* x_out, slq_report* report, slq_phase_times* times, double* residual_estimate) {
-    slq_dense* Ad = nullptr;
-    int st = slq_dense_upload(ctx, A, m, n, lda, b, row_begin, &Ad);
-    if (st != SLQ_OK) return st;
-    st = run_solve(ctx, dense_operand(ctx, Ad), d, zeta, seed, opts, x_out, report, times, residual_estimate);
-    std::string keep = g_last_error;
-    slq_dense_free(Ad);
-    g_last_error = keep;
-    return st;
+    // The device copy of A lives in a context-owned, grow-only buffer, so
+    // repeated host solves neither cudaMalloc nor cudaFree 8*m*ld bytes (a
+    // 32 GB free/alloc pair costs tens to hundreds of milliseconds).
+    slq_dense Ad;
+    const int st0 = guarded([&] {
+        need(ctx != nullptr, SLQ_INVALID_ARG, "solve_host: null ctx");
+        need(m >= 0 && n >= 0 && lda >= m && row_begin >= 0, SLQ_INVALID_DIMS, "solve_host: bad shape");
+        need(A != nullptr || m * n == 0, SLQ_INVALID_ARG, "solve_host: null A");
+        need(b != nullptr, SLQ_INVALID_ARG, "solve_host: null b");
+        SLQ_CUDA_CHECK(cudaSetDevice(ctx->device));
+        Ad.ctx = ctx;
+        Ad.m = m;
+        Ad.n = n;
+        Ad.ld = slq::dense_ld(n);
+        Ad.row_begin = row_begin;
+        Ad.owned = false;
+        Ad.has_b = true;
+        Ad.A = static_cast<double*>(ctx->ws.host_A.ensure(sizeof(double) * std::max<int64_t>(1, m * Ad.ld)));
+        if (m > 0) upload_dense(ctx, A, m, n, lda, b, Ad.A, Ad.ld);
+    });
+    if (st0 != SLQ_OK) return st0;
+    return run_solve(ctx, dense_operand(ctx, &Ad), d, zeta, seed, opts, x_out, report, times, residual_estimate);
 }
 
 }  // extern "C"

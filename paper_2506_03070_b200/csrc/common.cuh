@@ -84,6 +84,7 @@ struct Workspace {
     DevBuf mats;         // M, Mt
     DevBuf xbuf;         // solution vector
     DevBuf tmp;
+    DevBuf host_A;       // device copy of A for slq_solve_host (kept across calls)
 };
 
 }  // namespace slq
