@@ -43,6 +43,9 @@ STATUS = {
     5: "SingularTriangular",
     11: "InvalidDistortion",
     12: "Divergence",
+    13: "NegativeArgument",
+    14: "InvalidResidual",
+    15: "UnsupportedFormat",
     8: "OOM",
     99: "Error",
 }
@@ -407,6 +410,13 @@ class RefOracle(_Base):
         L.ref_lsqr.argtypes = [_dp, _i64, _i64, _dp, _dp, _dp, ct.c_double, _i64, ct.c_int, _dp,
                                ct.c_int, ct.c_int, _dp, ct.POINTER(_RefReport), _dp, _dp, _dp]
         L.ref_partition_rows.argtypes = [_i64, ct.c_int, _ip]
+        L.ref_embedding.argtypes = [_i64, _i64, _i64, ct.c_double, ct.c_double, _dp]
+        L.ref_distortion.argtypes = [_i64, _i64, _u64, _dp, _i64, _i64, _dp, _dp]
+        L.ref_metric_scalars.argtypes = [ct.c_double] * 5 + [_dp]
+        L.ref_mm_write_csc.argtypes = [ct.c_char_p, _i64, _i64, _ip, _dp, _ip]
+        L.ref_mm_write_dense.argtypes = [ct.c_char_p, _dp, _i64, _i64]
+        L.ref_mm_read_csc.argtypes = [ct.c_char_p, _ip, _ip, _dp, _ip]
+        L.ref_mm_read_dense.argtypes = [ct.c_char_p, _ip, _dp]
         L.ref_gradient_params.argtypes = [ct.c_double, ct.c_int, _dp]
         L.ref_gradient_descent_hbm.argtypes = [ct.c_int, _dp, _i64, _i64, _ip, _dp, _ip, _dp, _dp, _dp, ct.c_double,
                                                ct.c_double, ct.c_double, _i64, _dp, ct.c_int, ct.c_int, _dp,
@@ -511,6 +521,45 @@ class RefOracle(_Base):
         out = np.zeros(2)
         self._check(self.lib.ref_gradient_params(eta, int(hbm), _d(out)))
         return float(out[0]), float(out[1])
+
+    def embedding(self, m, n, d, eps, x):
+        """embedding.hpp: [rate, kappa, iterations_for, lambert_w(x), balance_real, plan d, iters, kappa]"""
+        out = np.zeros(8)
+        self._check(self.lib.ref_embedding(m, n, d, eps, x, _d(out)))
+        return out
+
+    def distortion(self, d, zeta, seed, U, b=None):
+        U = _f(U)
+        out = np.zeros(3)
+        self._check(self.lib.ref_distortion(d, zeta, seed, _d(U), U.shape[0], U.shape[1],
+                                            _d(_col(b)) if b is not None else None, _d(out)))
+        return tuple(float(v) for v in out)
+
+    def metric_scalars(self, x, ratio, eta, res_hat, res_star):
+        out = np.zeros(3)
+        self._check(self.lib.ref_metric_scalars(x, ratio, eta, res_hat, res_star, _d(out)))
+        return tuple(float(v) for v in out)
+
+    def mm_write_csc(self, path, m, n, rows, vals, colptr):
+        self._check(self.lib.ref_mm_write_csc(path.encode(), m, n, _i(rows), _d(vals), _i(colptr)))
+
+    def mm_write_dense(self, path, A):
+        A = _f(A)
+        self._check(self.lib.ref_mm_write_dense(path.encode(), _d(A), A.shape[0], A.shape[1]))
+
+    def mm_read_csc(self, path):
+        dims = np.zeros(3, np.int64)
+        self._check(self.lib.ref_mm_read_csc(path.encode(), _i(dims), None, None, None))
+        rows, vals, cp = np.zeros(dims[2], np.int64), np.zeros(dims[2]), np.zeros(dims[1] + 1, np.int64)
+        self._check(self.lib.ref_mm_read_csc(path.encode(), _i(dims), _i(rows), _d(vals), _i(cp)))
+        return int(dims[0]), int(dims[1]), rows, vals, cp
+
+    def mm_read_dense(self, path):
+        dims = np.zeros(2, np.int64)
+        self._check(self.lib.ref_mm_read_dense(path.encode(), _i(dims), None))
+        A = np.zeros((dims[0], dims[1]), order="F")
+        self._check(self.lib.ref_mm_read_dense(path.encode(), _i(dims), _d(A)))
+        return A
 
     def gd_hbm(self, A, M, b, x0, alpha, beta, eps=1e-10, maxit=100, x_star=None, track_true=False, workers=0,
                csc=None):

@@ -17,7 +17,10 @@
 #include <vector>
 
 #include "sketchlsq/distsim.hpp"
+#include "sketchlsq/embedding.hpp"
 #include "sketchlsq/gradient.hpp"
+#include "sketchlsq/matrix_market.hpp"
+#include "sketchlsq/metrics.hpp"
 #include "sketchlsq/lsqr.hpp"
 #include "sketchlsq/preconditioner.hpp"
 #include "sketchlsq/problems.hpp"
@@ -39,6 +42,9 @@ int map_exc() {
     catch (const SingularTriangular& e) { g_err = e.what(); return 5; }
     catch (const InvalidDistortion& e) { g_err = e.what(); return 11; }
     catch (const Divergence& e) { g_err = e.what(); return 12; }
+    catch (const NegativeArgument& e) { g_err = e.what(); return 13; }
+    catch (const InvalidResidual& e) { g_err = e.what(); return 14; }
+    catch (const UnsupportedFormat& e) { g_err = e.what(); return 15; }
     catch (const std::exception& e) { g_err = e.what(); return 99; }
 }
 
@@ -329,6 +335,94 @@ int ref_gradient_descent_hbm(int csc, const double* A, int64_t m, int64_t n, con
         }
         std::memcpy(x_out, res.first.data(), sizeof(double) * n);
         fill(res.second, rep, est, err, tru);
+        return 0;
+    } catch (...) { return map_exc(); }
+}
+
+// embedding.hpp:20-98 -- out: [rate, kappa, iterations_for, lambert_w(x), balance_real, plan.d,
+// plan.predicted_iters, plan.predicted_kappa]
+int ref_embedding(int64_t m, int64_t n, int64_t d, double eps, double x, double* out) {
+    try {
+        const RateEstimate r = estimate_rate(n, d);
+        out[0] = r.rate_per_iter;
+        out[1] = r.kappa;
+        out[2] = static_cast<double>(iterations_for(eps, n, d));
+        out[3] = lambert_w(x);
+        out[4] = balance_dimension_real(m, n, eps);
+        const DimensionPlan p = select_embedding_dim(m, n, eps);
+        out[5] = static_cast<double>(p.d);
+        out[6] = static_cast<double>(p.predicted_iters);
+        out[7] = p.predicted_kappa;
+        return 0;
+    } catch (...) { return map_exc(); }
+}
+
+// metrics.hpp:66-78 distortion of the sparse sign sketch (d, zeta, seed) on
+// range(U) [+ span(b)]: out = [eta, sigma_min, sigma_max]
+int ref_distortion(int64_t d, int64_t zeta, uint64_t seed, const double* U, int64_t m, int64_t n, const double* b,
+                   double* out) {
+    try {
+        SparseSignSketch S = generate_sparse_sign(d, m, zeta, seed);
+        Vector bv;
+        if (b) bv.assign(b, b + m);
+        const DistortionReport r = distortion(S, wrap(U, m, n), b ? &bv : nullptr);
+        out[0] = r.eta;
+        out[1] = r.sigma_min;
+        out[2] = r.sigma_max;
+        return 0;
+    } catch (...) { return map_exc(); }
+}
+
+// metrics.hpp:122-150 scalar helpers: out = [mp_pdf(x, ratio), cond_bound(eta), fwd_err(res_hat, res_star)]
+int ref_metric_scalars(double x, double ratio, double eta, double res_hat, double res_star, double* out) {
+    try {
+        out[0] = marchenko_pastur_pdf(x, ratio);
+        out[1] = cond_bound(eta);
+        out[2] = forward_error_from_residuals(res_hat, res_star);
+        return 0;
+    } catch (...) { return map_exc(); }
+}
+
+// matrix_market.hpp:140-166 writers
+int ref_mm_write_csc(const char* path, int64_t m, int64_t n, const int64_t* rows, const double* vals,
+                     const int64_t* colptr) {
+    try {
+        CscMatrix A(m, n);
+        const int64_t nnz = colptr[n];
+        A.row_indices.assign(rows, rows + nnz);
+        A.values.assign(vals, vals + nnz);
+        A.col_pointers.assign(colptr, colptr + n + 1);
+        mm::write_csc(path, A);
+        return 0;
+    } catch (...) { return map_exc(); }
+}
+int ref_mm_write_dense(const char* path, const double* A, int64_t m, int64_t n) {
+    try {
+        mm::write_dense(path, wrap(A, m, n));
+        return 0;
+    } catch (...) { return map_exc(); }
+}
+// matrix_market.hpp:64-128 readers: call with out buffers NULL to get the sizes (dims[0..2] = rows, cols, nnz)
+int ref_mm_read_csc(const char* path, int64_t* dims, int64_t* rows, double* vals, int64_t* colptr) {
+    try {
+        CscMatrix A = mm::read_csc(path);
+        dims[0] = A.rows;
+        dims[1] = A.cols;
+        dims[2] = A.nnz();
+        if (rows) {
+            std::memcpy(rows, A.row_indices.data(), sizeof(int64_t) * A.row_indices.size());
+            std::memcpy(vals, A.values.data(), sizeof(double) * A.values.size());
+            std::memcpy(colptr, A.col_pointers.data(), sizeof(int64_t) * A.col_pointers.size());
+        }
+        return 0;
+    } catch (...) { return map_exc(); }
+}
+int ref_mm_read_dense(const char* path, int64_t* dims, double* out) {
+    try {
+        DenseMatrix A = mm::read_dense(path);
+        dims[0] = A.rows();
+        dims[1] = A.cols();
+        if (out) put(A, out);
         return 0;
     } catch (...) { return map_exc(); }
 }

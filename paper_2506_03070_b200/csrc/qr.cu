@@ -970,9 +970,14 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
         const int kb = static_cast<int>(std::min<int64_t>(kNbMax, n - k0));
         const int64_t rows = d - k0;
         // register panel: <= 256 rows per CTA when the cluster allows, <= 512 at most
-        const int clmax = max_panel_cluster();
+        static const int cl_env = [] {
+            const char* e = std::getenv("SLQ_PANEL_CLUSTER");  // diagnostics: cap the panel cluster size
+            return e ? std::atoi(e) : 0;
+        }();
+        const int clmax = cl_env > 0 ? std::min(cl_env, max_panel_cluster()) : max_panel_cluster();
+        const int rows_target = cl_env > 0 ? 512 : 256;
         int cl = 1;
-        while (ceil_div(rows, cl) > 256 && cl < clmax) cl *= 2;
+        while (ceil_div(rows, cl) > rows_target && cl < clmax) cl *= 2;
         if (ceil_div(rows, cl) <= kRegWarps * 32) {
             const int64_t rpc = ceil_div(rows, cl);
             int rs = 2;
