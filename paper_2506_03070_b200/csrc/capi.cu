@@ -410,6 +410,10 @@ int slq_ctx_destroy(slq_ctx* ctx) {
         slq::comm_destroy(ctx);
         if (ctx->lsqr_exec) cudaGraphExecDestroy(ctx->lsqr_exec);
         if (ctx->lsqr_hdone) cudaFreeHost(ctx->lsqr_hdone);
+        if (ctx->qr_hi) cudaStreamDestroy(ctx->qr_hi);
+        if (ctx->qr_lo) cudaStreamDestroy(ctx->qr_lo);
+        for (cudaEvent_t e : ctx->qr_ev)
+            if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : ctx->lsqr_ev)
             if (e) cudaEventDestroy(e);
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);

@@ -79,7 +79,7 @@ struct Workspace {
     DevBuf yaug;         // Y_aug = [S A | S b], d x (n+1) column-major
     DevBuf flags;        // small device counters / error flags
     DevBuf staging[2];   // upload staging
-    DevBuf qr_t, qr_w, qr_q, qr_misc;
+    DevBuf qr_t, qr_w, qr_w2, qr_q, qr_misc;
     DevBuf lsqr_vec, lsqr_part, lsqr_state, lsqr_u;
     DevBuf mats;         // M, Mt
     DevBuf xbuf;         // solution vector
@@ -105,6 +105,9 @@ struct slq_ctx {
     // cached LSQR iteration graph (rebuilt when any captured pointer / size changes)
     cudaGraphExec_t lsqr_exec = nullptr;
     std::vector<uint64_t> lsqr_key;
+    // QR look-ahead streams (panel + narrow update / wide update) and events
+    cudaStream_t qr_hi = nullptr, qr_lo = nullptr;
+    cudaEvent_t qr_ev[3] = {nullptr, nullptr, nullptr};
     int* lsqr_hdone = nullptr;            // pinned done-flag mirror (2 ints)
     cudaEvent_t lsqr_ev[2] = {nullptr, nullptr};
 };

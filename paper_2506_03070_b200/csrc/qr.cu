@@ -840,7 +840,7 @@ __global__ void scale_cols_kernel(double* Q, int64_t d, int64_t n, const double*
     Q[e] *= sign[e / d];
 }
 
-void launch_panel(slq_ctx* ctx, const PanelArgs& pa, int cl) {
+void launch_panel(slq_ctx* ctx, const PanelArgs& pa, int cl, cudaStream_t st) {
     const size_t smem = static_cast<size_t>(pa.rpc) * kWs * sizeof(double);
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
@@ -850,7 +850,7 @@ void launch_panel(slq_ctx* ctx, const PanelArgs& pa, int cl) {
     cfg.gridDim = dim3(cl, 1, 1);
     cfg.blockDim = dim3(kPanelThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
-    cfg.stream = ctx->stream;
+    cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = cl;
@@ -863,7 +863,7 @@ void launch_panel(slq_ctx* ctx, const PanelArgs& pa, int cl) {
 }
 
 template <int RS>
-void launch_panel_reg_rs(slq_ctx* ctx, const PanelArgs& pa, int cl) {
+void launch_panel_reg_rs(slq_ctx* ctx, const PanelArgs& pa, int cl, cudaStream_t st) {
     const size_t smem = static_cast<size_t>(pa.rpc) * kWs * sizeof(double);
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(panel_reg_kernel<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
@@ -873,7 +873,7 @@ void launch_panel_reg_rs(slq_ctx* ctx, const PanelArgs& pa, int cl) {
     cfg.gridDim = dim3(cl, 1, 1);
     cfg.blockDim = dim3(kRegPanelThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
-    cfg.stream = ctx->stream;
+    cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = cl;
@@ -885,13 +885,13 @@ void launch_panel_reg_rs(slq_ctx* ctx, const PanelArgs& pa, int cl) {
     ctx->launches++;
 }
 
-void launch_panel_reg(slq_ctx* ctx, const PanelArgs& pa, int cl, int rs) {
+void launch_panel_reg(slq_ctx* ctx, const PanelArgs& pa, int cl, int rs, cudaStream_t st) {
     switch (rs) {
-        case 2: launch_panel_reg_rs<2>(ctx, pa, cl); break;
-        case 4: launch_panel_reg_rs<4>(ctx, pa, cl); break;
-        case 8: launch_panel_reg_rs<8>(ctx, pa, cl); break;
-        case 16: launch_panel_reg_rs<16>(ctx, pa, cl); break;
-        default: launch_panel_reg_rs<32>(ctx, pa, cl); break;
+        case 2: launch_panel_reg_rs<2>(ctx, pa, cl, st); break;
+        case 4: launch_panel_reg_rs<4>(ctx, pa, cl, st); break;
+        case 8: launch_panel_reg_rs<8>(ctx, pa, cl, st); break;
+        case 16: launch_panel_reg_rs<16>(ctx, pa, cl, st); break;
+        default: launch_panel_reg_rs<32>(ctx, pa, cl, st); break;
     }
 }
 
@@ -923,22 +923,39 @@ int max_panel_cluster() {
     return cached;
 }
 
-void launch_update(slq_ctx* ctx, const UpdArgs& u) {
+void launch_update(slq_ctx* ctx, const UpdArgs& u, cudaStream_t st, DevBuf& wbuf) {
     if (u.c_end <= u.c_begin || u.r_end <= u.k0) return;
     const unsigned ncb = static_cast<unsigned>(ceil_div(u.c_end - u.c_begin, kCB));
     const unsigned nrb = static_cast<unsigned>(ceil_div(u.r_end - u.k0, kRB));
-    double* Wpart = static_cast<double*>(ctx->ws.qr_w.ensure(sizeof(double) * kNbMax * kCB * ncb * (nrb + 1)));
+    double* Wpart = static_cast<double*>(wbuf.ensure(sizeof(double) * kNbMax * kCB * ncb * (nrb + 1)));
     double* W2 = Wpart + static_cast<int64_t>(kNbMax) * kCB * ncb * nrb;
     const size_t sm1 = sizeof(double) * (kNbMax + kCB) * kLdT;
     const size_t sm2 = sm1 + sizeof(double) * kNbMax * (kCB + 1);
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(update_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm1)));
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(update_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2)));
-    update_w_kernel<<<dim3(ncb, nrb), 256, sm1, ctx->stream>>>(u, Wpart);
+    update_w_kernel<<<dim3(ncb, nrb), 256, sm1, st>>>(u, Wpart);
     SLQ_LAUNCH_CHECK(ctx);
-    update_reduce_kernel<<<ncb, 256, 0, ctx->stream>>>(u, Wpart, static_cast<int>(nrb), W2);
+    update_reduce_kernel<<<ncb, 256, 0, st>>>(u, Wpart, static_cast<int>(nrb), W2);
     SLQ_LAUNCH_CHECK(ctx);
-    update_apply_kernel<<<dim3(ncb, nrb), 256, sm2, ctx->stream>>>(u, W2);
+    update_apply_kernel<<<dim3(ncb, nrb), 256, sm2, st>>>(u, W2);
     SLQ_LAUNCH_CHECK(ctx);
+}
+
+// the context's two QR streams (created on first use, high / low priority) and events
+void qr_streams(slq_ctx* ctx, cudaStream_t& hi, cudaStream_t& lo, cudaEvent_t& ev_p, cudaEvent_t& ev_w,
+                cudaEvent_t& ev_0) {
+    if (!ctx->qr_hi) {
+        int least = 0, greatest = 0;
+        SLQ_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        SLQ_CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->qr_hi, cudaStreamNonBlocking, greatest));
+        SLQ_CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->qr_lo, cudaStreamNonBlocking, least));
+        for (cudaEvent_t& e : ctx->qr_ev) SLQ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    hi = ctx->qr_hi;
+    lo = ctx->qr_lo;
+    ev_p = ctx->qr_ev[0];
+    ev_w = ctx->qr_ev[1];
+    ev_0 = ctx->qr_ev[2];
 }
 
 }  // namespace
@@ -965,6 +982,20 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
     maxabs_final_kernel<<<1, 32, 0, ctx->stream>>>(part, nb_blocks, rank_tol);
     SLQ_LAUNCH_CHECK(ctx);
 
+    // Look-ahead schedule (depth 1) on two streams: s_hi runs the panels and the
+    // narrow update N(p) of the next panel's 32 columns, s_lo the wide update
+    // W(p) of every column after it.  W(p-1) then overlaps panel(p):
+    //   s_hi: panel(p) -> [ev_p] -> wait W(p-1) -> N(p) -> panel(p+1) ...
+    //   s_lo: wait ev_p -> W(p) -> [ev_w]
+    // Column sets of N(p), W(p) and panel(p+1) are disjoint; W(p-1) precedes
+    // N(p) and W(p) on the columns they share (event / stream order).
+    cudaStream_t s_hi, s_lo;
+    cudaEvent_t ev_p, ev_w, ev_0;
+    qr_streams(ctx, s_hi, s_lo, ev_p, ev_w, ev_0);
+    SLQ_CUDA_CHECK(cudaEventRecord(ev_0, ctx->stream));
+    SLQ_CUDA_CHECK(cudaStreamWaitEvent(s_hi, ev_0, 0));
+    SLQ_CUDA_CHECK(cudaStreamWaitEvent(s_lo, ev_0, 0));
+    bool w_pending = false;
     for (int64_t p = 0; p < npanels; ++p) {
         const int64_t k0 = p * kNbMax;
         const int kb = static_cast<int>(std::min<int64_t>(kNbMax, n - k0));
@@ -983,7 +1014,7 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
             int rs = 2;
             while (rs * kRegWarps < rpc) rs *= 2;
             PanelArgs pa{Yaug, ldy, d, k0, kb, rpc, rank_tol, tau, T + p * kNbMax * kNbMax, err};
-            launch_panel_reg(ctx, pa, cl, rs);
+            launch_panel_reg(ctx, pa, cl, rs, s_hi);
         } else {
             // very tall sketches: shared-memory panel (two reductions per column)
             cl = 1;
@@ -992,11 +1023,26 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
             if (ceil_div(rows, cl) > max_rows_cta)
                 fail(SLQ_UNSUPPORTED, "householder_qr: sketch too tall for the panel kernel");
             PanelArgs pa{Yaug, ldy, d, k0, kb, ceil_div(rows, cl), rank_tol, tau, T + p * kNbMax * kNbMax, err};
-            launch_panel(ctx, pa, cl);
+            launch_panel(ctx, pa, cl, s_hi);
         }
-        UpdArgs u{Yaug, ldy, k0, kb, T + p * kNbMax * kNbMax, Yaug, ldy, k0 + kb, ncols, d, 1};
-        launch_update(ctx, u);
+        SLQ_CUDA_CHECK(cudaEventRecord(ev_p, s_hi));
+        const int64_t c_mid = std::min<int64_t>(ncols, k0 + kb + kNbMax);
+        if (k0 + kb < ncols) {
+            if (w_pending) SLQ_CUDA_CHECK(cudaStreamWaitEvent(s_hi, ev_w, 0));  // W(p-1) on these columns
+            UpdArgs un{Yaug, ldy, k0, kb, T + p * kNbMax * kNbMax, Yaug, ldy, k0 + kb, c_mid, d, 1};
+            launch_update(ctx, un, s_hi, ws.qr_w);
+        }
+        if (c_mid < ncols) {
+            SLQ_CUDA_CHECK(cudaStreamWaitEvent(s_lo, ev_p, 0));
+            UpdArgs uw{Yaug, ldy, k0, kb, T + p * kNbMax * kNbMax, Yaug, ldy, c_mid, ncols, d, 1};
+            launch_update(ctx, uw, s_lo, ws.qr_w2);
+            SLQ_CUDA_CHECK(cudaEventRecord(ev_w, s_lo));
+            w_pending = true;
+        }
     }
+    SLQ_CUDA_CHECK(cudaEventRecord(ev_p, s_hi));
+    SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ev_p, 0));
+    if (w_pending) SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ev_w, 0));
     int herr = 0;
     SLQ_CUDA_CHECK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
@@ -1015,7 +1061,7 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
             const int64_t k0 = p * kNbMax;
             const int kb = static_cast<int>(std::min<int64_t>(kNbMax, n - k0));
             UpdArgs u{Yaug, ldy, k0, kb, T + p * kNbMax * kNbMax, Q, d, k0, n, d, 0};
-            launch_update(ctx, u);
+            launch_update(ctx, u, ctx->stream, ws.qr_w);
         }
         scale_cols_kernel<<<static_cast<unsigned>(ceil_div(d * n, 256)), 256, 0, ctx->stream>>>(Q, d, n, sign);
         SLQ_LAUNCH_CHECK(ctx);
