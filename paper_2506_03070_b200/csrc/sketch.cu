@@ -239,7 +239,7 @@ struct BucketArgs {
     uint16_t* ent_out;
     int cap;                         // smem key capacity (power of 2)
     int* overflow;
-    int slots;                       // 1: entries as gather_kernel slots (see below)
+    int slots;                       // 0: (k_local << 1 | neg); W = 4 / 2 / 1: gather_kernel byte offsets (see below)
 };
 
 __device__ __forceinline__ int gslot(int k, int h);
@@ -295,11 +295,14 @@ __global__ void __launch_bounds__(1024) bucketize_kernel(BucketArgs a) {
     const uint32_t lowmask = (1u << sh) - 1u;
     for (int i = tid; i < N; i += T) {
         const uint32_t kv = keys[i] & lowmask;  // k_local << 1 | neg
-        // slots: byte offset of the entry's first 16-byte half in the A stage
-        // (the second is at offset ^ 16) with the sign in bit 0, so the
-        // gather decodes an entry with a few logic ops
-        ent[i] = a.slots ? static_cast<uint16_t>((gslot(static_cast<int>(kv >> 1), 0) << 4) | (kv & 1u))
-                         : static_cast<uint16_t>(kv);
+        // slots: byte offset of the entry's A row in the gather's smem stage
+        // (W = 4: the first 16-byte half, the second at offset ^ 16) with the
+        // sign in bit 0, so the gather decodes an entry with a few logic ops
+        const int kl = static_cast<int>(kv >> 1);
+        const uint32_t off = a.slots == 4 ? static_cast<uint32_t>(gslot(kl, 0)) << 4
+                             : a.slots == 2 ? static_cast<uint32_t>(kl) << 4
+                                            : static_cast<uint32_t>(kl) << 3;
+        ent[i] = a.slots ? static_cast<uint16_t>(off | (kv & 1u)) : static_cast<uint16_t>(kv);
         const int64_t r = keys[i] >> sh;
         const int64_t rp = (i == 0) ? -1 : static_cast<int64_t>(keys[i - 1] >> sh);
         for (int64_t rr = rp + 1; rr <= r; ++rr) ptr[rr] = static_cast<uint16_t>(i);
@@ -329,6 +332,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g));
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(g));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -338,15 +345,22 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // all eight 16-byte bank groups (row parity x bit 2 of k), as do the second.
 __device__ __forceinline__ int gslot(int k, int h) { return 2 * k + (h ^ ((k >> 2) & 1)); }  // gslot(k,1) == gslot(k,0)^1
 
+template <int W>
 __device__ __forceinline__ void stage_chunk(const GatherArgs& g, int64_t col0, int64_t c, double* As, uint16_t* Ps,
                                             uint16_t* Es) {
     const int tid = threadIdx.x;
     const int64_t k0 = c * g.K;
     const int kc = static_cast<int>(min(static_cast<int64_t>(g.K), g.m - k0));
     const double* base = g.A + k0 * g.ld + col0;
-    for (int p = tid; p < 2 * kc; p += kGThreads) {
-        const int k = p >> 1, h = p & 1;
-        cp_async16(As + 2 * gslot(k, h), base + static_cast<int64_t>(k) * g.ld + 2 * h);
+    if (W == 4) {
+        for (int p = tid; p < 2 * kc; p += kGThreads) {
+            const int k = p >> 1, h = p & 1;
+            cp_async16(As + 2 * gslot(k, h), base + static_cast<int64_t>(k) * g.ld + 2 * h);
+        }
+    } else if (W == 2) {
+        for (int k = tid; k < kc; k += kGThreads) cp_async16(As + 2 * k, base + static_cast<int64_t>(k) * g.ld);
+    } else {
+        for (int k = tid; k < kc; k += kGThreads) cp_async8(As + k, base + static_cast<int64_t>(k) * g.ld);
     }
     const uint16_t* gp = g.ptr + c * g.ptr_stride;
     for (int p = tid; p < g.ptr_stride / 8; p += kGThreads) cp_async16(Ps + 8 * p, gp + 8 * p);
@@ -367,16 +381,16 @@ __device__ __forceinline__ double acc_step(double y, double v, double a) {
 // (r, k) are staged by cp.async (double buffer); each thread walks its rows'
 // entries in ascending k -- the reference's order -- gathering 32 bytes of A
 // per entry.
-template <int RPT, bool EXACT>
+template <int RPT, int W, bool EXACT>
 __global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int tid = threadIdx.x;
-    const int64_t col0 = static_cast<int64_t>(blockIdx.x) * 4;
+    const int64_t col0 = static_cast<int64_t>(blockIdx.x) * W;
     const int64_t split = blockIdx.y;
     const int64_t cb = split * g.nchunks / g.nsplit;
     const int64_t ce = (split + 1) * g.nchunks / g.nsplit;
 
-    const size_t a_bytes = static_cast<size_t>(g.K) * 4 * sizeof(double);
+    const size_t a_bytes = static_cast<size_t>(g.K) * W * sizeof(double);
     const size_t p_bytes = g.ptr_stride * sizeof(uint16_t);
     const size_t e_bytes = g.ent_stride * sizeof(uint16_t);
     const size_t st_bytes = a_bytes + p_bytes + e_bytes;
@@ -385,17 +399,17 @@ __global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
     auto Es = [&](int s) { return reinterpret_cast<uint16_t*>(smem + s * st_bytes + a_bytes + p_bytes); };
 
     const uint64_t vbits = static_cast<uint64_t>(__double_as_longlong(g.val));
-    double y[RPT][4];
+    double y[RPT][W];
 #pragma unroll
     for (int q = 0; q < RPT; ++q)
 #pragma unroll
-        for (int w = 0; w < 4; ++w) y[q][w] = 0.0;
+        for (int w = 0; w < W; ++w) y[q][w] = 0.0;
 
-    if (cb < ce) stage_chunk(g, col0, cb, As(0), Ps(0), Es(0));
+    if (cb < ce) stage_chunk<W>(g, col0, cb, As(0), Ps(0), Es(0));
     cp_commit();
     for (int64_t c = cb; c < ce; ++c) {
         const int s = static_cast<int>((c - cb) & 1);
-        if (c + 1 < ce) stage_chunk(g, col0, c + 1, As(s ^ 1), Ps(s ^ 1), Es(s ^ 1));
+        if (c + 1 < ce) stage_chunk<W>(g, col0, c + 1, As(s ^ 1), Ps(s ^ 1), Es(s ^ 1));
         cp_commit();
         cp_wait<1>();
         __syncthreads();
@@ -409,14 +423,22 @@ __global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
                 const int e0 = P_s[r], e1 = P_s[r + 1];
                 for (int e = e0; e < e1; ++e) {
                     const unsigned en = E_s[e];
-                    const unsigned o0 = en & 0xFFF0u;
+                    const unsigned o0 = en & 0xFFF8u;
                     const double v = __longlong_as_double(static_cast<long long>(vbits ^ (static_cast<uint64_t>(en) << 63)));
-                    const double2 lo = *reinterpret_cast<const double2*>(A_b + o0);
-                    const double2 hi = *reinterpret_cast<const double2*>(A_b + (o0 ^ 16u));
-                    y[q][0] = acc_step<EXACT>(y[q][0], v, lo.x);
-                    y[q][1] = acc_step<EXACT>(y[q][1], v, lo.y);
-                    y[q][2] = acc_step<EXACT>(y[q][2], v, hi.x);
-                    y[q][3] = acc_step<EXACT>(y[q][3], v, hi.y);
+                    if (W == 4) {
+                        const double2 lo = *reinterpret_cast<const double2*>(A_b + o0);
+                        const double2 hi = *reinterpret_cast<const double2*>(A_b + (o0 ^ 16u));
+                        y[q][0] = acc_step<EXACT>(y[q][0], v, lo.x);
+                        y[q][1 % W] = acc_step<EXACT>(y[q][1 % W], v, lo.y);
+                        y[q][2 % W] = acc_step<EXACT>(y[q][2 % W], v, hi.x);
+                        y[q][3 % W] = acc_step<EXACT>(y[q][3 % W], v, hi.y);
+                    } else if (W == 2) {
+                        const double2 lo = *reinterpret_cast<const double2*>(A_b + o0);
+                        y[q][0] = acc_step<EXACT>(y[q][0], v, lo.x);
+                        y[q][1 % W] = acc_step<EXACT>(y[q][1 % W], v, lo.y);
+                    } else {
+                        y[q][0] = acc_step<EXACT>(y[q][0], v, *reinterpret_cast<const double*>(A_b + o0));
+                    }
                 }
             }
         }
@@ -429,7 +451,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
         const int r = tid + q * kGThreads;
         if (r < g.d)
 #pragma unroll
-            for (int w = 0; w < 4; ++w) Y[(col0 + w) * g.d + r] = y[q][w];
+            for (int w = 0; w < W; ++w) Y[(col0 + w) * g.d + r] = y[q][w];
     }
 }
 
@@ -750,16 +772,18 @@ void generate_sparse_sign_dev(slq_ctx* ctx, int64_t d, int64_t zeta, uint64_t se
 
 namespace {
 
-ChunkPlan plan_chunks(int64_t m, int64_t d, int64_t zeta_max) {
+ChunkPlan plan_chunks(int64_t m, int64_t d, int64_t zeta_max, int W) {
     ChunkPlan p{};
     int zp = 1;
     while (zp < zeta_max) zp <<= 1;
     p.ptr_stride = round_up(d + 1, 8);
     // largest power-of-two K (<= 2048, entries <= 16384 for u16 offsets) whose
-    // double-buffered stage (A slab 32 B/row + row pointers + entries) fits
+    // double-buffered stage (A slab 8*W B/row + row pointers + entries) fits
+    const int64_t rowb = 8 * std::max(W, 4);  // the sparse path (W = 0) keeps the W = 4 plan
     int K = 2048;
     while (K > 16 && (static_cast<int64_t>(K) * zp > 16384 ||
-                      2 * (K * 32 + p.ptr_stride * 2 + round_up(static_cast<int64_t>(K) * zeta_max, 8) * 2) > 220 * 1024))
+                      2 * (K * rowb + p.ptr_stride * 2 + round_up(static_cast<int64_t>(K) * zeta_max, 8) * 2) >
+                          220 * 1024))
         K >>= 1;
     p.K = K;
     p.KB = 0;
@@ -770,9 +794,9 @@ ChunkPlan plan_chunks(int64_t m, int64_t d, int64_t zeta_max) {
     return p;
 }
 
-template <int RPT, bool EXACT>
+template <int RPT, int W, bool EXACT>
 void launch_gather_t(slq_ctx* ctx, const GatherArgs& g, int64_t nslabs, size_t smem) {
-    auto kern = gather_kernel<RPT, EXACT>;
+    auto kern = gather_kernel<RPT, W, EXACT>;
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     dim3 grid(static_cast<unsigned>(nslabs), static_cast<unsigned>(g.nsplit));
     kern<<<grid, kGThreads, smem, ctx->stream>>>(g);
@@ -780,13 +804,15 @@ void launch_gather_t(slq_ctx* ctx, const GatherArgs& g, int64_t nslabs, size_t s
 }
 
 template <bool EXACT>
-void launch_gather(slq_ctx* ctx, const GatherArgs& g, int rpt, int64_t nslabs, size_t smem) {
+void launch_gather(slq_ctx* ctx, const GatherArgs& g, int rpt, int W, int64_t nslabs, size_t smem) {
     switch (rpt) {
-        case 1: launch_gather_t<1, EXACT>(ctx, g, nslabs, smem); break;
-        case 2: launch_gather_t<2, EXACT>(ctx, g, nslabs, smem); break;
-        case 4: launch_gather_t<4, EXACT>(ctx, g, nslabs, smem); break;
-        case 8: launch_gather_t<8, EXACT>(ctx, g, nslabs, smem); break;
-        default: fail(SLQ_UNSUPPORTED, "sketch_apply: d > 4096 not supported by the register-slab gather");
+        case 1: launch_gather_t<1, 4, EXACT>(ctx, g, nslabs, smem); break;
+        case 2: launch_gather_t<2, 4, EXACT>(ctx, g, nslabs, smem); break;
+        case 4: launch_gather_t<4, 4, EXACT>(ctx, g, nslabs, smem); break;
+        case 8: launch_gather_t<8, 4, EXACT>(ctx, g, nslabs, smem); break;
+        case 16: launch_gather_t<16, 2, EXACT>(ctx, g, nslabs, smem); break;  // 4096 < d <= 8192: 2-column slabs
+        case 32: launch_gather_t<32, 1, EXACT>(ctx, g, nslabs, smem); break;  // d <= 16384: 1-column slabs
+        default: fail(SLQ_UNSUPPORTED, "sketch_apply: d > 16384 not supported by the register-slab gather");
     }
 }
 
@@ -913,10 +939,10 @@ void generate_sparse_rows_dev(slq_ctx* ctx, int64_t n, int64_t nnz, uint64_t see
 }
 
 ChunkCsr build_chunk_csr(slq_ctx* ctx, const uint32_t* compact, const int64_t* colptr_dev, int64_t zeta_max,
-                         int64_t m, int64_t d, bool gather_slots) {
+                         int64_t m, int64_t d, int gather_width) {
     Workspace& ws = ctx->ws;
     ChunkCsr cc;
-    cc.plan = plan_chunks(m, d, zeta_max);
+    cc.plan = plan_chunks(m, d, zeta_max, gather_width);
     const ChunkPlan& cp = cc.plan;
     // slack: row-part slices may run past the last chunk
     cc.ptr = static_cast<uint16_t*>(ws.chunk_ptr.ensure(sizeof(uint16_t) * (cp.ptr_stride * cp.nchunks + d + 64)));
@@ -924,7 +950,7 @@ ChunkCsr build_chunk_csr(slq_ctx* ctx, const uint32_t* compact, const int64_t* c
     cc.flag = static_cast<int*>(ws.flags.ensure(4096));
     SLQ_CUDA_CHECK(cudaMemsetAsync(cc.flag, 0, sizeof(int), ctx->stream));
     BucketArgs ba{compact, colptr_dev, zeta_max, m, d, cp.K, cp.KB, cp.ptr_stride, cp.ent_stride, cc.ptr, cc.ent,
-                  cp.cap, cc.flag, gather_slots ? 1 : 0};
+                  cp.cap, cc.flag, gather_width};
     const size_t bsmem = sizeof(uint32_t) * cp.cap;
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(bucketize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(bsmem)));
@@ -955,16 +981,17 @@ void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const
     // d = 4n, slower than the register-row gather (one entry per warp
     // instruction vs 32): opt-in for experiments only
     if (slq_env_flag("SLQ_SLAB_GATHER") && sketch_apply_slab(ctx, A, d, compact, colptr_dev, zeta, val, exact, Y)) return;
-    ChunkCsr cc = build_chunk_csr(ctx, compact, colptr_dev, zeta, m, d, true);
+    // W-column slab per CTA, all d rows of the slab in registers (32 doubles per
+    // thread: W = 4 up to d = 4096, W = 2 up to 8192, W = 1 up to 16384)
+    int rpt = 1;
+    while (rpt * kGThreads < d) rpt <<= 1;
+    const int W = rpt <= 8 ? 4 : (rpt == 16 ? 2 : 1);
+    ChunkCsr cc = build_chunk_csr(ctx, compact, colptr_dev, zeta, m, d, W);
     const ChunkPlan& cp = cc.plan;
     uint16_t* ptr = cc.ptr;
     uint16_t* ent = cc.ent;
-
-    // 4-column slab per CTA, all d rows of the slab in registers (<= 8 rows per thread)
-    int rpt = 1;
-    while (rpt * kGThreads < d) rpt <<= 1;
-    const int64_t ldw = round_up(ld, 4);
-    const int64_t nslabs = ldw / 4;
+    const int64_t ldw = round_up(ld, W);
+    const int64_t nslabs = ldw / W;
     // splits along m: balance waves over the SMs unless the exact serial order is asked for
     int64_t nsplit = 1;
     if (!exact) {
@@ -983,11 +1010,11 @@ void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const
     double* Yw = (nsplit == 1 && ldw == ncols_out) ? Y
                  : static_cast<double*>(ws.ypart.ensure(sizeof(double) * nsplit * ldw * d));
     GatherArgs g{A->A, ld, m, d, cp.K, cp.nchunks, nsplit, cp.ptr_stride, cp.ent_stride, ptr, ent, val, ldw, Yw};
-    const size_t smem = 2 * (static_cast<size_t>(cp.K) * 4 * sizeof(double) + cp.ptr_stride * sizeof(uint16_t) +
+    const size_t smem = 2 * (static_cast<size_t>(cp.K) * W * sizeof(double) + cp.ptr_stride * sizeof(uint16_t) +
                              cp.ent_stride * sizeof(uint16_t));
     if (smem > 227 * 1024) fail(SLQ_UNSUPPORTED, "sketch_apply: stage exceeds shared memory");
-    if (exact) launch_gather<true>(ctx, g, rpt, nslabs, smem);
-    else launch_gather<false>(ctx, g, rpt, nslabs, smem);
+    if (exact) launch_gather<true>(ctx, g, rpt, W, nslabs, smem);
+    else launch_gather<false>(ctx, g, rpt, W, nslabs, smem);
     if (Yw != Y) {
         const int64_t tot = d * ncols_out;
         reduce_splits_kernel<<<static_cast<unsigned>(ceil_div(tot, 256)), 256, 0, ctx->stream>>>(

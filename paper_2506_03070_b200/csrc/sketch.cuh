@@ -18,10 +18,10 @@ struct ChunkCsr {
     uint16_t* ent = nullptr;
     int* flag = nullptr;
 };
-// gather_slots: entries encoded for the dense gather (slot | neg << 15)
-// instead of (k_local << 1 | neg).
+// gather_width W = 4 / 2 / 1: entries encoded for the dense gather of W-column
+// slabs (smem byte offset | neg); 0: (k_local << 1 | neg) for the sparse path.
 ChunkCsr build_chunk_csr(slq_ctx* ctx, const uint32_t* compact, const int64_t* colptr_dev, int64_t zeta_max,
-                         int64_t m, int64_t d, bool gather_slots);
+                         int64_t m, int64_t d, int gather_width);
 void check_chunk_csr(slq_ctx* ctx, const ChunkCsr& cc);
 
 // K1: sparse-sign generator for global columns [col_begin, col_begin+ncols).

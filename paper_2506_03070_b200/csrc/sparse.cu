@@ -564,7 +564,7 @@ void sketch_apply_sparse_compact_dev(slq_ctx* ctx, const slq_sparse* A, int64_t 
         SLQ_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(double) * d * (n + 1), ctx->stream));
         return;
     }
-    ChunkCsr cc = build_chunk_csr(ctx, compact, colptr_dev, zeta_max, m, d, false);
+    ChunkCsr cc = build_chunk_csr(ctx, compact, colptr_dev, zeta_max, m, d, 0);
     // S^T rows (entries of each Y row in ascending k)
     DevBuf srp, scan_tmp;
     int64_t* srow_ptr = static_cast<int64_t*>(srp.ensure(sizeof(int64_t) * (d + 1)));

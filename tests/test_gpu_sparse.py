@@ -90,3 +90,24 @@ def test_sparse_solve_pipeline():
     assert rep.iterations == 25
     assert eta(x) <= max(2 * eta(xo), 1e-14)
     assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+def test_sparse_lsqr_long_rows():
+    """Rows longer than 64 and 255 entries take the pass's tail path."""
+    m, n, d, zeta = 3000, 600, 1200, 8
+    Acsc, A = rand_csc(m, n, 0.01, 5, long_rows=4)
+    Ad = A.toarray()
+    Ad[10, :500] = np.random.default_rng(9).standard_normal(500)  # 500-entry row
+    Ad[11, ::7] = 1.0
+    As = sp.csc_matrix(Ad)
+    As.sort_indices()
+    Acsc = slq.CscMatrix(m, n, As.data.copy(), As.indices.astype(np.int64), As.indptr.astype(np.int64))
+    b = np.random.default_rng(2).standard_normal(m)
+    Y, Sb = C.sketch_apply_csc(d, zeta, 5, m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, b)
+    M, Q = C.build_preconditioner(Y)
+    x0 = C.initial_guess(M, Q, Sb)
+    x, rep = slq.lsqr_one_sync(Acsc, M, b, x0, slq.SolveOptions(eps=0.0, maxit=8))
+    xo, repo = C.lsqr_csc(m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, M, b, x0, eps=0.0, maxit=8,
+                          one_sync=True)
+    assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
+    assert np.allclose(rep.residual_estimate, repo.residual_estimate, rtol=1e-9)
