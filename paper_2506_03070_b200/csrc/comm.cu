@@ -73,7 +73,10 @@ void comm_init(slq_ctx* ctx, const unsigned char id[128], int rank, int nranks) 
     }
     ctx->rank = rank;
     ctx->nranks = nranks;
-    if (nranks == 1) return;  // single rank: collectives are identities
+    // single rank: collectives are identities and are skipped, unless
+    // SLQ_FORCE_NCCL asks for a real one-rank communicator (exercises the
+    // NCCL path on one GPU)
+    if (nranks == 1 && !slq_env_flag("SLQ_FORCE_NCCL")) return;
     ncclUniqueId uid;
     std::memcpy(&uid, id, 128);
     SLQ_CUDA_CHECK(cudaSetDevice(ctx->device));
