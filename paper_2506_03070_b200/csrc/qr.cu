@@ -22,6 +22,8 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <vector>
 
 #include "common.cuh"
 #include "qr.cuh"
@@ -73,6 +75,7 @@ struct PanelArgs {
     double* tau;       // global tau[n]
     double* T;         // kb x kb (ld kNbMax) compact-WY factor of this panel
     int* err;          // 0 or 1 + failing column
+    long long* prof;   // diagnostics (SLQ_PANEL_PROF): per CTA / column phase clocks, or null
 };
 
 // Point-to-point cluster reduction: warp 0 of every CTA pushes its L partials
@@ -302,14 +305,25 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(PanelArgs a) {
 // applied, so each column costs one block barrier plus one DSMEM exchange.
 // The panel slice lives in registers: thread (warp w, lane j) owns column j
 // of local rows w + 16 s, s < RS.
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
 constexpr int kRegPanelThreads = 512;
 constexpr int kRegWarps = kRegPanelThreads / 32;
 
 template <int RS>
 __global__ void __launch_bounds__(kRegPanelThreads, 1) panel_reg_kernel(PanelArgs a) {
     extern __shared__ __align__(16) double w[];  // [rpc][kWs] staging for the coalesced load / store
-    __shared__ double red[kRegWarps][32];
-    __shared__ double rrow[32];
+    __shared__ double red[2][kRegWarps][32];  // warp partials, double-buffered by column parity
+    __shared__ double rrow[2][32];
+    __shared__ __align__(16) double mine[2][64];  // this CTA's (G_j, R_j) pairs (bulk-copied to peers)
+    __shared__ __align__(16) double tot[2][64];   // cluster sums, broadcast to the CTA's warps
     __shared__ __align__(16) double inbox[2][16][64];
     __shared__ double Ts[kNbMax][kNbMax + 1];
     __shared__ uint64_t mbar[2];
@@ -353,39 +367,47 @@ __global__ void __launch_bounds__(kRegPanelThreads, 1) panel_reg_kernel(PanelArg
         if (il < nrows && (!r0 || il > 0)) g = fma(v[s], vk, g);
     }
 
+    long long* prof = (a.prof && tid == 0) ? a.prof + static_cast<int64_t>(rank) * 32 * 8 : nullptr;
     for (int kk = 0; kk < kb; ++kk) {
         const int p = kk & 1;
         const unsigned phase = static_cast<unsigned>((kk >> 1) & 1);
-        red[wid][lane] = g;
-        if (r0 && wid == (kk & (kRegWarps - 1))) rrow[lane] = (kk < kRegWarps) ? v[0] : v[1];
+        if (prof) prof[kk * 8 + 0] = clock64();
+        red[p][wid][lane] = g;
+        if (r0 && wid == (kk & (kRegWarps - 1))) rrow[p][lane] = (kk < kRegWarps) ? v[0] : v[1];
         __syncthreads();
+        if (prof) prof[kk * 8 + 1] = clock64();
         const unsigned bar = static_cast<unsigned>(__cvta_generic_to_shared(&mbar[p]));
         if (wid == 0) {
+            // warp 0: this CTA's (G_j, R_j) vector = fixed-order sum of the 16 warp partials
             double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
 #pragma unroll
             for (int q = 0; q < kRegWarps; q += 4) {
-                t0 += red[q][lane];
-                t1 += red[q + 1][lane];
-                t2 += red[q + 2][lane];
-                t3 += red[q + 3][lane];
+                t0 += red[p][q][lane];
+                t1 += red[p][q + 1][lane];
+                t2 += red[p][q + 2][lane];
+                t3 += red[p][q + 3][lane];
             }
-            const double gsum = (t0 + t1) + (t2 + t3);
-            const double rj = r0 ? rrow[lane] : 0.0;
+            *reinterpret_cast<double2*>(&mine[p][2 * lane]) = make_double2((t0 + t1) + (t2 + t3), r0 ? rrow[p][lane] : 0.0);
             if (lane == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
                              "r"(static_cast<unsigned>(nr * 64 * sizeof(double)))
                              : "memory");
-            const unsigned slot = static_cast<unsigned>(__cvta_generic_to_shared(&inbox[p][rank][2 * lane]));
-            for (unsigned q = 0; q < nr; ++q) {
-                unsigned rslot, rbar;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rslot) : "r"(slot), "r"(q));
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rbar) : "r"(bar), "r"(q));
-                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(rslot),
-                             "d"(gsum), "d"(rj), "r"(rbar)
-                             : "memory");
-            }
         }
-        {
+        __syncthreads();
+        if (wid < static_cast<int>(nr)) {
+            // warp q pushes the vector to CTA q (DSMEM store completing bytes on
+            // the peer's mbarrier): the 16 pushes leave in parallel
+            const double2 mv = *reinterpret_cast<const double2*>(&mine[p][2 * lane]);
+            const unsigned slot = static_cast<unsigned>(__cvta_generic_to_shared(&inbox[p][rank][2 * lane]));
+            unsigned rslot, rbar;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rslot) : "r"(slot), "r"(wid));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rbar) : "r"(bar), "r"(wid));
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(rslot),
+                         "d"(mv.x), "d"(mv.y), "r"(rbar)
+                         : "memory");
+        }
+        if (prof) prof[kk * 8 + 2] = clock64();
+        if (wid == 0) {
             unsigned ok = 0;
             do {
                 asm volatile(
@@ -395,16 +417,32 @@ __global__ void __launch_bounds__(kRegPanelThreads, 1) panel_reg_kernel(PanelArg
                     : "r"(bar), "r"(phase)
                     : "memory");
             } while (!ok);
+            if (prof) prof[kk * 8 + 3] = clock64();
+            // fixed pairwise tree over 16 slots (absent ranks add exact zeros), so
+            // every CTA obtains bit-identical sums; all 16 loads issue at once
+            double gv[16], rv[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                double2 pr = make_double2(0.0, 0.0);
+                if (q < static_cast<int>(nr)) pr = *reinterpret_cast<const double2*>(&inbox[p][q][2 * lane]);
+                gv[q] = pr.x;
+                rv[q] = pr.y;
+            }
+#pragma unroll
+            for (int w = 1; w < 16; w <<= 1)
+#pragma unroll
+                for (int q = 0; q < 16; q += 2 * w) {
+                    gv[q] += gv[q + w];
+                    rv[q] += rv[q + w];
+                }
+            *reinterpret_cast<double2*>(&tot[p][2 * lane]) = make_double2(gv[0], rv[0]);
         }
-        // every thread sums the inbox itself (rank order): no second barrier.  The
-        // buffer is safe to reuse two columns later: a peer can only push column
-        // kk+2 after this CTA pushed kk+1, i.e. after all its warps passed here.
-        double G = 0.0, R = 0.0;
-        for (unsigned q = 0; q < nr; ++q) {
-            const double2 pr = *reinterpret_cast<const double2*>(&inbox[p][q][2 * lane]);
-            G += pr.x;
-            R += pr.y;
-        }
+        // the inbox / mine / red buffers of parity p are reused two columns
+        // later: a peer can only push column kk+2 after this CTA pushed kk+1,
+        // i.e. after every warp here passed this barrier
+        __syncthreads();
+        const double2 gr = *reinterpret_cast<const double2*>(&tot[p][2 * lane]);
+        const double G = gr.x, R = gr.y;
         const double sigma = __shfl_sync(0xffffffffu, G, kk), x0 = __shfl_sync(0xffffffffu, R, kk);
         const double normx = sqrt(x0 * x0 + sigma);
         if (normx < rank_tol || normx == 0.0) {
@@ -414,8 +452,10 @@ __global__ void __launch_bounds__(kRegPanelThreads, 1) panel_reg_kernel(PanelArg
         }
         const double beta = (x0 > 0.0) ? -normx : normx;
         const double v0 = x0 - beta;
-        const double tau = (beta - x0) / beta;
-        const double rv0 = 1.0 / v0;
+        // branch-free reciprocals (hardware estimate + two Newton steps, within
+        // an ulp) instead of two IEEE divisions on the per-column critical path
+        const double tau = (beta - x0) * rcp_nr(beta);
+        const double rv0 = rcp_nr(v0);
         const double sdot = R + G * rv0;  // s_j (j > kk) or v_j^T v_kk (j < kk)
         const double sj = (lane > kk && lane < kb) ? sdot * tau : 0.0;
         const double cj = sj * rv0;       // w_ij -= tau s_j v_i = cj w_ik
@@ -426,6 +466,7 @@ __global__ void __launch_bounds__(kRegPanelThreads, 1) panel_reg_kernel(PanelArg
                 a.tau[a.k0 + kk] = tau;
             }
         }
+        if (prof) prof[kk * 8 + 4] = clock64();
         // apply H_kk to this thread's column and accumulate the next column's
         // partial G.  Rows past the slice are zero and stay zero, so only rank
         // 0's first two slots (rows < 32: finished rows of R, the diagonal row)
@@ -448,6 +489,7 @@ __global__ void __launch_bounds__(kRegPanelThreads, 1) panel_reg_kernel(PanelArg
             const double wn = __shfl_sync(0xffffffffu, nv, kn);
             if (acc) g = fma(nv, wn, g);
         }
+        if (prof) prof[kk * 8 + 5] = clock64();
     }
     __syncthreads();
     // compact-WY T by recursive doubling (dlarft): T[a:b, b:e] = -T11 (V1^T V2) T22,
@@ -1013,8 +1055,32 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
             const int64_t rpc = ceil_div(rows, cl);
             int rs = 2;
             while (rs * kRegWarps < rpc) rs *= 2;
-            PanelArgs pa{Yaug, ldy, d, k0, kb, rpc, rank_tol, tau, T + p * kNbMax * kNbMax, err};
+            PanelArgs pa{Yaug, ldy, d, k0, kb, rpc, rank_tol, tau, T + p * kNbMax * kNbMax, err, nullptr};
+            static const bool pprof = slq_env_flag("SLQ_PANEL_PROF");
+            DevBuf profbuf;
+            if (pprof && p == 1) {
+                pa.prof = static_cast<long long*>(profbuf.ensure(sizeof(long long) * 16 * 32 * 8));
+                SLQ_CUDA_CHECK(cudaMemsetAsync(pa.prof, 0, sizeof(long long) * 16 * 32 * 8, s_hi));
+            }
             launch_panel_reg(ctx, pa, cl, rs, s_hi);
+            if (pa.prof) {  // diagnostics: mean cycles per phase over columns, min/max over CTAs
+                std::vector<long long> h(16 * 32 * 8);
+                SLQ_CUDA_CHECK(cudaMemcpyAsync(h.data(), pa.prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, s_hi));
+                SLQ_CUDA_CHECK(cudaStreamSynchronize(s_hi));
+                static const char* names[5] = {"barrier", "reduce+push", "wait", "scalars", "update"};
+                std::fprintf(stderr, "[slq] panel %d (rows %lld, cluster %d, RS %d): cycles per column\n", int(p),
+                             (long long)rows, cl, rs);
+                for (int ph = 0; ph < 5; ++ph) {
+                    double mn = 1e30, mx = 0;
+                    for (int c = 0; c < cl; ++c) {
+                        double sum = 0;
+                        for (int k = 0; k < kb; ++k) sum += double(h[(c * 32 + k) * 8 + ph + 1] - h[(c * 32 + k) * 8 + ph]);
+                        mn = std::min(mn, sum / kb);
+                        mx = std::max(mx, sum / kb);
+                    }
+                    std::fprintf(stderr, "[slq]   %-12s min %8.0f max %8.0f\n", names[ph], mn, mx);
+                }
+            }
         } else {
             // very tall sketches: shared-memory panel (two reductions per column)
             cl = 1;
@@ -1022,7 +1088,7 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
             while (ceil_div(rows, cl) > max_rows_cta && cl < 16) cl *= 2;
             if (ceil_div(rows, cl) > max_rows_cta)
                 fail(SLQ_UNSUPPORTED, "householder_qr: sketch too tall for the panel kernel");
-            PanelArgs pa{Yaug, ldy, d, k0, kb, ceil_div(rows, cl), rank_tol, tau, T + p * kNbMax * kNbMax, err};
+            PanelArgs pa{Yaug, ldy, d, k0, kb, ceil_div(rows, cl), rank_tol, tau, T + p * kNbMax * kNbMax, err, nullptr};
             launch_panel(ctx, pa, cl, s_hi);
         }
         SLQ_CUDA_CHECK(cudaEventRecord(ev_p, s_hi));
