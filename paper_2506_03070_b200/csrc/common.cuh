@@ -79,7 +79,7 @@ struct Workspace {
     DevBuf yaug;         // Y_aug = [S A | S b], d x (n+1) column-major
     DevBuf flags;        // small device counters / error flags
     DevBuf staging[2];   // upload staging
-    DevBuf qr_t, qr_w, qr_w2, qr_q, qr_misc;
+    DevBuf qr_t, qr_w, qr_w2, qr_cnt, qr_cnt2, qr_q, qr_misc;
     DevBuf lsqr_vec, lsqr_part, lsqr_state, lsqr_u;
     DevBuf mats;         // M, Mt
     DevBuf xbuf;         // solution vector

@@ -573,6 +573,7 @@ __device__ __forceinline__ double vget(const UpdArgs& u, int64_t r, int a) {
 constexpr int kRB = 128;
 constexpr int kCB = 32;
 constexpr int kLdT = kRB + 4;  // smem leading dimension (doubles): conflict-free fragments
+constexpr int kWChunks = 1;    // row blocks per update_w CTA (more serialises the narrow update)
 
 // Stage V rows [r0, r0+kRB) (implicit unit diagonal / zero upper part) as Vs[a][i]
 __device__ __forceinline__ void stage_v(const UpdArgs& u, int64_t r0, double* Vs) {
@@ -592,30 +593,35 @@ __device__ __forceinline__ void stage_c(const UpdArgs& u, int64_t r0, int64_t c0
 }
 
 // U1: Wpart[rb][cb] = V_rb^T C_rb  (kNbMax x kCB)
-__global__ void __launch_bounds__(256) update_w_kernel(UpdArgs u, double* Wpart) {
+__global__ void __launch_bounds__(256) update_w_kernel(UpdArgs u, double* Wpart, int* counters, double* W2g) {
     extern __shared__ __align__(16) double sm[];
     double* Vs = sm;
     double* Cs = sm + kNbMax * kLdT;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int lr = lane & 3, lg = lane >> 2;
-    const int64_t r0 = u.k0 + static_cast<int64_t>(blockIdx.y) * kRB;
     const int64_t c0 = u.c_begin + static_cast<int64_t>(blockIdx.x) * kCB;
-    stage_v(u, r0, Vs);
-    stage_c(u, r0, c0, Cs);
-    __syncthreads();
     // 16 output tiles (4 along a, 4 along c); warp w owns tiles 2w, 2w+1
     double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     const int t0 = 2 * warp;
     const int at = t0 >> 2;  // both tiles share the a-tile
     const int ct0 = t0 & 3, ct1 = ct0 + 1;
+    // kWChunks row blocks of kRB rows per CTA (fewer partials to sum)
+    for (int ch = 0; ch < kWChunks; ++ch) {
+        const int64_t r0 = u.k0 + (static_cast<int64_t>(blockIdx.y) * kWChunks + ch) * kRB;
+        if (r0 >= u.r_end) break;
+        if (ch) __syncthreads();
+        stage_v(u, r0, Vs);
+        stage_c(u, r0, c0, Cs);
+        __syncthreads();
 #pragma unroll 8
-    for (int ks = 0; ks < kRB / 4; ++ks) {
-        const int i = ks * 4 + lr;
-        const double af = Vs[(at * 8 + lg) * kLdT + i];
-        const double b0 = Cs[(ct0 * 8 + lg) * kLdT + i];
-        const double b1 = Cs[(ct1 * 8 + lg) * kLdT + i];
-        dmma(acc[0][0], acc[0][1], af, b0);
-        dmma(acc[1][0], acc[1][1], af, b1);
+        for (int ks = 0; ks < kRB / 4; ++ks) {
+            const int i = ks * 4 + lr;
+            const double af = Vs[(at * 8 + lg) * kLdT + i];
+            const double b0 = Cs[(ct0 * 8 + lg) * kLdT + i];
+            const double b1 = Cs[(ct1 * 8 + lg) * kLdT + i];
+            dmma(acc[0][0], acc[0][1], af, b0);
+            dmma(acc[1][0], acc[1][1], af, b1);
+        }
     }
     double* W = Wpart + (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * (kNbMax * kCB);
     const int a = at * 8 + lg;
@@ -623,43 +629,50 @@ __global__ void __launch_bounds__(256) update_w_kernel(UpdArgs u, double* Wpart)
     W[a * kCB + ct0 * 8 + 2 * lr + 1] = acc[0][1];
     W[a * kCB + ct1 * 8 + 2 * lr] = acc[1][0];
     W[a * kCB + ct1 * 8 + 2 * lr + 1] = acc[1][1];
-}
-
-// U2: W = sum_rb Wpart[rb][cb] (fixed order);  W2[cb] = T^T W (or T W).
-// One CTA per column block, so the partials are summed once, not once per
-// row block of the apply.
-__global__ void __launch_bounds__(256) update_reduce_kernel(UpdArgs u, const double* Wpart, int nrb, double* W2g) {
-    __shared__ double W[kNbMax][kCB + 1];
-    __shared__ double Ts[kNbMax][kNbMax + 1];
+    // the last row-block CTA of this column block sums all partials in fixed
+    // order and applies T^T (or T): W2 = T^T sum_rb Wpart (no separate launch)
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int t = atomicAdd(&counters[blockIdx.x], 1);
+        s_last = (t == static_cast<int>(gridDim.y) - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double* Wsum = sm;                       // [kNbMax][kCB + 1]
+    double* Ts = sm + kNbMax * (kCB + 1);    // [kNbMax][kNbMax + 1]
     const int tid = threadIdx.x;
-    const int ncb = gridDim.x;
+    const int nrb = gridDim.y, ncb = gridDim.x;
     for (int e = tid; e < kNbMax * kCB; e += 256) {
         const double* src = Wpart + static_cast<int64_t>(blockIdx.x) * (kNbMax * kCB) + e;
         const int64_t step = static_cast<int64_t>(ncb) * (kNbMax * kCB);
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int rb = 0;
         for (; rb + 4 <= nrb; rb += 4) {
-            a0 += src[(rb + 0) * step];
-            a1 += src[(rb + 1) * step];
-            a2 += src[(rb + 2) * step];
-            a3 += src[(rb + 3) * step];
+            a0 += __ldcg(src + (rb + 0) * step);
+            a1 += __ldcg(src + (rb + 1) * step);
+            a2 += __ldcg(src + (rb + 2) * step);
+            a3 += __ldcg(src + (rb + 3) * step);
         }
-        for (; rb < nrb; ++rb) a0 += src[rb * step];
-        W[e / kCB][e % kCB] = (a0 + a1) + (a2 + a3);
+        for (; rb < nrb; ++rb) a0 += __ldcg(src + rb * step);
+        Wsum[(e / kCB) * (kCB + 1) + e % kCB] = (a0 + a1) + (a2 + a3);
     }
-    for (int e = tid; e < kNbMax * kNbMax; e += 256) Ts[e % kNbMax][e / kNbMax] = u.T[e];  // Ts[i][j] = T(i,j)
+    for (int e = tid; e < kNbMax * kNbMax; e += 256) Ts[(e % kNbMax) * (kNbMax + 1) + e / kNbMax] = u.T[e];
     __syncthreads();
     double* out = W2g + static_cast<int64_t>(blockIdx.x) * (kNbMax * kCB);
     for (int e = tid; e < kNbMax * kCB; e += 256) {
-        const int a = e / kCB, c = e % kCB;
-        double acc = 0.0;
+        const int ra = e / kCB, c = e % kCB;
+        double t = 0.0;
         if (u.transT) {
-            for (int b = 0; b <= a; ++b) acc += Ts[b][a] * W[b][c];
+            for (int b = 0; b <= ra; ++b) t += Ts[b * (kNbMax + 1) + ra] * Wsum[b * (kCB + 1) + c];
         } else {
-            for (int b = a; b < kNbMax; ++b) acc += Ts[a][b] * W[b][c];
+            for (int b = ra; b < kNbMax; ++b) t += Ts[ra * (kNbMax + 1) + b] * Wsum[b * (kCB + 1) + c];
         }
-        out[e] = acc;
+        out[e] = t;
     }
+    if (tid == 0) counters[blockIdx.x] = 0;  // ready for the next launch
 }
 
 // U3: C_rb -= V_rb W2[cb]
@@ -965,19 +978,30 @@ int max_panel_cluster() {
     return cached;
 }
 
-void launch_update(slq_ctx* ctx, const UpdArgs& u, cudaStream_t st, DevBuf& wbuf) {
+// zeroed completion counters of a trailing-update buffer (one per column block;
+// the last CTA of each column block resets its counter)
+int* update_counters(DevBuf& cnt, cudaStream_t st, int64_t ncb) {
+    const size_t need = sizeof(int) * static_cast<size_t>(std::max<int64_t>(ncb, 1024));
+    if (cnt.bytes < need) {
+        cnt.ensure(need);
+        SLQ_CUDA_CHECK(cudaMemsetAsync(cnt.p, 0, need, st));
+    }
+    return static_cast<int*>(cnt.p);
+}
+
+void launch_update(slq_ctx* ctx, const UpdArgs& u, cudaStream_t st, DevBuf& wbuf, DevBuf& cbuf) {
     if (u.c_end <= u.c_begin || u.r_end <= u.k0) return;
     const unsigned ncb = static_cast<unsigned>(ceil_div(u.c_end - u.c_begin, kCB));
     const unsigned nrb = static_cast<unsigned>(ceil_div(u.r_end - u.k0, kRB));
-    double* Wpart = static_cast<double*>(wbuf.ensure(sizeof(double) * kNbMax * kCB * ncb * (nrb + 1)));
-    double* W2 = Wpart + static_cast<int64_t>(kNbMax) * kCB * ncb * nrb;
+    const unsigned nwb = static_cast<unsigned>(ceil_div(nrb, kWChunks));  // update_w row groups (= partials)
+    double* Wpart = static_cast<double*>(wbuf.ensure(sizeof(double) * kNbMax * kCB * ncb * (nwb + 1)));
+    double* W2 = Wpart + static_cast<int64_t>(kNbMax) * kCB * ncb * nwb;
     const size_t sm1 = sizeof(double) * (kNbMax + kCB) * kLdT;
     const size_t sm2 = sm1 + sizeof(double) * kNbMax * (kCB + 1);
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(update_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm1)));
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(update_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2)));
-    update_w_kernel<<<dim3(ncb, nrb), 256, sm1, st>>>(u, Wpart);
-    SLQ_LAUNCH_CHECK(ctx);
-    update_reduce_kernel<<<ncb, 256, 0, st>>>(u, Wpart, static_cast<int>(nrb), W2);
+    int* counters = update_counters(cbuf, st, ncb);
+    update_w_kernel<<<dim3(ncb, nwb), 256, sm1, st>>>(u, Wpart, counters, W2);
     SLQ_LAUNCH_CHECK(ctx);
     update_apply_kernel<<<dim3(ncb, nrb), 256, sm2, st>>>(u, W2);
     SLQ_LAUNCH_CHECK(ctx);
@@ -1096,12 +1120,12 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
         if (k0 + kb < ncols) {
             if (w_pending) SLQ_CUDA_CHECK(cudaStreamWaitEvent(s_hi, ev_w, 0));  // W(p-1) on these columns
             UpdArgs un{Yaug, ldy, k0, kb, T + p * kNbMax * kNbMax, Yaug, ldy, k0 + kb, c_mid, d, 1};
-            launch_update(ctx, un, s_hi, ws.qr_w);
+            launch_update(ctx, un, s_hi, ws.qr_w, ws.qr_cnt);
         }
         if (c_mid < ncols) {
             SLQ_CUDA_CHECK(cudaStreamWaitEvent(s_lo, ev_p, 0));
             UpdArgs uw{Yaug, ldy, k0, kb, T + p * kNbMax * kNbMax, Yaug, ldy, c_mid, ncols, d, 1};
-            launch_update(ctx, uw, s_lo, ws.qr_w2);
+            launch_update(ctx, uw, s_lo, ws.qr_w2, ws.qr_cnt2);
             SLQ_CUDA_CHECK(cudaEventRecord(ev_w, s_lo));
             w_pending = true;
         }
@@ -1127,7 +1151,7 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
             const int64_t k0 = p * kNbMax;
             const int kb = static_cast<int>(std::min<int64_t>(kNbMax, n - k0));
             UpdArgs u{Yaug, ldy, k0, kb, T + p * kNbMax * kNbMax, Q, d, k0, n, d, 0};
-            launch_update(ctx, u, ctx->stream, ws.qr_w);
+            launch_update(ctx, u, ctx->stream, ws.qr_w, ws.qr_cnt);
         }
         scale_cols_kernel<<<static_cast<unsigned>(ceil_div(d * n, 256)), 256, 0, ctx->stream>>>(Q, d, n, sign);
         SLQ_LAUNCH_CHECK(ctx);
