@@ -109,11 +109,17 @@ void transpose_square(slq_ctx* ctx, const double* M, int64_t n, double* Mt) {
     SLQ_LAUNCH_CHECK(ctx);
 }
 
-// Host column-major block (m x n, lda) + optional b -> device layout.
+// Host column-major block (m x n, lda) + optional b -> device layout, in row
+// blocks double-buffered over a copy stream.  on_rows(r0, rows), if given, is
+// enqueued on the context stream after each block lands (the e2e path sketches
+// the block there while the next one is in flight); blocks are then multiples
+// of align rows.
 void upload_dense(slq_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, const double* b, double* dst,
-                  int64_t ld) {
+                  int64_t ld, const std::function<void(int64_t, int64_t)>& on_rows = {}, int64_t align = 32) {
     slq::Workspace& ws = ctx->ws;
-    const int64_t rows_cap = std::max<int64_t>(32, std::min<int64_t>(m, (int64_t(256) << 20) / (8 * std::max<int64_t>(n + 1, 1))));
+    int64_t rows_cap = std::max<int64_t>(32, std::min<int64_t>(m, (int64_t(256) << 20) / (8 * std::max<int64_t>(n + 1, 1))));
+    if (const char* e = std::getenv("SLQ_UPLOAD_ROWS")) rows_cap = std::max<int64_t>(1, std::atoll(e));  // diagnostics
+    if (align > 1) rows_cap = std::max<int64_t>(align, rows_cap / align * align);
     double* stg[2];
     for (int s = 0; s < 2; ++s) stg[s] = static_cast<double*>(ws.staging[s].ensure(sizeof(double) * rows_cap * (n + 1)));
     cudaStream_t cs;
@@ -143,6 +149,7 @@ void upload_dense(slq_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t l
                                                                    dst + r0 * ld, ld);
         SLQ_LAUNCH_CHECK(ctx);
         SLQ_CUDA_CHECK(cudaEventRecord(done[s], ctx->stream));
+        if (on_rows) on_rows(r0, rows);
     }
     SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     SLQ_CUDA_CHECK(cudaStreamSynchronize(cs));
@@ -246,6 +253,35 @@ Operand sparse_operand(slq_ctx* ctx, const slq_sparse* A) {
         slq::sketch_apply_sparse_dev(ctx, A, d, zeta, seed, Yaug);
     };
     o.make_op = [ctx, A] { return slq::make_sparse_op(ctx, A); };
+    return o;
+}
+
+// A still on the host (column-major, lda): the sketch uploads it block by block
+// into Ad's device storage and applies S to each block as it lands, so the
+// HBM-side work of the sketch hides behind the PCIe copy of the next block.
+Operand host_dense_operand(slq_ctx* ctx, slq_dense* Ad, const double* Ah, int64_t lda, const double* bh) {
+    Operand o;
+    o.m = Ad->m;
+    o.n = Ad->n;
+    o.sketch = [ctx, Ad, Ah, lda, bh](double* Yaug, int64_t d, int64_t zeta, uint64_t seed, Timer* t_gen) {
+        slq::Workspace& ws = ctx->ws;
+        const int64_t m = Ad->m;
+        uint32_t* compact = static_cast<uint32_t*>(ws.compact.ensure(sizeof(uint32_t) * std::max<int64_t>(1, m * zeta)));
+        int64_t* work = zeta > 32 ? static_cast<int64_t*>(ws.tmp.ensure(sizeof(int64_t) * m * zeta)) : nullptr;
+        slq::generate_sparse_sign_dev(ctx, d, zeta, seed, Ad->row_begin, m, compact, work, nullptr, nullptr, nullptr);
+        if (t_gen) SLQ_CUDA_CHECK(cudaEventRecord(t_gen->e, ctx->stream));
+        if (m == 0) {
+            SLQ_CUDA_CHECK(cudaMemsetAsync(Yaug, 0, sizeof(double) * d * (Ad->n + 1), ctx->stream));
+            return;
+        }
+        slq::DenseGather G = slq::dense_gather_plan(ctx, m, Ad->n, Ad->ld, d, compact, nullptr, zeta,
+                                                    1.0 / std::sqrt(static_cast<double>(zeta)), false, Yaug, true);
+        upload_dense(ctx, Ah, m, Ad->n, lda, bh, Ad->A, Ad->ld,
+                     [&](int64_t r0, int64_t rows) { slq::dense_gather_rows(ctx, G, Ad->A, r0, r0 + rows); },
+                     G.chunk_rows());
+        slq::dense_gather_finish(ctx, G);
+    };
+    o.make_op = [ctx, Ad] { return slq::make_dense_op(ctx, Ad); };
     return o;
 }
 
@@ -1096,10 +1132,11 @@ int slq_solve_host(slq_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t 
         Ad.owned = false;
         Ad.has_b = true;
         Ad.A = static_cast<double*>(ctx->ws.host_A.ensure(sizeof(double) * std::max<int64_t>(1, m * Ad.ld)));
-        if (m > 0) upload_dense(ctx, A, m, n, lda, b, Ad.A, Ad.ld);
     });
     if (st0 != SLQ_OK) return st0;
-    return run_solve(ctx, dense_operand(ctx, &Ad), d, zeta, seed, opts, x_out, report, times, residual_estimate);
+    // the upload happens inside the sketch phase, overlapped with it
+    return run_solve(ctx, host_dense_operand(ctx, &Ad, A, lda, b), d, zeta, seed, opts, x_out, report, times,
+                     residual_estimate);
 }
 
 }  // extern "C"

@@ -326,6 +326,8 @@ struct GatherArgs {
     double val;
     int64_t ldw;   // columns of Yw (>= ld, multiple of the slab width)
     double* Yw;    // [nsplit][ldw][d]
+    int64_t c_lo, c_hi;  // chunk range of this launch (split evenly over nsplit)
+    int accumulate;      // 1: y starts from Yw (nsplit == 1; incremental row ranges)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
@@ -387,8 +389,8 @@ __global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
     const int tid = threadIdx.x;
     const int64_t col0 = static_cast<int64_t>(blockIdx.x) * W;
     const int64_t split = blockIdx.y;
-    const int64_t cb = split * g.nchunks / g.nsplit;
-    const int64_t ce = (split + 1) * g.nchunks / g.nsplit;
+    const int64_t cb = g.c_lo + split * (g.c_hi - g.c_lo) / g.nsplit;
+    const int64_t ce = g.c_lo + (split + 1) * (g.c_hi - g.c_lo) / g.nsplit;
 
     const size_t a_bytes = static_cast<size_t>(g.K) * W * sizeof(double);
     const size_t p_bytes = g.ptr_stride * sizeof(uint16_t);
@@ -401,9 +403,11 @@ __global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
     const uint64_t vbits = static_cast<uint64_t>(__double_as_longlong(g.val));
     double y[RPT][W];
 #pragma unroll
-    for (int q = 0; q < RPT; ++q)
+    for (int q = 0; q < RPT; ++q) {
+        const int r = tid + q * kGThreads;
 #pragma unroll
-        for (int w = 0; w < W; ++w) y[q][w] = 0.0;
+        for (int w = 0; w < W; ++w) y[q][w] = (g.accumulate && r < g.d) ? g.Yw[(col0 + w) * g.d + r] : 0.0;
+    }
 
     if (cb < ce) stage_chunk<W>(g, col0, cb, As(0), Ps(0), Es(0));
     cp_commit();
@@ -966,62 +970,97 @@ void check_chunk_csr(slq_ctx* ctx, const ChunkCsr& cc) {
     if (hflag) fail(SLQ_UNSUPPORTED, "sketch_apply: a chunk exceeded 16384 sketch entries");
 }
 
-void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32_t* compact,
-                              const int64_t* colptr_dev, int64_t zeta, double val, bool exact,
-                              double* Y) {
-    const int64_t m = A->m, ld = A->ld, ncols_out = A->n + 1;
+DenseGather dense_gather_plan(slq_ctx* ctx, int64_t m, int64_t n, int64_t ld, int64_t d, const uint32_t* compact,
+                              const int64_t* colptr_dev, int64_t zeta, double val, bool exact, double* Y,
+                              bool incremental) {
     if (d > 16384) fail(SLQ_UNSUPPORTED, "sketch_apply: d > 16384 not supported");
     if (d >= (int64_t(1) << 21)) fail(SLQ_UNSUPPORTED, "sketch_apply: d too large for chunk keys");
     Workspace& ws = ctx->ws;
+    DenseGather G;
+    G.m = m;
+    G.d = d;
+    G.ld = ld;
+    G.ncols_out = n + 1;
+    G.val = val;
+    G.exact = exact;
+    G.Y = Y;
+    // W-column slab per CTA, all d rows of the slab in registers (32 doubles per
+    // thread: W = 4 up to d = 4096, W = 2 up to 8192, W = 1 up to 16384)
+    G.rpt = 1;
+    while (G.rpt * kGThreads < d) G.rpt <<= 1;
+    G.W = G.rpt <= 8 ? 4 : (G.rpt == 16 ? 2 : 1);
+    G.cc = build_chunk_csr(ctx, compact, colptr_dev, zeta, std::max<int64_t>(m, 1), d, G.W);
+    const ChunkPlan& cp = G.cc.plan;
+    G.ldw = round_up(ld, G.W);
+    G.nslabs = G.ldw / G.W;
+    // splits along m: balance waves over the SMs unless the exact serial order
+    // (or incremental row ranges) is asked for
+    G.nsplit = 1;
+    if (!exact && !incremental) {
+        double best = 1e30;
+        for (int64_t s = 1; s <= 16; ++s) {
+            if (s > cp.nchunks) break;
+            const int64_t ctas = G.nslabs * s;
+            const double waves = std::ceil(static_cast<double>(ctas) / ctx->num_sms);
+            const double cost = waves / s + 0.02 * s;  // per-split overhead (partials + reduce)
+            if (cost < best - 1e-9) {
+                best = cost;
+                G.nsplit = s;
+            }
+        }
+    }
+    G.Yw = (G.nsplit == 1 && G.ldw == G.ncols_out) ? Y
+           : static_cast<double*>(ws.ypart.ensure(sizeof(double) * G.nsplit * G.ldw * d));
+    G.smem = 2 * (static_cast<size_t>(cp.K) * G.W * sizeof(double) + cp.ptr_stride * sizeof(uint16_t) +
+                  cp.ent_stride * sizeof(uint16_t));
+    if (G.smem > 227 * 1024) fail(SLQ_UNSUPPORTED, "sketch_apply: stage exceeds shared memory");
+    return G;
+}
+
+void dense_gather_rows(slq_ctx* ctx, const DenseGather& G, const double* A, int64_t row_lo, int64_t row_hi) {
+    const ChunkPlan& cp = G.cc.plan;
+    const int64_t c_lo = row_lo / cp.K, c_hi = std::min(cp.nchunks, ceil_div(row_hi, static_cast<int64_t>(cp.K)));
+    if (c_hi <= c_lo) return;
+    if (row_lo % cp.K != 0 || (row_hi % cp.K != 0 && row_hi != G.m))
+        fail(SLQ_INVALID_ARG, "sketch_apply: row range not aligned to the chunk size");
+    GatherArgs g{A, G.ld, G.m, G.d, cp.K, cp.nchunks, G.nsplit, cp.ptr_stride, cp.ent_stride, G.cc.ptr, G.cc.ent,
+                 G.val, G.ldw, G.Yw, c_lo, c_hi, c_lo > 0 ? 1 : 0};
+    if (G.exact) launch_gather<true>(ctx, g, G.rpt, G.W, G.nslabs, G.smem);
+    else launch_gather<false>(ctx, g, G.rpt, G.W, G.nslabs, G.smem);
+}
+
+void dense_gather_finish(slq_ctx* ctx, const DenseGather& G) {
+    if (G.m == 0) {
+        SLQ_CUDA_CHECK(cudaMemsetAsync(G.Y, 0, sizeof(double) * G.d * G.ncols_out, ctx->stream));
+    } else if (G.Yw != G.Y) {
+        if (G.nsplit == 1) {  // same column-major layout: the first n+1 columns are contiguous
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(G.Y, G.Yw, sizeof(double) * G.d * G.ncols_out, cudaMemcpyDeviceToDevice,
+                                           ctx->stream));
+        } else {
+            const int64_t tot = G.d * G.ncols_out;
+            reduce_splits_kernel<<<static_cast<unsigned>(ceil_div(tot, 256)), 256, 0, ctx->stream>>>(
+                G.Yw, G.nsplit, G.d, G.ldw, G.ncols_out, G.Y);
+            SLQ_LAUNCH_CHECK(ctx);
+        }
+    }
+    check_chunk_csr(ctx, G.cc);
+}
+
+void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32_t* compact,
+                              const int64_t* colptr_dev, int64_t zeta, double val, bool exact,
+                              double* Y) {
+    const int64_t m = A->m;
     if (m == 0) {
-        SLQ_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(double) * d * ncols_out, ctx->stream));
+        SLQ_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(double) * d * (A->n + 1), ctx->stream));
         return;
     }
     // the cluster slab gather is exact without splits but, at zeta = 8 and
     // d = 4n, slower than the register-row gather (one entry per warp
     // instruction vs 32): opt-in for experiments only
     if (slq_env_flag("SLQ_SLAB_GATHER") && sketch_apply_slab(ctx, A, d, compact, colptr_dev, zeta, val, exact, Y)) return;
-    // W-column slab per CTA, all d rows of the slab in registers (32 doubles per
-    // thread: W = 4 up to d = 4096, W = 2 up to 8192, W = 1 up to 16384)
-    int rpt = 1;
-    while (rpt * kGThreads < d) rpt <<= 1;
-    const int W = rpt <= 8 ? 4 : (rpt == 16 ? 2 : 1);
-    ChunkCsr cc = build_chunk_csr(ctx, compact, colptr_dev, zeta, m, d, W);
-    const ChunkPlan& cp = cc.plan;
-    uint16_t* ptr = cc.ptr;
-    uint16_t* ent = cc.ent;
-    const int64_t ldw = round_up(ld, W);
-    const int64_t nslabs = ldw / W;
-    // splits along m: balance waves over the SMs unless the exact serial order is asked for
-    int64_t nsplit = 1;
-    if (!exact) {
-        double best = 1e30;
-        for (int64_t s = 1; s <= 16; ++s) {
-            if (s > cp.nchunks) break;
-            const int64_t ctas = nslabs * s;
-            const double waves = std::ceil(static_cast<double>(ctas) / ctx->num_sms);
-            const double cost = waves / s + 0.02 * s;  // per-split overhead (partials + reduce)
-            if (cost < best - 1e-9) {
-                best = cost;
-                nsplit = s;
-            }
-        }
-    }
-    double* Yw = (nsplit == 1 && ldw == ncols_out) ? Y
-                 : static_cast<double*>(ws.ypart.ensure(sizeof(double) * nsplit * ldw * d));
-    GatherArgs g{A->A, ld, m, d, cp.K, cp.nchunks, nsplit, cp.ptr_stride, cp.ent_stride, ptr, ent, val, ldw, Yw};
-    const size_t smem = 2 * (static_cast<size_t>(cp.K) * W * sizeof(double) + cp.ptr_stride * sizeof(uint16_t) +
-                             cp.ent_stride * sizeof(uint16_t));
-    if (smem > 227 * 1024) fail(SLQ_UNSUPPORTED, "sketch_apply: stage exceeds shared memory");
-    if (exact) launch_gather<true>(ctx, g, rpt, W, nslabs, smem);
-    else launch_gather<false>(ctx, g, rpt, W, nslabs, smem);
-    if (Yw != Y) {
-        const int64_t tot = d * ncols_out;
-        reduce_splits_kernel<<<static_cast<unsigned>(ceil_div(tot, 256)), 256, 0, ctx->stream>>>(
-            Yw, nsplit, d, ldw, ncols_out, Y);
-        SLQ_LAUNCH_CHECK(ctx);
-    }
-    check_chunk_csr(ctx, cc);
+    DenseGather G = dense_gather_plan(ctx, m, A->n, A->ld, d, compact, colptr_dev, zeta, val, exact, Y, false);
+    dense_gather_rows(ctx, G, A->A, 0, m);
+    dense_gather_finish(ctx, G);
 }
 
 void sketch_apply_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed,

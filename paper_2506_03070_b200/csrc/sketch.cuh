@@ -42,6 +42,27 @@ void generate_sparse_rows_dev(slq_ctx* ctx, int64_t n, int64_t nnz, uint64_t see
 void sketch_apply_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed,
                       bool exact, double* Y);
 
+// K2 in phases, for A arriving in row ranges (the host e2e path applies the
+// sketch to each uploaded block while the next one is in flight): plan (chunk-
+// CSR, slab width, Y workspace), gather of row ranges aligned to the chunk size
+// (later ranges accumulate onto earlier ones, in ascending row order), finish.
+struct DenseGather {
+    ChunkCsr cc;
+    int W = 4, rpt = 1;
+    int64_t m = 0, d = 0, ld = 0, ncols_out = 0, ldw = 0, nslabs = 0, nsplit = 1;
+    double val = 0.0;
+    bool exact = false;
+    double* Yw = nullptr;
+    double* Y = nullptr;
+    size_t smem = 0;
+    int chunk_rows() const { return cc.plan.K; }
+};
+DenseGather dense_gather_plan(slq_ctx* ctx, int64_t m, int64_t n, int64_t ld, int64_t d, const uint32_t* compact,
+                              const int64_t* colptr_dev, int64_t zeta, double val, bool exact, double* Y,
+                              bool incremental);
+void dense_gather_rows(slq_ctx* ctx, const DenseGather& G, const double* A, int64_t row_lo, int64_t row_hi);
+void dense_gather_finish(slq_ctx* ctx, const DenseGather& G);
+
 // K2 for a caller CSC sketch already in compact form on the device
 // (colptr_dev int64, may be null for uniform zeta) against device A.
 void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32_t* compact,

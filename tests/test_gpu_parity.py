@@ -296,3 +296,34 @@ def test_solve_pipeline_c1_small():
     # backward error no worse than the reference's at fixed T
     assert eta(x) <= max(2 * eta(xo), 1e-14)
     assert times["kernel_launches"] > 0
+
+
+@pytest.mark.parametrize("block_rows", [None, "5000"])
+def test_solve_host_streams_blocks(block_rows, monkeypatch):
+    """slq_solve_host (e2e path): A uploaded block by block from a column-major
+    host buffer with the sketch applied to each block as it lands; same solve as
+    the device-resident path up to summation order."""
+    import ctypes as ct
+    from paper_2506_03070_b200 import _capi as CA
+    if block_rows:
+        monkeypatch.setenv("SLQ_UPLOAD_ROWS", block_rows)  # several blocks (rounded to the chunk size)
+    rng = np.random.default_rng(8)
+    m, n, d, zeta, T = 30000, 40, 160, 8, 20
+    A = np.asfortranarray(rng.standard_normal((m, n)) @ np.diag(np.logspace(0, -3, n)))
+    b = rng.standard_normal(m)
+    ctx = slq.Context(0)
+    co = CA.SolveOpts()
+    CA.lib.slq_solve_opts_default(ct.byref(co))
+    co.eps, co.maxit, co.one_sync = 0.0, T, 1
+    x = np.zeros(n)
+    rep = CA.Report()
+    st = CA.lib.slq_solve_host(ctx.handle, A.ctypes.data_as(CA.dp), m, n, m, b.ctypes.data_as(CA.dp), 0, d, zeta, 5,
+                               ct.byref(co), x.ctypes.data_as(CA.dp), ct.byref(rep), None, None)
+    assert st == 0, CA.lib.slq_last_error()
+    xr, repr_, _ = slq.solve(slq.DeviceMatrix.from_numpy(A, b), d, zeta, 5, slq.SolveOptions(eps=0.0, maxit=T))
+    assert rep.iterations == repr_.iterations == T
+    assert np.linalg.norm(x - xr) <= 1e-9 * np.linalg.norm(xr)
+    Y, Sb = C.sketch_apply(d, zeta, 5, A, b)
+    M, Q = C.build_preconditioner(Y)
+    xo, _ = C.lsqr(A, M, b, C.initial_guess(M, Q, Sb), eps=0.0, maxit=T, one_sync=True)
+    assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)
