@@ -82,6 +82,23 @@ def device_algorithm_lsqr(Ak, bk, M, x0, maxit, counter):
     return x, hist
 
 
+def device_algorithm_hbm(Ak, bk, M, x0, alpha, beta, maxit, counter):
+    """Mirror of gd_dev (csrc/lsqr.cu): one pass per iteration gives
+    u_hat = A x - b and z = A^T u_hat (one allreduce of n values)."""
+    x, xp = x0.copy(), x0.copy()
+    hist = []
+    for _ in range(maxit):
+        uh = Ak @ x - bk
+        z = _allreduce(Ak.T @ uh)
+        counter[0] += 1
+        h = M.T @ (-z)
+        hist.append(np.linalg.norm(h))
+        g = M @ h
+        xn = x * (1.0 + beta) + (-beta) * xp + alpha * g
+        xp, x = x, xn
+    return x, hist
+
+
 def _worker(rank, world, port, results):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -120,8 +137,11 @@ def _worker(rank, world, port, results):
 
         counter = [0]
         x, hist = device_algorithm_lsqr(Ak, bk, M, x0, 10, counter)
+        gcount = [0]
+        alpha, beta = C.gradient_params(float(np.sqrt(n / d)), True)
+        xg, ghist = device_algorithm_hbm(Ak, bk, M, x0, alpha, beta, 12, gcount)
         results[rank] = {"Y": Y, "Sb": Sb, "x": x, "hist": np.array(hist), "allreduces": counter[0],
-                         "M": M, "x0": x0}
+                         "M": M, "x0": x0, "xg": xg, "ghist": np.array(ghist), "g_allreduces": gcount[0]}
     finally:
         dist.destroy_process_group()
 
@@ -150,6 +170,16 @@ def test_row_partitioned_pipeline_gloo_world2():
         assert np.allclose(res["hist"], rep.residual_estimate, rtol=1e-8)
         # one reduction per iteration + one at init (the reference's one-sync count)
         assert res["allreduces"] == 10 + 1
+    # heavy ball over the same decomposition: one allreduce per iteration
+    # (the reference's dist HBM counts one reduction per iteration, test_distsim.cpp:282)
+    a, bb = C.gradient_params(float(np.sqrt(n / d)), True)
+    xgs, greps = C.gd_hbm(A, M, b, x0, a, bb, eps=0.0, maxit=12)
+    for r in range(world):
+        res = results[r]
+        assert np.linalg.norm(res["xg"] - xgs) <= 1e-10 * max(1.0, np.linalg.norm(xgs))
+        assert np.allclose(res["ghist"], greps.residual_estimate, rtol=1e-9)
+        assert res["g_allreduces"] == 12
+    assert np.array_equal(results[0]["xg"], results[1]["xg"])
     # replicated state is bitwise identical on every rank (allreduce/broadcast semantics)
     assert np.array_equal(results[0]["x"], results[1]["x"])
     assert np.array_equal(results[0]["M"], results[1]["M"])
