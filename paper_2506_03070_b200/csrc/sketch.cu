@@ -20,8 +20,11 @@
 // split reproduces the reference Y bit for bit.  No atomics anywhere.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "ptx.cuh"
 #include "rng.cuh"
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(1024) bucketize_kernel(BucketArgs a) {
         // (W = 4: the first 16-byte half, the second at offset ^ 16) with the
         // sign in bit 0, so the gather decodes an entry with a few logic ops
         const int kl = static_cast<int>(kv >> 1);
-        const uint32_t off = a.slots == 4 ? static_cast<uint32_t>(gslot(kl, 0)) << 4
+        const uint32_t off = a.slots == 4 ? static_cast<uint32_t>(kl) << 5
                              : a.slots == 2 ? static_cast<uint32_t>(kl) << 4
                                             : static_cast<uint32_t>(kl) << 3;
         ent[i] = a.slots ? static_cast<uint16_t>(off | (kv & 1u)) : static_cast<uint16_t>(kv);
@@ -313,7 +316,7 @@ __global__ void __launch_bounds__(1024) bucketize_kernel(BucketArgs a) {
 
 // ---------------------------------------------------------------- K2 gather
 
-constexpr int kGThreads = 512;
+constexpr int kGThreads = 1024;
 
 struct GatherArgs {
     const double* A;  // row-major block, row 0 = local row 0
@@ -384,8 +387,15 @@ __device__ __forceinline__ double acc_step(double y, double v, double a) {
 // entries in ascending k -- the reference's order -- gathering 32 bytes of A
 // per entry.
 template <int RPT, int W, bool EXACT>
-__global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
-    extern __shared__ __align__(16) unsigned char smem[];
+__global__ void __launch_bounds__(kGThreads, 1) gather_kernel(const __grid_constant__ CUtensorMap tmap, GatherArgs g) {
+    // W >= 2: the A slab of a chunk arrives by TMA (2D tensor map over the
+    // row-major A, boxes of 256 rows x W columns) and the chunk's row pointers
+    // and entries by 1D bulk copies, all issued by one thread and completing on
+    // the stage's mbarrier; W == 1 (8-byte rows, below the TMA box minimum)
+    // stages with cp.async.
+    constexpr bool kTma = W >= 2;
+    extern __shared__ __align__(128) unsigned char gsmem[];
+    __shared__ __align__(8) uint64_t full[2];
     const int tid = threadIdx.x;
     const int64_t col0 = static_cast<int64_t>(blockIdx.x) * W;
     const int64_t split = blockIdx.y;
@@ -395,10 +405,32 @@ __global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
     const size_t a_bytes = static_cast<size_t>(g.K) * W * sizeof(double);
     const size_t p_bytes = g.ptr_stride * sizeof(uint16_t);
     const size_t e_bytes = g.ent_stride * sizeof(uint16_t);
-    const size_t st_bytes = a_bytes + p_bytes + e_bytes;
-    auto As = [&](int s) { return reinterpret_cast<double*>(smem + s * st_bytes); };
-    auto Ps = [&](int s) { return reinterpret_cast<uint16_t*>(smem + s * st_bytes + a_bytes); };
-    auto Es = [&](int s) { return reinterpret_cast<uint16_t*>(smem + s * st_bytes + a_bytes + p_bytes); };
+    const size_t st_bytes = (a_bytes + p_bytes + e_bytes + 127) & ~size_t(127);
+    auto As = [&](int s) { return reinterpret_cast<double*>(gsmem + s * st_bytes); };
+    auto Ps = [&](int s) { return reinterpret_cast<uint16_t*>(gsmem + s * st_bytes + a_bytes); };
+    auto Es = [&](int s) { return reinterpret_cast<uint16_t*>(gsmem + s * st_bytes + a_bytes + p_bytes); };
+
+    if (kTma && tid == 0) {
+        ptx::mbar_init(&full[0], 1);
+        ptx::mbar_init(&full[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int64_t c, int s) {  // thread 0: TMA the chunk into stage s
+        const int64_t k0 = c * g.K;
+        const int kc = static_cast<int>(min(static_cast<int64_t>(g.K), g.m - k0));
+        const int nbox = (kc + 255) >> 8;
+        ptx::mbar_expect_tx(&full[s], static_cast<unsigned>(nbox * 256 * W * 8 + p_bytes + e_bytes));
+        for (int bx = 0; bx < nbox; ++bx) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+                    ptx::smem_u32(As(s) + static_cast<size_t>(bx) * 256 * W)),
+                "l"(&tmap), "r"(static_cast<int>(col0)), "r"(static_cast<int>(k0 + 256 * bx)), "r"(ptx::smem_u32(&full[s]))
+                : "memory");
+        }
+        ptx::bulk_g2s(Ps(s), g.ptr + c * g.ptr_stride, static_cast<unsigned>(p_bytes), &full[s]);
+        ptx::bulk_g2s(Es(s), g.ent + c * g.ent_stride, static_cast<unsigned>(e_bytes), &full[s]);
+    };
 
     const uint64_t vbits = static_cast<uint64_t>(__double_as_longlong(g.val));
     double y[RPT][W];
@@ -409,14 +441,25 @@ __global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
         for (int w = 0; w < W; ++w) y[q][w] = (g.accumulate && r < g.d) ? g.Yw[(col0 + w) * g.d + r] : 0.0;
     }
 
-    if (cb < ce) stage_chunk<W>(g, col0, cb, As(0), Ps(0), Es(0));
-    cp_commit();
+    if (cb < ce) {
+        if (kTma) {
+            if (tid == 0) issue(cb, 0);
+        } else {
+            stage_chunk<W>(g, col0, cb, As(0), Ps(0), Es(0));
+        }
+    }
+    if (!kTma) cp_commit();
     for (int64_t c = cb; c < ce; ++c) {
         const int s = static_cast<int>((c - cb) & 1);
-        if (c + 1 < ce) stage_chunk<W>(g, col0, c + 1, As(s ^ 1), Ps(s ^ 1), Es(s ^ 1));
-        cp_commit();
-        cp_wait<1>();
-        __syncthreads();
+        if (kTma) {
+            if (tid == 0 && c + 1 < ce) issue(c + 1, s ^ 1);  // stage s^1 was released by the last barrier
+            ptx::mbar_wait(&full[s], static_cast<unsigned>(((c - cb) >> 1) & 1));
+        } else {
+            if (c + 1 < ce) stage_chunk<W>(g, col0, c + 1, As(s ^ 1), Ps(s ^ 1), Es(s ^ 1));
+            cp_commit();
+            cp_wait<1>();
+            __syncthreads();
+        }
         const unsigned char* A_b = reinterpret_cast<const unsigned char*>(As(s));
         const uint16_t* P_s = Ps(s);
         const uint16_t* E_s = Es(s);
@@ -448,7 +491,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gather_kernel(GatherArgs g) {
         }
         __syncthreads();
     }
-    cp_wait<0>();
+    if (!kTma) cp_wait<0>();
     double* Y = g.Yw + split * g.ldw * g.d;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
@@ -798,26 +841,53 @@ ChunkPlan plan_chunks(int64_t m, int64_t d, int64_t zeta_max, int W) {
     return p;
 }
 
+// 2D tensor map over the row-major A block (inner dim = ld columns, outer = m
+// rows), boxes of 256 rows x W columns, no swizzle (the gather's entries hold
+// plain byte offsets k * 8W).
+CUtensorMap gather_tensor_map(const double* A, int64_t ld, int64_t m, int W) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        SLQ_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn) fail(SLQ_CUDA, "cuTensorMapEncodeTiled not available");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    if (W < 2) return map;  // 1-column slabs stage with cp.async
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(std::max<int64_t>(m, 1))};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(double)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(W), 256u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(SLQ_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+    return map;
+}
+
 template <int RPT, int W, bool EXACT>
 void launch_gather_t(slq_ctx* ctx, const GatherArgs& g, int64_t nslabs, size_t smem) {
     auto kern = gather_kernel<RPT, W, EXACT>;
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    const CUtensorMap map = gather_tensor_map(g.A, g.ld, g.m, W);
     dim3 grid(static_cast<unsigned>(nslabs), static_cast<unsigned>(g.nsplit));
-    kern<<<grid, kGThreads, smem, ctx->stream>>>(g);
+    kern<<<grid, kGThreads, smem, ctx->stream>>>(map, g);
     SLQ_LAUNCH_CHECK(ctx);
 }
 
+// slab width W and rows per thread: y holds RPT x W = 16 doubles per thread
 template <bool EXACT>
 void launch_gather(slq_ctx* ctx, const GatherArgs& g, int rpt, int W, int64_t nslabs, size_t smem) {
     switch (rpt) {
         case 1: launch_gather_t<1, 4, EXACT>(ctx, g, nslabs, smem); break;
         case 2: launch_gather_t<2, 4, EXACT>(ctx, g, nslabs, smem); break;
         case 4: launch_gather_t<4, 4, EXACT>(ctx, g, nslabs, smem); break;
-        case 8: launch_gather_t<8, 4, EXACT>(ctx, g, nslabs, smem); break;
-        case 16: launch_gather_t<16, 2, EXACT>(ctx, g, nslabs, smem); break;  // 4096 < d <= 8192: 2-column slabs
-        case 32: launch_gather_t<32, 1, EXACT>(ctx, g, nslabs, smem); break;  // d <= 16384: 1-column slabs
+        case 8: launch_gather_t<8, 2, EXACT>(ctx, g, nslabs, smem); break;   // 4096 < d <= 8192: 2-column slabs
+        case 16: launch_gather_t<16, 1, EXACT>(ctx, g, nslabs, smem); break; // d <= 16384: 1-column slabs
         default: fail(SLQ_UNSUPPORTED, "sketch_apply: d > 16384 not supported by the register-slab gather");
     }
+    (void)W;
 }
 
 template <int RW, bool EXACT>
@@ -988,7 +1058,7 @@ DenseGather dense_gather_plan(slq_ctx* ctx, int64_t m, int64_t n, int64_t ld, in
     // thread: W = 4 up to d = 4096, W = 2 up to 8192, W = 1 up to 16384)
     G.rpt = 1;
     while (G.rpt * kGThreads < d) G.rpt <<= 1;
-    G.W = G.rpt <= 8 ? 4 : (G.rpt == 16 ? 2 : 1);
+    G.W = G.rpt <= 4 ? 4 : (G.rpt == 8 ? 2 : 1);
     G.cc = build_chunk_csr(ctx, compact, colptr_dev, zeta, std::max<int64_t>(m, 1), d, G.W);
     const ChunkPlan& cp = G.cc.plan;
     G.ldw = round_up(ld, G.W);
@@ -1011,8 +1081,8 @@ DenseGather dense_gather_plan(slq_ctx* ctx, int64_t m, int64_t n, int64_t ld, in
     }
     G.Yw = (G.nsplit == 1 && G.ldw == G.ncols_out) ? Y
            : static_cast<double*>(ws.ypart.ensure(sizeof(double) * G.nsplit * G.ldw * d));
-    G.smem = 2 * (static_cast<size_t>(cp.K) * G.W * sizeof(double) + cp.ptr_stride * sizeof(uint16_t) +
-                  cp.ent_stride * sizeof(uint16_t));
+    G.smem = 2 * round_up(static_cast<int64_t>(cp.K) * G.W * sizeof(double) + cp.ptr_stride * sizeof(uint16_t) +
+                              cp.ent_stride * sizeof(uint16_t), 128);
     if (G.smem > 227 * 1024) fail(SLQ_UNSUPPORTED, "sketch_apply: stage exceeds shared memory");
     return G;
 }
