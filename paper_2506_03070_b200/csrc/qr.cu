@@ -718,6 +718,131 @@ __global__ void __launch_bounds__(256) update_apply_kernel(UpdArgs u, const doub
     }
 }
 
+// N(p): the next panel's <= kCB columns, C <- C - V T^T (V^T C), in ONE launch.
+// This update sits on the panel chain's critical path (panel(p) -> N(p) ->
+// panel(p+1)), so instead of the two-kernel grid update (partials in global
+// memory, last-CTA reduce, second launch) one thread-block cluster owns all
+// rows: each CTA stages its rows of V and C once, forms its partial V^T C on
+// DMMA, the partials are summed over DSMEM in fixed rank order (every CTA
+// redundantly, deterministic), T^T is applied, and the CTA updates the staged
+// C rows from shared memory.
+constexpr int kNRB = 256;        // rows per staged chunk
+constexpr int kNLd = kNRB + 4;   // conflict-free fragment loads (as kLdT)
+constexpr size_t kNarrowSmem = sizeof(double) * (2 * kNbMax * kNLd + kNbMax * kCB + 3 * kNbMax * (kCB + 1));
+
+__global__ void __launch_bounds__(256) narrow_update_kernel(UpdArgs u, int64_t rpc) {
+    static_assert(kNbMax == kCB, "V and C tiles share the staging loop");
+    extern __shared__ __align__(16) double sm[];
+    double* Vs = sm;                          // [a][i], kNLd
+    double* Cs = Vs + kNbMax * kNLd;          // [c][i], kNLd
+    double* Wp = Cs + kCB * kNLd;             // [a][c] this CTA's partial V^T C (read remotely)
+    double* Ws = Wp + kNbMax * kCB;           // [a][kCB + 1] cluster sum
+    double* W2 = Ws + kNbMax * (kCB + 1);     // [a][kCB + 1] T^T Ws
+    double* Ts = W2 + kNbMax * (kCB + 1);     // [b][kNbMax + 1]
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = static_cast<int>(cluster.block_rank());
+    const int ncta = static_cast<int>(cluster.num_blocks());
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lr = lane & 3, lg = lane >> 2;
+    const int64_t rbeg = u.k0 + rank * rpc;
+    const int64_t rend = (rbeg + rpc < u.r_end) ? rbeg + rpc : u.r_end;
+    const int64_t nrows = rend > rbeg ? rend - rbeg : 0;
+    const int nch = static_cast<int>((nrows + kNRB - 1) / kNRB);
+    const int64_t c0 = u.c_begin;
+    auto stage = [&](int64_t r0) {
+        for (int e = tid; e < kNbMax * kNRB; e += 256) {
+            const int a = e / kNRB, i = e % kNRB;
+            const int64_t r = r0 + i;
+            double v = 0.0, c = 0.0;
+            if (r < rend) {
+                v = vget(u, r, a);
+                if (c0 + a < u.c_end) c = u.C[(c0 + a) * u.ldc + r];
+            }
+            Vs[a * kNLd + i] = v;
+            Cs[a * kNLd + i] = c;
+        }
+    };
+    for (int e = tid; e < kNbMax * kNbMax; e += 256) Ts[(e % kNbMax) * (kNbMax + 1) + e / kNbMax] = u.T[e];
+    // phase 1: Wp = V^T C over this CTA's rows (16 8x8 tiles, two per warp)
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    const int t0 = 2 * warp, at = t0 >> 2, ct0 = t0 & 3, ct1 = ct0 + 1;
+    for (int ch = 0; ch < nch; ++ch) {
+        const int64_t r0 = rbeg + static_cast<int64_t>(ch) * kNRB;
+        const int rows = static_cast<int>(rend - r0 < kNRB ? rend - r0 : kNRB);
+        if (ch) __syncthreads();
+        stage(r0);
+        __syncthreads();
+        const int nks = (rows + 3) >> 2;
+        for (int ks = 0; ks < nks; ++ks) {
+            const int i = ks * 4 + lr;
+            const double af = Vs[(at * 8 + lg) * kNLd + i];
+            const double b0 = Cs[(ct0 * 8 + lg) * kNLd + i];
+            const double b1 = Cs[(ct1 * 8 + lg) * kNLd + i];
+            dmma(acc[0][0], acc[0][1], af, b0);
+            dmma(acc[1][0], acc[1][1], af, b1);
+        }
+    }
+    {
+        const int a = at * 8 + lg;
+        Wp[a * kCB + ct0 * 8 + 2 * lr] = acc[0][0];
+        Wp[a * kCB + ct0 * 8 + 2 * lr + 1] = acc[0][1];
+        Wp[a * kCB + ct1 * 8 + 2 * lr] = acc[1][0];
+        Wp[a * kCB + ct1 * 8 + 2 * lr + 1] = acc[1][1];
+    }
+    cluster.sync();
+    // cluster sum in fixed rank order, then W2 = T^T Ws
+    for (int e = tid; e < kNbMax * kCB; e += 256) {
+        double s = 0.0;
+        for (int q = 0; q < ncta; ++q) s += cluster.map_shared_rank(Wp, q)[e];
+        Ws[(e / kCB) * (kCB + 1) + e % kCB] = s;
+    }
+    __syncthreads();
+    for (int e = tid; e < kNbMax * kCB; e += 256) {
+        const int ra = e / kCB, c = e % kCB;
+        double t = 0.0;
+        if (u.transT) {
+            for (int b = 0; b <= ra; ++b) t += Ts[b * (kNbMax + 1) + ra] * Ws[b * (kCB + 1) + c];
+        } else {
+            for (int b = ra; b < kNbMax; ++b) t += Ts[ra * (kNbMax + 1) + b] * Ws[b * (kCB + 1) + c];
+        }
+        W2[ra * (kCB + 1) + c] = t;
+    }
+    // phase 2: C_rows -= V_rows W2 (the single chunk is still staged)
+    for (int ch = 0; ch < nch; ++ch) {
+        const int64_t r0 = rbeg + static_cast<int64_t>(ch) * kNRB;
+        const int rows = static_cast<int>(rend - r0 < kNRB ? rend - r0 : kNRB);
+        if (nch > 1) {
+            __syncthreads();
+            stage(r0);
+        }
+        __syncthreads();
+        const int nrt = (rows + 7) >> 3;
+        for (int rt = warp; rt < nrt; rt += 8) {
+            double d[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+            for (int ks = 0; ks < kNbMax / 4; ++ks) {
+                const double af = Vs[(ks * 4 + lr) * kNLd + rt * 8 + lg];
+#pragma unroll
+                for (int ct = 0; ct < 4; ++ct) {
+                    const double bf = W2[(ks * 4 + lr) * (kCB + 1) + ct * 8 + lg];
+                    dmma(d[ct][0], d[ct][1], af, bf);
+                }
+            }
+            const int64_t r = r0 + rt * 8 + lg;
+            if (r < rend) {
+#pragma unroll
+                for (int ct = 0; ct < 4; ++ct)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int cl = ct * 8 + 2 * lr + e;
+                        if (c0 + cl < u.c_end) u.C[(c0 + cl) * u.ldc + r] = Cs[cl * kNLd + rt * 8 + lg] - d[ct][e];
+                    }
+            }
+        }
+    }
+    cluster.sync();  // peers may still be reading this CTA's Wp
+}
+
 // R = triu(Y[0:n,0:n]) with the diag >= 0 flip (qr.hpp:79-86); flips the
 // transformed Sb column (Q^T Sb) and records the signs.
 __global__ void extract_r_kernel(const double* Y, int64_t ldy, int64_t n, double* R, double* sign,
@@ -1007,6 +1132,65 @@ void launch_update(slq_ctx* ctx, const UpdArgs& u, cudaStream_t st, DevBuf& wbuf
     SLQ_LAUNCH_CHECK(ctx);
 }
 
+// one-cluster narrow update (N(p)); falls back to the grid update when no
+// cluster shape fits (cluster of 16 needs a GPC with 16 free SMs)
+int narrow_cluster_max() {
+    static int cached = -1;
+    if (cached >= 0) return cached;
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(narrow_update_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(narrow_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kNarrowSmem)));
+    cached = 0;
+    for (int cl = 16; cl >= 1 && !cached; cl /= 2) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cl, 1, 1);
+        cfg.blockDim = dim3(256, 1, 1);
+        cfg.dynamicSmemBytes = kNarrowSmem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cl;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, narrow_update_kernel, &cfg) != cudaSuccess) {
+            (void)cudaGetLastError();
+            nclusters = 0;
+        }
+        if (nclusters > 0) cached = cl;
+    }
+    return cached;
+}
+
+void launch_narrow(slq_ctx* ctx, const UpdArgs& u, cudaStream_t st, DevBuf& wbuf, DevBuf& cbuf) {
+    if (u.c_end <= u.c_begin || u.r_end <= u.k0) return;
+    static const bool grid_only = slq_env_flag("SLQ_QR_GRID_NARROW");  // diagnostics: old two-kernel path
+    const int clmax = grid_only ? 0 : narrow_cluster_max();
+    if (clmax == 0 || u.c_end - u.c_begin > kCB) {
+        launch_update(ctx, u, st, wbuf, cbuf);
+        return;
+    }
+    const int64_t rows = u.r_end - u.k0;
+    int cl = 1;
+    while (ceil_div(rows, cl) > kNRB && cl < clmax) cl *= 2;
+    const int64_t rpc = ceil_div(ceil_div(rows, cl), 8) * 8;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl, 1, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = kNarrowSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SLQ_CUDA_CHECK(cudaLaunchKernelEx(&cfg, narrow_update_kernel, u, rpc));
+    ctx->launches++;
+}
+
 // the context's two QR streams (created on first use, high / low priority) and events
 void qr_streams(slq_ctx* ctx, cudaStream_t& hi, cudaStream_t& lo, cudaEvent_t& ev_p, cudaEvent_t& ev_w,
                 cudaEvent_t& ev_0) {
@@ -1049,7 +1233,8 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
     SLQ_LAUNCH_CHECK(ctx);
 
     // Look-ahead schedule (depth 1) on two streams: s_hi runs the panels and the
-    // narrow update N(p) of the next panel's 32 columns, s_lo the wide update
+    // narrow update N(p) of the next panel's 32 columns (one cluster launch,
+    // narrow_update_kernel), s_lo the wide update
     // W(p) of every column after it.  W(p-1) then overlaps panel(p):
     //   s_hi: panel(p) -> [ev_p] -> wait W(p-1) -> N(p) -> panel(p+1) ...
     //   s_lo: wait ev_p -> W(p) -> [ev_w]
@@ -1120,7 +1305,7 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
         if (k0 + kb < ncols) {
             if (w_pending) SLQ_CUDA_CHECK(cudaStreamWaitEvent(s_hi, ev_w, 0));  // W(p-1) on these columns
             UpdArgs un{Yaug, ldy, k0, kb, T + p * kNbMax * kNbMax, Yaug, ldy, k0 + kb, c_mid, d, 1};
-            launch_update(ctx, un, s_hi, ws.qr_w, ws.qr_cnt);
+            launch_narrow(ctx, un, s_hi, ws.qr_w, ws.qr_cnt);
         }
         if (c_mid < ncols) {
             SLQ_CUDA_CHECK(cudaStreamWaitEvent(s_lo, ev_p, 0));
