@@ -313,6 +313,11 @@ int slq_solve_sparse(slq_ctx* ctx, const slq_sparse* A, int64_t d, int64_t zeta,
 int slq_time_kernels(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed, int reps,
                      double* out);
 
+/* Benchmark helper (no reference counterpart): average device seconds of one
+ * K4s launch -- the sparse LSQR pass u_hat = A p + c u, z = A^T u_hat,
+ * ||u_hat||^2 -- over `reps` launches on the context stream (CUDA events). */
+int slq_time_sparse_pass(slq_ctx* ctx, const slq_sparse* A, int reps, double* seconds);
+
 /* slq_solve from host buffers: upload (column-major A, lda) + solve + free. */
 int slq_solve_host(slq_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda,
                    const double* b, int64_t row_begin, int64_t d, int64_t zeta, uint64_t seed,

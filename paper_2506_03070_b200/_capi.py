@@ -136,6 +136,7 @@ _SIGS = {
     "slq_gradient_descent_hbm_sparse": (ct.c_int, [vp, vp, dp, dp, dp, ct.POINTER(GradientParams),
                                                    ct.POINTER(SolveOpts), dp, ct.POINTER(Report), dp, dp, dp]),
     "slq_time_kernels": (ct.c_int, [vp, vp, i64, i64, u64, ct.c_int, dp]),
+    "slq_time_sparse_pass": (ct.c_int, [vp, vp, ct.c_int, dp]),
     "slq_solve_host": (ct.c_int, [vp, dp, i64, i64, i64, dp, i64, i64, i64, u64, ct.POINTER(SolveOpts), dp,
                                   ct.POINTER(Report), ct.POINTER(PhaseTimes), dp]),
 }

@@ -1111,6 +1111,14 @@ int slq_time_kernels(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, 
     });
 }
 
+int slq_time_sparse_pass(slq_ctx* ctx, const slq_sparse* A, int reps, double* seconds) {
+    return guarded([&] {
+        need(ctx && A && seconds, SLQ_INVALID_ARG, "time_sparse_pass: null argument");
+        SLQ_CUDA_CHECK(cudaSetDevice(ctx->device));
+        *seconds = slq::time_fused_pass(ctx, *slq::make_sparse_op(ctx, A), reps);
+    });
+}
+
 int slq_solve_host(slq_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t lda, const double* b,
                    int64_t row_begin, int64_t d, int64_t zeta, uint64_t seed, const slq_solve_opts* opts,
                    double* x_out, slq_report* report, slq_phase_times* times, double* residual_estimate) {

@@ -1105,10 +1105,10 @@ double time_fused_pass(slq_ctx* ctx, const PassOp& op, int reps) {
     DevBuf part, pv, uv, cf;
     double* dpart = static_cast<double*>(part.ensure(sizeof(double) * op.grid() * (n + 1)));
     double* p = static_cast<double*>(pv.ensure(sizeof(double) * (n + 8)));
-    double* u = static_cast<double*>(uv.ensure(sizeof(double) * std::max<int64_t>(1, m)));
+    double* u = static_cast<double*>(uv.ensure(sizeof(double) * (m + kSparseRowPad)));  // slack for tile copies
     double* c = static_cast<double*>(cf.ensure(sizeof(double) * 8));
     SLQ_CUDA_CHECK(cudaMemsetAsync(p, 0, sizeof(double) * (n + 8), ctx->stream));
-    SLQ_CUDA_CHECK(cudaMemsetAsync(u, 0, sizeof(double) * std::max<int64_t>(1, m), ctx->stream));
+    SLQ_CUDA_CHECK(cudaMemsetAsync(u, 0, sizeof(double) * (m + kSparseRowPad), ctx->stream));
     SLQ_CUDA_CHECK(cudaMemsetAsync(c, 0, sizeof(double) * 8, ctx->stream));
     const PassCall call{p, u, u, c, 0.0, dpart, 1, nullptr};
     op.pass(ctx, call);  // warm

@@ -14,9 +14,9 @@
 //        warp per Y row keeps the row (n+1 doubles) in shared memory and adds
 //        s * A[k, :] for its entries in ascending k -- the reference's
 //        accumulation order (bit-identical), no atomics.
-//   K4s  one pass per LSQR iteration: row tiles (column indices, values, row
-//        pointers, u) arrive by TMA bulk copy into a 3-stage mbarrier ring; a
-//        warp per row computes u_hat = A_i p + c u_i (p in shared memory) and
+//   K4s  one pass per LSQR iteration: a warp takes quads of 4 rows, loads
+//        their column indices and values straight into registers (three quads
+//        in flight), computes u_hat = A_i p + c u_i (p in shared memory) and
 //        scatters z += A_i^T u_hat into a warp-private copy of z in shared
 //        memory (column indices within a row are distinct: no races, no
 //        atomics); the copies are summed in a fixed order at the end.

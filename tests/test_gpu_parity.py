@@ -155,7 +155,11 @@ def _rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
-@pytest.mark.parametrize("d,n", [(96, 24), (400, 100), (130, 33), (1000, 250), (64, 64), (2000, 40)])
+# (5000, 70) / (9000, 40): taller than one 16-CTA cluster x 256 rows, so the
+# narrow next-panel update restages its rows in chunks; (9000, 40) also takes
+# the shared-memory panel
+@pytest.mark.parametrize("d,n", [(96, 24), (400, 100), (130, 33), (1000, 250), (64, 64), (2000, 40), (5000, 70),
+                                 (9000, 40)])
 def test_qr_vs_oracle(d, n):
     rng = np.random.default_rng(d * n)
     Y = np.asfortranarray(rng.standard_normal((d, n)) @ np.diag(np.logspace(0, -4, n)))
