@@ -75,6 +75,7 @@ struct Workspace {
     DevBuf compact;      // sketch entries, u32 (row | neg << 31), column order
     DevBuf chunk_ptr;    // per-chunk row pointers (u16)
     DevBuf chunk_ent;    // per-chunk sorted entries (u16: k_local << 1 | neg)
+    DevBuf tile_ent;     // per-(chunk, row block) tile-grouped entries of the DMMA gather
     DevBuf ypart;        // sketch partials [nsplit][ld][d]
     DevBuf yaug;         // Y_aug = [S A | S b], d x (n+1) column-major
     DevBuf flags;        // small device counters / error flags

@@ -512,6 +512,218 @@ __global__ void reduce_splits_kernel(const double* Yw, int64_t nsplit, int64_t d
     Y[i] = s;
 }
 
+// ------------------------------------------------- K2d tile gather (DMMA)
+//
+// Fast-mode S.[A b] on the FP64 tensor cores.  A CTA owns a 16-column slab of
+// Y_aug for a block of 1024 rows, held as 128 8x8 row tiles x 2 column tiles
+// of mma.m8n8k4 accumulators (warp w owns row tiles w, w+32, w+64, w+96).  Per
+// chunk of K <= 512 rows of A, the slab segment (K x 128 B) arrives by TMA with
+// the 128-byte swizzle, together with the chunk's entries for this row block
+// grouped by row tile and padded to multiples of 4 (tile_repack_kernel).  One
+// group of 4 entries is one k-step: A-fragment = the 8x4 block of S (entry j's
+// sign * val in the row of its target, 0 elsewhere), B-fragment = the 4 A rows'
+// even / odd columns gathered from shared memory with one 16-byte load, two
+// DMMAs (column tiles 0 and 1).
+// Every warp runs the same instruction stream (no per-lane row ownership, so
+// none of the register gather's divergence), the swizzle spreads the four
+// gathered rows over the banks, and the 8x zero padding of S runs on tensor
+// cores that would otherwise idle.  Order of accumulation differs from the
+// reference's serial order: fast mode only (exact mode keeps gather_kernel).
+constexpr int kTdRows = 1024;          // Y rows per CTA (row block)
+constexpr int kTdTiles = kTdRows / 8;  // 8-row tiles per row block
+constexpr int kTdHdr = 136;            // u16 header: tile offsets [129], 16-byte multiple
+constexpr int kTdMaxStages = 3;
+
+struct RepackArgs {
+    const uint16_t* ptr;  // chunk-CSR row pointers (u16, per chunk ptr_stride)
+    const uint16_t* ent;  // chunk-CSR entries (k_local << 1 | neg)
+    int64_t ptr_stride, ent_stride, d;
+    int nrb, cap;
+    int64_t blk_stride;   // u16 per (chunk, row block): kTdHdr + cap
+    uint16_t* out;
+    int* flag;
+};
+
+// one CTA per chunk: thread (rb % 8, tile) counts its tile's entries, pads to
+// a multiple of 4, a per-row-block scan places it; entries are re-encoded as
+// k_local | row_in_tile << 9 | valid << 12 | neg << 15 (0 = padding).
+__global__ void __launch_bounds__(1024) tile_repack_kernel(RepackArgs a) {
+    __shared__ int wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t c = blockIdx.x;
+    const uint16_t* ptr = a.ptr + c * a.ptr_stride;
+    const uint16_t* ent = a.ent + c * a.ent_stride;
+    for (int rb0 = 0; rb0 < a.nrb; rb0 += 8) {
+        const int rb = rb0 + tid / kTdTiles, tb = tid % kTdTiles;
+        const int64_t r0 = (static_cast<int64_t>(rb) * kTdTiles + tb) * 8;
+        int e0 = 0, cnt = 0;
+        if (rb < a.nrb && r0 < a.d) {
+            e0 = ptr[r0];
+            cnt = ptr[r0 + 8 < a.d ? r0 + 8 : a.d] - e0;
+        }
+        const int pad = (cnt + 3) & ~3;
+        int x = pad;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        const int w0 = warp & ~3;  // 4 warps per row block
+        int base = 0;
+        for (int q = w0; q < warp; ++q) base += wsum[q];
+        const int total = wsum[w0] + wsum[w0 + 1] + wsum[w0 + 2] + wsum[w0 + 3];
+        __syncthreads();
+        if (rb < a.nrb) {
+            const int off = base + x - pad;
+            uint16_t* blk = a.out + (c * a.nrb + rb) * a.blk_stride;
+            blk[tb] = static_cast<uint16_t>(off < a.cap ? off : a.cap);
+            if (tb == kTdTiles - 1) blk[kTdTiles] = static_cast<uint16_t>(total < a.cap ? total : a.cap);
+            if (total > a.cap) {
+                if (tb == 0) atomicExch(a.flag, 1);
+            } else {
+                uint16_t* eo = blk + kTdHdr + off;
+                int j = 0;
+                for (int rr = 0; rr < 8; ++rr) {
+                    const int64_t r = r0 + rr;
+                    if (r >= a.d) break;
+                    for (int e = ptr[r]; e < ptr[r + 1]; ++e, ++j) {
+                        const unsigned kv = ent[e];
+                        eo[j] = static_cast<uint16_t>((kv >> 1) | (rr << 9) | 0x1000u | ((kv & 1u) << 15));
+                    }
+                }
+                for (; j < pad; ++j) eo[j] = 0;
+            }
+        }
+    }
+}
+
+struct TdArgs {
+    int64_t m, d, ldw;
+    int K;
+    int64_t nsplit, c_lo, c_hi;
+    const uint16_t* tiles;
+    int64_t blk_stride;
+    int nrb, ns;
+    double val;
+    double* Yw;  // [nsplit][ldw][d]
+};
+
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(1024, 1) gather_dmma_kernel(const __grid_constant__ CUtensorMap tmap, TdArgs g) {
+    extern __shared__ __align__(16) unsigned char tdsm[];
+    __shared__ __align__(8) uint64_t full[kTdMaxStages];
+    __shared__ int done[kTdMaxStages];  // warps finished with the stage's current chunk
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lr = lane & 3, lg = lane >> 2;
+    const int64_t col0 = static_cast<int64_t>(blockIdx.x) * 16;
+    const int rb = blockIdx.y;
+    const int64_t split = blockIdx.z;
+    const int64_t cb = g.c_lo + split * (g.c_hi - g.c_lo) / g.nsplit;
+    const int64_t ce = g.c_lo + (split + 1) * (g.c_hi - g.c_lo) / g.nsplit;
+    // stage s: [A box K x 128 B, 1024-aligned for the 128-byte swizzle][tile block]
+    // align inside the shared window (keeps the compiler on ld.shared)
+    unsigned char* base = tdsm + ((1024u - (ptx::smem_u32(tdsm) & 1023u)) & 1023u);
+    const size_t a_bytes = static_cast<size_t>(g.K) * 128;
+    const size_t t_bytes = (static_cast<size_t>(g.blk_stride) * 2 + 1023) & ~size_t(1023);
+    const size_t st_bytes = a_bytes + t_bytes;
+    auto As = [&](int s) { return base + s * st_bytes; };
+    auto Ts = [&](int s) { return reinterpret_cast<const uint16_t*>(base + s * st_bytes + a_bytes); };
+    if (tid == 0) {
+        for (int s = 0; s < g.ns; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            done[s] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int64_t c, int s) {  // one thread
+        const int64_t k0 = c * g.K;
+        const int kc = static_cast<int>(min(static_cast<int64_t>(g.K), g.m - k0));
+        const int nbox = (kc + 255) >> 8;
+        const unsigned tb = static_cast<unsigned>(g.blk_stride * 2);
+        ptx::mbar_expect_tx(&full[s], static_cast<unsigned>(nbox * 256 * 128) + tb);
+        for (int bx = 0; bx < nbox; ++bx)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+                    ptx::smem_u32(As(s) + static_cast<size_t>(bx) * 256 * 128)),
+                "l"(&tmap), "r"(static_cast<int>(col0)), "r"(static_cast<int>(k0 + 256 * bx)), "r"(ptx::smem_u32(&full[s]))
+                : "memory");
+        ptx::bulk_g2s(const_cast<uint16_t*>(Ts(s)), g.tiles + (c * g.nrb + rb) * g.blk_stride, tb, &full[s]);
+    };
+    double acc[4][2][2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[q][j][0] = acc[q][j][1] = 0.0;
+    if (tid == 0)
+        for (int s = 0; s < g.ns && cb + s < ce; ++s) issue(cb + s, s);
+    const unsigned vhi = static_cast<unsigned>(__double2hiint(g.val)), vlo = static_cast<unsigned>(__double2loint(g.val));
+    const unsigned rowkey = 0x1000u | (static_cast<unsigned>(lg) << 9);  // valid | row lg
+    const unsigned lgu = static_cast<unsigned>(lg);
+    int s = 0;
+    unsigned phase = 0;
+    for (int64_t c = cb; c < ce; ++c) {
+        ptx::mbar_wait(&full[s], phase);
+        const unsigned char* Ab = As(s);
+        const uint16_t* T = Ts(s);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int tb = warp + 32 * q;
+            const int g0 = T[tb], g1 = T[tb + 1];
+            const uint16_t* ep = T + kTdHdr + lr;
+            for (int gi = g0; gi < g1; gi += 4) {
+                const unsigned en = ep[gi];
+                // A-fragment: +-val where the entry's row is this lane's row lg
+                // (valid bit and row compared in one mask), 0 elsewhere -- built
+                // on the high word: sign flip by XOR, zero by AND
+                const unsigned hit = ((en & 0x1e00u) == rowkey) ? 0xffffffffu : 0u;
+                const unsigned hi = (vhi ^ ((en & 0x8000u) << 16)) & hit;
+                const double a = __hiloint2double(static_cast<int>(hi), static_cast<int>(vlo & hit));
+                // B-fragments: column tile 0 = the slab's even columns, tile 1 =
+                // its odd columns, so lane lg's two operands (columns 2lg and
+                // 2lg + 1 of row k) are one 16-byte unit: unit lg ^ (k & 7) of
+                // the 128-byte-swizzled row, one LDS.128 for both DMMAs
+                const unsigned k = en & 511u;
+                const double2 bb = *reinterpret_cast<const double2*>(Ab + ((k << 7) | (((lgu ^ k) & 7u) << 4)));
+                dmma_f64(acc[q][0][0], acc[q][0][1], a, bb.x);
+                dmma_f64(acc[q][1][0], acc[q][1][1], a, bb.y);
+            }
+        }
+        // no block barrier: the last warp done with stage s refills it with
+        // chunk c + ns, so warps drift up to ns - 1 chunks apart and uneven
+        // per-tile group counts average out
+        __syncwarp();
+        if (lane == 0 && atomicAdd(&done[s], 1) == 31) {
+            done[s] = 0;
+            if (c + g.ns < ce) issue(c + g.ns, s);
+        }
+        if (++s == g.ns) {
+            s = 0;
+            phase ^= 1u;
+        }
+    }
+    double* Y = g.Yw + split * g.ldw * g.d;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t r = static_cast<int64_t>(rb) * kTdRows + (warp + 32 * q) * 8 + lg;
+        if (r < g.d)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int64_t col = col0 + 2 * (2 * lr + i) + j;  // tile j holds the columns of parity j
+                    if (col < g.ldw) Y[col * g.d + r] = acc[q][j][i];
+                }
+    }
+}
+
 // ------------------------------------------------- K2 cluster slab gather
 //
 // Experimental alternative (SLQ_SLAB_GATHER=1).  Y held in registers with
@@ -844,7 +1056,7 @@ ChunkPlan plan_chunks(int64_t m, int64_t d, int64_t zeta_max, int W) {
 // 2D tensor map over the row-major A block (inner dim = ld columns, outer = m
 // rows), boxes of 256 rows x W columns, no swizzle (the gather's entries hold
 // plain byte offsets k * 8W).
-CUtensorMap gather_tensor_map(const double* A, int64_t ld, int64_t m, int W) {
+CUtensorMap gather_tensor_map(const double* A, int64_t ld, int64_t m, int W, bool swizzle128 = false) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -860,7 +1072,8 @@ CUtensorMap gather_tensor_map(const double* A, int64_t ld, int64_t m, int W) {
     const cuuint32_t box[2] = {static_cast<cuuint32_t>(W), 256u};
     const cuuint32_t estr[2] = {1u, 1u};
     const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides, box, estr,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(SLQ_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
     return map;
@@ -1012,11 +1225,11 @@ void generate_sparse_rows_dev(slq_ctx* ctx, int64_t n, int64_t nnz, uint64_t see
     SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
 }
 
-ChunkCsr build_chunk_csr(slq_ctx* ctx, const uint32_t* compact, const int64_t* colptr_dev, int64_t zeta_max,
-                         int64_t m, int64_t d, int gather_width) {
+static ChunkCsr build_chunk_csr_plan(slq_ctx* ctx, const uint32_t* compact, const int64_t* colptr_dev,
+                                     int64_t zeta_max, int64_t m, int64_t d, int gather_width, const ChunkPlan& plan) {
     Workspace& ws = ctx->ws;
     ChunkCsr cc;
-    cc.plan = plan_chunks(m, d, zeta_max, gather_width);
+    cc.plan = plan;
     const ChunkPlan& cp = cc.plan;
     // slack: row-part slices may run past the last chunk
     cc.ptr = static_cast<uint16_t*>(ws.chunk_ptr.ensure(sizeof(uint16_t) * (cp.ptr_stride * cp.nchunks + d + 64)));
@@ -1032,6 +1245,95 @@ ChunkCsr build_chunk_csr(slq_ctx* ctx, const uint32_t* compact, const int64_t* c
     SLQ_LAUNCH_CHECK(ctx);
     return cc;
 }
+
+ChunkCsr build_chunk_csr(slq_ctx* ctx, const uint32_t* compact, const int64_t* colptr_dev, int64_t zeta_max,
+                         int64_t m, int64_t d, int gather_width) {
+    return build_chunk_csr_plan(ctx, compact, colptr_dev, zeta_max, m, d, gather_width,
+                                plan_chunks(m, d, zeta_max, gather_width));
+}
+
+namespace {
+
+// K2d (fast mode, device-resident A): tile gather on the FP64 tensor cores.
+// Returns false if a chunk overflowed its bucket (caller falls back to the
+// register gather, which has no per-row-block capacity).
+bool sketch_apply_dmma(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32_t* compact,
+                       const int64_t* colptr_dev, int64_t zeta_max, double val, double* Y) {
+    const int64_t m = A->m, ld = A->ld, ncols_out = A->n + 1;
+    int zp = 1;
+    while (zp < zeta_max) zp <<= 1;
+    ChunkPlan p{};
+    p.K = 512;
+    while (p.K > 16 && static_cast<int64_t>(p.K) * zp > 16384) p.K >>= 1;
+    p.KB = 0;
+    while ((1 << p.KB) < p.K) ++p.KB;
+    p.cap = 16384;
+    p.nchunks = ceil_div(m, static_cast<int64_t>(p.K));
+    p.ptr_stride = round_up(d + 1, 8);
+    p.ent_stride = round_up(static_cast<int64_t>(p.K) * zeta_max, 8);
+    ChunkCsr cc = build_chunk_csr_plan(ctx, compact, colptr_dev, zeta_max, m, d, 0, p);
+
+    const int nrb = static_cast<int>(ceil_div(d, static_cast<int64_t>(kTdRows)));
+    const int64_t rows_rb = std::min<int64_t>(kTdRows, d);
+    const int64_t expect = static_cast<int64_t>(p.K) * zeta_max * rows_rb / d;
+    const int64_t cap = round_up(std::min<int64_t>(static_cast<int64_t>(p.K) * zeta_max, 2 * expect + 256) + 3 * kTdTiles, 8);
+    const int64_t blk_stride = kTdHdr + cap;
+    Workspace& ws = ctx->ws;
+    uint16_t* tiles = static_cast<uint16_t*>(ws.tile_ent.ensure(sizeof(uint16_t) * p.nchunks * nrb * blk_stride));
+    int* flag = cc.flag + 1;
+    SLQ_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    RepackArgs ra{cc.ptr, cc.ent, p.ptr_stride, p.ent_stride, d, nrb, static_cast<int>(cap), blk_stride, tiles, flag};
+    tile_repack_kernel<<<static_cast<unsigned>(p.nchunks), 1024, 0, ctx->stream>>>(ra);
+    SLQ_LAUNCH_CHECK(ctx);
+
+    const int64_t ldw = round_up(ncols_out, 16);
+    const int64_t nslabs = ldw / 16;
+    const size_t a_bytes = static_cast<size_t>(p.K) * 128;
+    const size_t t_bytes = round_up(static_cast<int64_t>(blk_stride) * 2, 1024);
+    const size_t st = a_bytes + t_bytes;
+    const int ns = static_cast<int>(std::min<size_t>(kTdMaxStages, (226 * 1024 - 1024) / st));
+    if (ns < 2) return false;
+    const size_t smem = ns * st + 1024;
+    int64_t nsplit = 1;
+    {
+        double best = 1e30;
+        const int64_t ctas = nslabs * nrb;
+        for (int64_t s = 1; s <= 16 && s <= p.nchunks; ++s) {
+            const double waves = std::ceil(static_cast<double>(ctas * s) / ctx->num_sms);
+            const double cost = waves / s + 0.02 * s;
+            if (cost < best - 1e-9) {
+                best = cost;
+                nsplit = s;
+            }
+        }
+    }
+    double* Yw = (nsplit == 1 && ldw == ncols_out) ? Y
+                 : static_cast<double*>(ws.ypart.ensure(sizeof(double) * nsplit * ldw * d));
+    TdArgs g{m, d, ldw, p.K, nsplit, 0, p.nchunks, tiles, blk_stride, nrb, ns, val, Yw};
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(gather_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    const CUtensorMap map = gather_tensor_map(A->A, ld, m, 16, true);
+    gather_dmma_kernel<<<dim3(static_cast<unsigned>(nslabs), static_cast<unsigned>(nrb), static_cast<unsigned>(nsplit)),
+                         1024, smem, ctx->stream>>>(map, g);
+    SLQ_LAUNCH_CHECK(ctx);
+    int hflag[2] = {0, 0};
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(hflag, cc.flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (hflag[0] || hflag[1]) return false;
+    if (Yw != Y) {
+        if (nsplit == 1) {
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(Y, Yw, sizeof(double) * d * ncols_out, cudaMemcpyDeviceToDevice, ctx->stream));
+        } else {
+            const int64_t tot = d * ncols_out;
+            reduce_splits_kernel<<<static_cast<unsigned>(ceil_div(tot, 256)), 256, 0, ctx->stream>>>(Yw, nsplit, d, ldw,
+                                                                                                    ncols_out, Y);
+            SLQ_LAUNCH_CHECK(ctx);
+        }
+    }
+    return true;
+}
+
+}  // namespace
 
 void check_chunk_csr(slq_ctx* ctx, const ChunkCsr& cc) {
     int hflag = 0;
@@ -1128,6 +1430,9 @@ void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const
     // d = 4n, slower than the register-row gather (one entry per warp
     // instruction vs 32): opt-in for experiments only
     if (slq_env_flag("SLQ_SLAB_GATHER") && sketch_apply_slab(ctx, A, d, compact, colptr_dev, zeta, val, exact, Y)) return;
+    // fast mode: the DMMA tile gather (falls back if a bucket overflowed)
+    const bool row_gather = slq_env_flag("SLQ_ROW_GATHER");  // diagnostics: register gather in fast mode
+    if (!exact && !row_gather && sketch_apply_dmma(ctx, A, d, compact, colptr_dev, zeta, val, Y)) return;
     DenseGather G = dense_gather_plan(ctx, m, A->n, A->ld, d, compact, colptr_dev, zeta, val, exact, Y, false);
     dense_gather_rows(ctx, G, A->A, 0, m);
     dense_gather_finish(ctx, G);
