@@ -108,6 +108,26 @@ def test_apply_exact(m, n, d, zeta):
     assert np.abs(Yf - Yo).max() <= tol and np.abs(Sbf - Sbo).max() <= tol
 
 
+@pytest.mark.parametrize("m,n,d,zeta", [(513, 16, 1030, 8), (1, 5, 40, 3), (2000, 47, 8, 8), (7000, 15, 2100, 32),
+                                        (1537, 33, 4096, 2)])
+def test_apply_fast_tile_gather(m, n, d, zeta, monkeypatch):
+    """Fast mode runs the DMMA tile gather (K2d); it must agree with the
+    reference order to 1e-12 and with the register gather (SLQ_ROW_GATHER=1):
+    partial chunks, partial 16-column slabs, several 1024-row blocks, zeta up
+    to 32."""
+    rng = np.random.default_rng(m * 7 + d)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    b = rng.standard_normal(m)
+    Yo, Sbo = C.sketch_apply(d, zeta, 29, A, b)
+    dm = slq.DeviceMatrix.from_numpy(A, b)
+    Yf, Sbf = dm.sketch(d, zeta, 29, exact=False)
+    monkeypatch.setenv("SLQ_ROW_GATHER", "1")
+    Yr, Sbr = dm.sketch(d, zeta, 29, exact=False)
+    tol = 1e-12 * max(1.0, np.abs(Yo).max())
+    assert np.abs(Yf - Yo).max() <= tol and np.abs(Sbf - Sbo).max() <= tol
+    assert np.abs(Yf - Yr).max() <= tol and np.abs(Sbf - Sbr).max() <= tol
+
+
 @pytest.mark.parametrize("m,n,d,zeta", [(5000, 37, 200, 8), (4096, 64, 512, 16), (3000, 40, 9000, 4)])
 def test_apply_cluster_slab_gather(m, n, d, zeta, monkeypatch):
     """The opt-in cluster/multicast slab gather (SLQ_SLAB_GATHER=1) is
