@@ -622,8 +622,10 @@ __global__ void __launch_bounds__(1024, 1) gather_dmma_kernel(const __grid_const
     __shared__ int done[kTdMaxStages];  // warps finished with the stage's current chunk
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int lr = lane & 3, lg = lane >> 2;
-    const int64_t col0 = static_cast<int64_t>(blockIdx.x) * 16;
-    const int rb = blockIdx.y;
+    // row block fastest in the grid: the CTAs reading the same A slab chunks
+    // are resident together, so A streams from DRAM once (L2 serves the rest)
+    const int rb = blockIdx.x;
+    const int64_t col0 = static_cast<int64_t>(blockIdx.y) * 16;
     const int64_t split = blockIdx.z;
     const int64_t cb = g.c_lo + split * (g.c_hi - g.c_lo) / g.nsplit;
     const int64_t ce = g.c_lo + (split + 1) * (g.c_hi - g.c_lo) / g.nsplit;
@@ -1313,7 +1315,7 @@ bool sketch_apply_dmma(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(gather_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
     const CUtensorMap map = gather_tensor_map(A->A, ld, m, 16, true);
-    gather_dmma_kernel<<<dim3(static_cast<unsigned>(nslabs), static_cast<unsigned>(nrb), static_cast<unsigned>(nsplit)),
+    gather_dmma_kernel<<<dim3(static_cast<unsigned>(nrb), static_cast<unsigned>(nslabs), static_cast<unsigned>(nsplit)),
                          1024, smem, ctx->stream>>>(map, g);
     SLQ_LAUNCH_CHECK(ctx);
     int hflag[2] = {0, 0};
