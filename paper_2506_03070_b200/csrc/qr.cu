@@ -727,10 +727,11 @@ __global__ void __launch_bounds__(256) update_apply_kernel(UpdArgs u, const doub
 // redundantly, deterministic), T^T is applied, and the CTA updates the staged
 // C rows from shared memory.
 constexpr int kNRB = 256;        // rows per staged chunk
+constexpr int kNThreads = 512;   // 16 warps: one W tile each in phase 1, more loads in flight when staging
 constexpr int kNLd = kNRB + 4;   // conflict-free fragment loads (as kLdT)
 constexpr size_t kNarrowSmem = sizeof(double) * (2 * kNbMax * kNLd + kNbMax * kCB + 3 * kNbMax * (kCB + 1));
 
-__global__ void __launch_bounds__(256) narrow_update_kernel(UpdArgs u, int64_t rpc) {
+__global__ void __launch_bounds__(kNThreads) narrow_update_kernel(UpdArgs u, int64_t rpc) {
     static_assert(kNbMax == kCB, "V and C tiles share the staging loop");
     extern __shared__ __align__(16) double sm[];
     double* Vs = sm;                          // [a][i], kNLd
@@ -750,7 +751,7 @@ __global__ void __launch_bounds__(256) narrow_update_kernel(UpdArgs u, int64_t r
     const int nch = static_cast<int>((nrows + kNRB - 1) / kNRB);
     const int64_t c0 = u.c_begin;
     auto stage = [&](int64_t r0) {
-        for (int e = tid; e < kNbMax * kNRB; e += 256) {
+        for (int e = tid; e < kNbMax * kNRB; e += kNThreads) {
             const int a = e / kNRB, i = e % kNRB;
             const int64_t r = r0 + i;
             double v = 0.0, c = 0.0;
@@ -762,10 +763,10 @@ __global__ void __launch_bounds__(256) narrow_update_kernel(UpdArgs u, int64_t r
             Cs[a * kNLd + i] = c;
         }
     };
-    for (int e = tid; e < kNbMax * kNbMax; e += 256) Ts[(e % kNbMax) * (kNbMax + 1) + e / kNbMax] = u.T[e];
-    // phase 1: Wp = V^T C over this CTA's rows (16 8x8 tiles, two per warp)
-    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    const int t0 = 2 * warp, at = t0 >> 2, ct0 = t0 & 3, ct1 = ct0 + 1;
+    for (int e = tid; e < kNbMax * kNbMax; e += kNThreads) Ts[(e % kNbMax) * (kNbMax + 1) + e / kNbMax] = u.T[e];
+    // phase 1: Wp = V^T C over this CTA's rows (16 8x8 tiles, one per warp)
+    double acc0 = 0.0, acc1 = 0.0;
+    const int at = warp >> 2, ctile = warp & 3;
     for (int ch = 0; ch < nch; ++ch) {
         const int64_t r0 = rbeg + static_cast<int64_t>(ch) * kNRB;
         const int rows = static_cast<int>(rend - r0 < kNRB ? rend - r0 : kNRB);
@@ -776,28 +777,24 @@ __global__ void __launch_bounds__(256) narrow_update_kernel(UpdArgs u, int64_t r
         for (int ks = 0; ks < nks; ++ks) {
             const int i = ks * 4 + lr;
             const double af = Vs[(at * 8 + lg) * kNLd + i];
-            const double b0 = Cs[(ct0 * 8 + lg) * kNLd + i];
-            const double b1 = Cs[(ct1 * 8 + lg) * kNLd + i];
-            dmma(acc[0][0], acc[0][1], af, b0);
-            dmma(acc[1][0], acc[1][1], af, b1);
+            const double bf = Cs[(ctile * 8 + lg) * kNLd + i];
+            dmma(acc0, acc1, af, bf);
         }
     }
     {
         const int a = at * 8 + lg;
-        Wp[a * kCB + ct0 * 8 + 2 * lr] = acc[0][0];
-        Wp[a * kCB + ct0 * 8 + 2 * lr + 1] = acc[0][1];
-        Wp[a * kCB + ct1 * 8 + 2 * lr] = acc[1][0];
-        Wp[a * kCB + ct1 * 8 + 2 * lr + 1] = acc[1][1];
+        Wp[a * kCB + ctile * 8 + 2 * lr] = acc0;
+        Wp[a * kCB + ctile * 8 + 2 * lr + 1] = acc1;
     }
     cluster.sync();
     // cluster sum in fixed rank order, then W2 = T^T Ws
-    for (int e = tid; e < kNbMax * kCB; e += 256) {
+    for (int e = tid; e < kNbMax * kCB; e += kNThreads) {
         double s = 0.0;
         for (int q = 0; q < ncta; ++q) s += cluster.map_shared_rank(Wp, q)[e];
         Ws[(e / kCB) * (kCB + 1) + e % kCB] = s;
     }
     __syncthreads();
-    for (int e = tid; e < kNbMax * kCB; e += 256) {
+    for (int e = tid; e < kNbMax * kCB; e += kNThreads) {
         const int ra = e / kCB, c = e % kCB;
         double t = 0.0;
         if (u.transT) {
@@ -807,17 +804,18 @@ __global__ void __launch_bounds__(256) narrow_update_kernel(UpdArgs u, int64_t r
         }
         W2[ra * (kCB + 1) + c] = t;
     }
-    // phase 2: C_rows -= V_rows W2 (the single chunk is still staged)
-    for (int ch = 0; ch < nch; ++ch) {
+    // phase 2: C_rows -= V_rows W2, last chunk first (it is still staged)
+    for (int cc = 0; cc < nch; ++cc) {
+        const int ch = nch - 1 - cc;
         const int64_t r0 = rbeg + static_cast<int64_t>(ch) * kNRB;
         const int rows = static_cast<int>(rend - r0 < kNRB ? rend - r0 : kNRB);
-        if (nch > 1) {
+        if (cc > 0) {
             __syncthreads();
             stage(r0);
         }
         __syncthreads();
         const int nrt = (rows + 7) >> 3;
-        for (int rt = warp; rt < nrt; rt += 8) {
+        for (int rt = warp; rt < nrt; rt += kNThreads / 32) {
             double d[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
             for (int ks = 0; ks < kNbMax / 4; ++ks) {
@@ -1144,7 +1142,7 @@ int narrow_cluster_max() {
     for (int cl = 16; cl >= 1 && !cached; cl /= 2) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(cl, 1, 1);
-        cfg.blockDim = dim3(256, 1, 1);
+        cfg.blockDim = dim3(kNThreads, 1, 1);
         cfg.dynamicSmemBytes = kNarrowSmem;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1177,7 +1175,7 @@ void launch_narrow(slq_ctx* ctx, const UpdArgs& u, cudaStream_t st, DevBuf& wbuf
     const int64_t rpc = ceil_div(ceil_div(rows, cl), 8) * 8;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cl, 1, 1);
-    cfg.blockDim = dim3(256, 1, 1);
+    cfg.blockDim = dim3(kNThreads, 1, 1);
     cfg.dynamicSmemBytes = kNarrowSmem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
