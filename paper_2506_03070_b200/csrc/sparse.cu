@@ -214,8 +214,13 @@ struct SGatherArgs {
 };
 
 // One warp per Y row; the row lives in shared memory.  Entries are processed
-// in ascending k; the (column, value) pairs of 4 consecutive A rows are
-// loaded before they are applied (loads in flight), then added row by row.
+// in ascending k in batches of kSgB A rows: the batch's S^T entries (one
+// coalesced load, lane q holds entry q), their row pointers (lane q loads row
+// q's pair) and then every row's (column, value) pairs are all in flight
+// before the batch is added row by row -- three dependent load rounds per kSgB
+// rows.
+constexpr int kSgB = 8;
+
 __global__ void __launch_bounds__(512) sparse_gather_kernel(SGatherArgs g) {
     extern __shared__ double ys[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -226,21 +231,22 @@ __global__ void __launch_bounds__(512) sparse_gather_kernel(SGatherArgs g) {
     __syncwarp();
     if (r < g.d) {
         const int64_t e0 = g.srow_ptr[r], e1 = g.srow_ptr[r + 1];
-        for (int64_t e = e0; e < e1; e += 4) {
-            const int nb = (e1 - e < 4) ? static_cast<int>(e1 - e) : 4;
-            uint32_t en[4];
-            int64_t rb[4], re[4];
+        for (int64_t e = e0; e < e1; e += kSgB) {
+            const int nb = (e1 - e < kSgB) ? static_cast<int>(e1 - e) : kSgB;
+            // round 1: entries; round 2: row pointers and b (lane q: row q)
+            const uint32_t my_en = lane < nb ? g.sent[e + lane] : 0u;
+            const int64_t my_k = my_en & 0x7fffffffu;
+            const int64_t my_rb = lane < nb ? g.rowptr[my_k] : 0;
+            const int64_t my_re = lane < nb ? g.rowptr[my_k + 1] : 0;
+            const double my_b = (g.b && lane < nb) ? g.b[my_k] : 0.0;
+            // round 3: every row's (column, value) pairs
+            int32_t cc[kSgB][2];
+            double vv[kSgB][2];
+            int64_t rb[kSgB], re[kSgB];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                en[q] = q < nb ? g.sent[e + q] : 0u;
-                const int64_t k = en[q] & 0x7fffffffu;
-                rb[q] = q < nb ? g.rowptr[k] : 0;
-                re[q] = q < nb ? g.rowptr[k + 1] : 0;
-            }
-            int32_t cc[4][2];
-            double vv[4][2];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < kSgB; ++q) {
+                rb[q] = __shfl_sync(0xffffffffu, my_rb, q);
+                re[q] = __shfl_sync(0xffffffffu, my_re, q);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int64_t t = rb[q] + lane + 32 * h;
@@ -248,22 +254,22 @@ __global__ void __launch_bounds__(512) sparse_gather_kernel(SGatherArgs g) {
                     cc[q][h] = ok ? g.colidx[t] : -1;
                     vv[q][h] = ok ? g.vals[t] : 0.0;
                 }
-            double bq[4];
+            }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) bq[q] = (g.b && q < nb && lane == 0) ? g.b[en[q] & 0x7fffffffu] : 0.0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < kSgB; ++q) {
+                const uint32_t en = __shfl_sync(0xffffffffu, my_en, q);
+                const double bq = __shfl_sync(0xffffffffu, my_b, q);
                 if (q >= nb) break;
-                const double s = (en[q] >> 31) ? -g.val : g.val;
+                const double sv = (en >> 31) ? -g.val : g.val;
                 // csc_matrix.hpp:133: yj[row] += S_val * akj (two roundings)
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
-                    if (cc[q][h] >= 0) y[cc[q][h]] = __dadd_rn(y[cc[q][h]], __dmul_rn(s, vv[q][h]));
+                    if (cc[q][h] >= 0) y[cc[q][h]] = __dadd_rn(y[cc[q][h]], __dmul_rn(sv, vv[q][h]));
                 for (int64_t t = rb[q] + 64 + lane; t < re[q]; t += 32) {  // rows longer than 64
                     const int32_t c = g.colidx[t];
-                    y[c] = __dadd_rn(y[c], __dmul_rn(s, g.vals[t]));
+                    y[c] = __dadd_rn(y[c], __dmul_rn(sv, g.vals[t]));
                 }
-                if (lane == 0 && g.b && bq[q] != 0.0) y[g.n] = __dadd_rn(y[g.n], __dmul_rn(s, bq[q]));
+                if (lane == 0 && g.b && bq != 0.0) y[g.n] = __dadd_rn(y[g.n], __dmul_rn(sv, bq));
                 __syncwarp();
             }
         }
