@@ -119,7 +119,9 @@ int64_t slq_dense_ld(const slq_dense* A);
  * sign sketch (d, zeta, seed) is generated on the device for this rank's rows
  * and applied to [A | b] in one pass.  Y (d x n, column-major, ldy = d) and
  * Sb (d) are host outputs; either may be NULL.  exact != 0 forces the
- * reference's serial accumulation order (bit-identical Y on one GPU). */
+ * reference's serial accumulation order (bit-identical Y on one GPU);
+ * exact == 0 (and slq_solve) runs the FP64 tensor-core tile gather, whose
+ * sums differ from the serial order by rounding only (~1e-15 relative). */
 int slq_sketch_apply(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_t seed,
                      int exact, double* Y, double* Sb);
 
