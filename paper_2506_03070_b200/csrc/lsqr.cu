@@ -154,16 +154,15 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
                 const double* row = tile + static_cast<int64_t>(i) * ld;
                 const double u = a.u_in ? a.u_in[row0 + i] : row[a.n];
                 double acc0 = 0.0, acc1 = 0.0;
+                double2 vr[NP];  // the row stays in registers for the z update: one shared-memory read
 #pragma unroll
                 for (int q = 0; q < NP; ++q) {
                     const int64_t j = 2 * lane + 64 * q;
-                    if (j < ld) {
-                        const double2 v = *reinterpret_cast<const double2*>(row + j);
-                        const double p0 = P_SMEM ? p_s[j] : pr[2 * q];
-                        const double p1 = P_SMEM ? p_s[j + 1] : pr[2 * q + 1];
-                        acc0 = fma(v.x, p0, acc0);
-                        acc1 = fma(v.y, p1, acc1);
-                    }
+                    vr[q] = j < ld ? *reinterpret_cast<const double2*>(row + j) : make_double2(0.0, 0.0);
+                    const double p0 = j < ld ? (P_SMEM ? p_s[j] : pr[2 * q]) : 0.0;
+                    const double p1 = j < ld ? (P_SMEM ? p_s[j + 1] : pr[2 * q + 1]) : 0.0;
+                    acc0 = fma(vr[q].x, p0, acc0);
+                    acc1 = fma(vr[q].y, p1, acc1);
                 }
                 const double y = warp_sum(acc0 + acc1);
                 const double uh = __dadd_rn(y, __dmul_rn(c, u));
@@ -172,12 +171,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
                 if (a.want_z) {
 #pragma unroll
                     for (int q = 0; q < NP; ++q) {
-                        const int64_t j = 2 * lane + 64 * q;
-                        if (j < ld) {
-                            const double2 v = *reinterpret_cast<const double2*>(row + j);
-                            z[2 * q] = fma(v.x, uh, z[2 * q]);
-                            z[2 * q + 1] = fma(v.y, uh, z[2 * q + 1]);
-                        }
+                        z[2 * q] = fma(vr[q].x, uh, z[2 * q]);
+                        z[2 * q + 1] = fma(vr[q].y, uh, z[2 * q + 1]);
                     }
                 }
             }
