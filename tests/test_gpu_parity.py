@@ -128,6 +128,19 @@ def test_apply_fast_tile_gather(m, n, d, zeta, monkeypatch):
     assert np.abs(Yf - Yr).max() <= tol and np.abs(Sbf - Sbr).max() <= tol
 
 
+def test_apply_fast_tile_gather_tall_sketch():
+    """d = 20000 is past the register gather's envelope (d <= 16384); the
+    tile gather covers it in fast mode (20 row blocks of 1024)."""
+    m, n, d, zeta = 6000, 9, 20000, 4
+    rng = np.random.default_rng(5)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    b = rng.standard_normal(m)
+    Yo, Sbo = C.sketch_apply(d, zeta, 31, A, b)
+    Yf, Sbf = slq.DeviceMatrix.from_numpy(A, b).sketch(d, zeta, 31, exact=False)
+    tol = 1e-12 * max(1.0, np.abs(Yo).max())
+    assert np.abs(Yf - Yo).max() <= tol and np.abs(Sbf - Sbo).max() <= tol
+
+
 @pytest.mark.parametrize("m,n,d,zeta", [(5000, 37, 200, 8), (4096, 64, 512, 16), (3000, 40, 9000, 4)])
 def test_apply_cluster_slab_gather(m, n, d, zeta, monkeypatch):
     """The opt-in cluster/multicast slab gather (SLQ_SLAB_GATHER=1) is
