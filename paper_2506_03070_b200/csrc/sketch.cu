@@ -726,272 +726,6 @@ __global__ void __launch_bounds__(1024, 1) gather_dmma_kernel(const __grid_const
     }
 }
 
-// ------------------------------------------------- K2 cluster slab gather
-//
-// Experimental alternative (SLQ_SLAB_GATHER=1).  Y held in registers with
-// lane = column:
-//   * a thread-block CLUSTER of C CTAs owns a 32-column slab of Y_aug for all
-//     d rows: CTA rank b owns rows [b*16*RW, (b+1)*16*RW), its consumer warp
-//     w the RW rows b*16*RW + w*RW + q, one register per row per lane;
-//   * per chunk of K rows of A, each CTA's producer warp multicasts K/C rows
-//     of the slab (cp.async.bulk .multicast::cluster), so the chunk lands in
-//     every CTA's shared memory while A leaves HBM exactly once;
-//   * the chunk's sketch entries were bucketed once (bucketize_blob_kernel)
-//     into one blob per CTA: 17 u16 warp offsets, then u16 entries
-//     (q << (KB+1) | k << 1 | negative) sorted by (row, k).  Warp w walks its
-//     entries with warp-uniform control flow, lane j adding +-val *
-//     A[k][col0 + j] into y[q]: one conflict-free 256-byte shared-memory row
-//     read per entry, no divergence, no bank conflicts;
-//   * stages are released cluster-wide: every consumer warp arrives on the
-//     stage's "empty" mbarrier in each CTA of the cluster (remote arrive).
-// Every Y element is accumulated by one lane in ascending k, so EXACT (mul
-// then add) reproduces the reference's spmm (csc_matrix.hpp:103-120) bit for
-// bit with no split.
-constexpr int kSlabWarps = 16;                       // consumer warps per CTA
-constexpr int kSlabThreads = (kSlabWarps + 1) * 32;  // + one producer warp
-constexpr int kBlobHdr = 48;                         // 17 u16 warp offsets, padded to 16 B
-constexpr int kSlabMaxStages = 8;
-
-// Fill keys[0, NP) of chunk c with (row << (KB+1) | k << 1 | neg), padded with
-// kPad to a power of two, and sort them (bitonic, whole block).  Returns N.
-__device__ int load_sort_chunk_keys(const uint32_t* compact, const int64_t* colptr, int64_t zeta, int64_t ncols,
-                                    int K, int KB, int cap, int64_t c, uint32_t* keys, int* overflow, int* NPout) {
-    const int tid = threadIdx.x, T = blockDim.x;
-    const int64_t k0 = c * K;
-    const int64_t kc = min(static_cast<int64_t>(K), ncols - k0);
-    const int64_t eb = colptr ? colptr[k0] : k0 * zeta;
-    const int64_t ee = colptr ? colptr[k0 + kc] : (k0 + kc) * zeta;
-    const int N = static_cast<int>(ee - eb);
-    if (N > cap) {
-        if (tid == 0) atomicExch(overflow, 1);
-        return -1;
-    }
-    int NP = 2;
-    while (NP < N) NP <<= 1;
-    const int sh = KB + 1;
-    if (colptr) {
-        for (int64_t kl = tid; kl < kc; kl += T)
-            for (int64_t e = colptr[k0 + kl]; e < colptr[k0 + kl + 1]; ++e) {
-                const uint32_t ent = compact[e];
-                keys[e - eb] = ((ent & 0x7fffffffu) << sh) | (static_cast<uint32_t>(kl) << 1) | (ent >> 31);
-            }
-    } else {
-        for (int i = tid; i < N; i += T) {
-            const uint32_t ent = compact[eb + i];
-            const uint32_t kl = static_cast<uint32_t>(i / zeta);
-            keys[i] = ((ent & 0x7fffffffu) << sh) | (kl << 1) | (ent >> 31);
-        }
-    }
-    for (int i = N + tid; i < NP; i += T) keys[i] = kPad;
-    __syncthreads();
-    for (int k = 2; k <= NP; k <<= 1) {
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
-            for (int i = tid; i < (NP >> 1); i += T) {
-                const int lo = ((i & ~(jj - 1)) << 1) | (i & (jj - 1));
-                const int hi = lo + jj;
-                const bool asc = (lo & k) == 0;
-                const uint32_t x = keys[lo], y = keys[hi];
-                if ((x > y) == asc) {
-                    keys[lo] = y;
-                    keys[hi] = x;
-                }
-            }
-            __syncthreads();
-        }
-    }
-    *NPout = NP;
-    return N;
-}
-
-struct BlobArgs {
-    const uint32_t* compact;
-    const int64_t* colptr;  // null => uniform zeta
-    int64_t zeta, ncols;
-    int K, KB, RW, band_shift, nbands;
-    int64_t chunk_stride;   // bytes per chunk region
-    uint8_t* blob;          // [nchunks][chunk_stride]
-    uint32_t* off;          // [nchunks][nbands + 1] byte offsets of the band blobs
-    int cap;
-    int* overflow;
-};
-
-__global__ void __launch_bounds__(1024) bucketize_blob_kernel(BlobArgs a) {
-    extern __shared__ uint32_t keys[];
-    const int tid = threadIdx.x, T = blockDim.x;
-    const int64_t c = blockIdx.x;
-    int NP = 0;
-    const int N = load_sort_chunk_keys(a.compact, a.colptr, a.zeta, a.ncols, a.K, a.KB, a.cap, c, keys, a.overflow, &NP);
-    if (N < 0) return;
-    const int sh = a.KB + 1;
-    const int nw = a.nbands * kSlabWarps;
-    int* wfirst = reinterpret_cast<int*>(keys + a.cap);           // [nw + 1]
-    uint32_t* boff = reinterpret_cast<uint32_t*>(wfirst + nw + 1);  // [nbands + 1]
-    for (int gw = tid; gw <= nw; gw += T) {
-        const uint32_t key = static_cast<uint32_t>(gw * a.RW) << sh;
-        int lo = 0, hi = N;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (keys[mid] < key) lo = mid + 1;
-            else hi = mid;
-        }
-        wfirst[gw] = lo;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        uint32_t o = 0;
-        for (int b = 0; b < a.nbands; ++b) {
-            boff[b] = o;
-            const int cnt = wfirst[(b + 1) * kSlabWarps] - wfirst[b * kSlabWarps];
-            o += kBlobHdr + ((2 * cnt + 15) & ~15);
-        }
-        boff[a.nbands] = o;
-    }
-    __syncthreads();
-    uint8_t* base = a.blob + c * a.chunk_stride;
-    for (int b = tid; b <= a.nbands; b += T) a.off[c * (a.nbands + 1) + b] = boff[b];
-    for (int e = tid; e < a.nbands * (kBlobHdr / 2); e += T) {
-        const int b = e / (kBlobHdr / 2), w = e % (kBlobHdr / 2);
-        const int v = (w <= kSlabWarps) ? wfirst[b * kSlabWarps + w] - wfirst[b * kSlabWarps] : 0;
-        reinterpret_cast<uint16_t*>(base + boff[b])[w] = static_cast<uint16_t>(v);
-    }
-    const uint32_t lowmask = (1u << sh) - 1u;
-    for (int i = tid; i < N; i += T) {
-        const uint32_t key = keys[i];
-        const uint32_t r = key >> sh;
-        const int b = static_cast<int>(r >> a.band_shift);
-        const uint32_t q = r & static_cast<uint32_t>(a.RW - 1);
-        reinterpret_cast<uint16_t*>(base + boff[b] + kBlobHdr)[i - wfirst[b * kSlabWarps]] =
-            static_cast<uint16_t>((q << sh) | (key & lowmask));
-    }
-}
-
-struct SlabArgs {
-    const double* A;   // row-major, row 0 = local row 0
-    int64_t ld, m, d;
-    int K, KB, C, nstages;
-    int64_t nchunks, chunk_stride;
-    const uint8_t* blob;
-    const uint32_t* off;
-    int nbands;
-    unsigned stage_bytes, a_bytes;
-    double val;
-    int64_t ncols_out;  // columns of Y_aug (n + 1)
-    double* Y;          // d x ncols_out column-major
-};
-
-template <int RW, bool EXACT>
-__global__ void __launch_bounds__(kSlabThreads, 1) slab_gather_kernel(SlabArgs g) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ __align__(8) uint64_t full[kSlabMaxStages];
-    __shared__ __align__(8) uint64_t empty[kSlabMaxStages];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    cg::cluster_group cl = cg::this_cluster();
-    const unsigned rank = cl.block_rank();
-    const int C = g.C;
-    const int64_t col0 = static_cast<int64_t>(blockIdx.x / C) * 32;
-    const int width = static_cast<int>(min(static_cast<int64_t>(32), g.ld - col0));
-    const int S = g.nstages;
-    const int sh = g.KB + 1;
-    if (tid == 0) {
-        for (int s = 0; s < S; ++s) {
-            ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], static_cast<unsigned>(C * kSlabWarps));
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    cl.sync();
-    if (wid == kSlabWarps) {
-        // ---- producer warp
-        const int rpc = (g.K + C - 1) / C;
-        const int r_lo = static_cast<int>(rank) * rpc, r_hi = min(g.K, r_lo + rpc);
-        const uint16_t mask = static_cast<uint16_t>((1u << C) - 1u);
-        const unsigned wbytes = static_cast<unsigned>(width) * 8u;
-        uint32_t pre_lo = 0, pre_hi = 0;
-        int s = -1;
-        unsigned u = 0;
-        for (int64_t c = 0; c < g.nchunks; ++c) {
-            if (++s == S) {
-                s = 0;
-                ++u;
-            }
-            if ((c & 31) == 0) {
-                const int64_t cc = c + lane;
-                if (cc < g.nchunks) {
-                    pre_lo = g.off[cc * (g.nbands + 1) + rank];
-                    pre_hi = g.off[cc * (g.nbands + 1) + rank + 1];
-                }
-            }
-            const uint32_t lo = __shfl_sync(0xffffffffu, pre_lo, static_cast<int>(c & 31));
-            const uint32_t hi = __shfl_sync(0xffffffffu, pre_hi, static_cast<int>(c & 31));
-            if (c >= S) ptx::mbar_wait(&empty[s], (u - 1) & 1u);
-            unsigned char* st = smem + static_cast<size_t>(s) * g.stage_bytes;
-            const int64_t k0 = c * g.K;
-            const int kc = static_cast<int>(min(static_cast<int64_t>(g.K), g.m - k0));
-            if (lane == 0) {
-                ptx::mbar_expect_tx(&full[s], static_cast<unsigned>(kc) * wbytes + (hi - lo));
-                ptx::bulk_g2s(st + g.a_bytes, g.blob + c * g.chunk_stride + lo, hi - lo, &full[s]);
-            }
-            __syncwarp();
-            const double* src = g.A + k0 * g.ld + col0;
-            for (int r = r_lo + lane; r < r_hi; r += 32)
-                if (r < kc)
-                    ptx::bulk_g2s_multicast(st + static_cast<size_t>(r) * 256, src + static_cast<int64_t>(r) * g.ld, wbytes,
-                                            &full[s], mask);
-        }
-    } else {
-        // ---- consumer warps
-        double y[RW];
-#pragma unroll
-        for (int q = 0; q < RW; ++q) y[q] = 0.0;
-        const uint64_t vbits = static_cast<uint64_t>(__double_as_longlong(g.val));
-        const unsigned kmask = static_cast<unsigned>(g.K - 1);
-        int s = -1;
-        unsigned u = 0;
-        for (int64_t c = 0; c < g.nchunks; ++c) {
-            if (++s == S) {
-                s = 0;
-                ++u;
-            }
-            ptx::mbar_wait(&full[s], u & 1u);
-            const unsigned char* st = smem + static_cast<size_t>(s) * g.stage_bytes;
-            const double* As = reinterpret_cast<const double*>(st) + lane;
-            const uint16_t* hdr = reinterpret_cast<const uint16_t*>(st + g.a_bytes);
-            const uint16_t* ent = hdr + kBlobHdr / 2;
-            // entries are sorted by (q, k): walk the rows in order (static
-            // register index), each row's run with a warp-uniform loop; the
-            // next entry and its A value are loaded one step ahead
-            int i = hdr[wid];
-            const int e_end = hdr[wid + 1];
-            unsigned e = (i < e_end) ? ent[i] : 0xFFFFu;  // sentinel: row field > 31
-            double a = As[((e >> 1) & kmask) * 32];
-            unsigned qn = e >> sh;
-#pragma unroll
-            for (int q = 0; q < RW; ++q) {
-                while (qn == static_cast<unsigned>(q)) {
-                    const double sv =
-                        __longlong_as_double(static_cast<long long>(vbits ^ (static_cast<uint64_t>(e & 1u) << 63)));
-                    const double ac = a;
-                    ++i;
-                    e = (i < e_end) ? ent[i] : 0xFFFFu;
-                    a = As[((e >> 1) & kmask) * 32];
-                    y[q] = acc_step<EXACT>(y[q], sv, ac);
-                    qn = e >> sh;
-                }
-            }
-            __syncwarp();
-            if (lane < C) ptx::mbar_arrive_remote_relaxed(&empty[s], static_cast<unsigned>(lane));
-        }
-        const int64_t row0 = static_cast<int64_t>(rank) * (kSlabWarps * RW) + static_cast<int64_t>(wid) * RW;
-        const int64_t col = col0 + lane;
-        if (col < g.ncols_out) {
-#pragma unroll
-            for (int q = 0; q < RW; ++q)
-                if (row0 + q < g.d) g.Y[col * g.d + row0 + q] = y[q];
-        }
-    }
-    cl.sync();  // peers may still arrive on this CTA's barriers
-}
-
 uint64_t lemire_thresh(uint64_t d) { return (0 - d) % d; }
 
 }  // namespace
@@ -1103,115 +837,6 @@ void launch_gather(slq_ctx* ctx, const GatherArgs& g, int rpt, int W, int64_t ns
         default: fail(SLQ_UNSUPPORTED, "sketch_apply: d > 16384 not supported by the register-slab gather");
     }
     (void)W;
-}
-
-template <int RW, bool EXACT>
-void launch_slab_t(slq_ctx* ctx, const SlabArgs& g, int64_t nslabs, size_t smem) {
-    auto kern = slab_gather_kernel<RW, EXACT>;
-    SLQ_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    if (g.C > 8) SLQ_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(nslabs * g.C), 1, 1);
-    cfg.blockDim = dim3(kSlabThreads, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = ctx->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = static_cast<unsigned>(g.C);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    SLQ_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, g));
-    ctx->launches++;
-}
-
-template <bool EXACT>
-void launch_slab(slq_ctx* ctx, const SlabArgs& g, int rw, int64_t nslabs, size_t smem) {
-    switch (rw) {
-        case 8: launch_slab_t<8, EXACT>(ctx, g, nslabs, smem); break;
-        case 16: launch_slab_t<16, EXACT>(ctx, g, nslabs, smem); break;
-        default: launch_slab_t<32, EXACT>(ctx, g, nslabs, smem); break;
-    }
-}
-
-// can a cluster of C CTAs (one per SM, smem bytes each) be scheduled?
-bool cluster_fits(slq_ctx* ctx, int C, size_t smem) {
-    auto kern = slab_gather_kernel<32, false>;
-    SLQ_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    SLQ_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(C), 1, 1);
-    cfg.blockDim = dim3(kSlabThreads, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = ctx->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = static_cast<unsigned>(C);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
-        (void)cudaGetLastError();
-        return false;
-    }
-    return n > 0;
-}
-
-// Cluster slab gather (see slab_gather_kernel).  Returns false when the shape
-// is outside its envelope (caller falls back to the register-row gather).
-bool sketch_apply_slab(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32_t* compact,
-                       const int64_t* colptr_dev, int64_t zeta_max, double val, bool exact, double* Y) {
-    const int64_t m = A->m, ld = A->ld, ncols_out = A->n + 1;
-    if (zeta_max > 32 || d > 16 * kSlabWarps * 32) return false;
-    int rw = 32;
-    if (d <= kSlabWarps * 8) rw = 8;
-    else if (d <= kSlabWarps * 16) rw = 16;
-    const int C = static_cast<int>(ceil_div(d, static_cast<int64_t>(kSlabWarps) * rw));
-    int zp = 1;
-    while (zp < zeta_max) zp <<= 1;
-    int K = 256;
-    while (K > 16 && K * zp > 2048) K >>= 1;
-    int KB = 0;
-    while ((1 << KB) < K) ++KB;
-    const int nbands = C;
-    int band_shift = 0;
-    while ((1 << band_shift) < kSlabWarps * rw) ++band_shift;
-    const int64_t nchunks = ceil_div(m, static_cast<int64_t>(K));
-    const int64_t chunk_stride = round_up(static_cast<int64_t>(nbands) * (kBlobHdr + 16) + 2 * K * zeta_max, 16);
-    const unsigned a_bytes = static_cast<unsigned>(K) * 256u;
-    const unsigned blob_cap = static_cast<unsigned>(round_up(kBlobHdr + 2 * K * zeta_max + 16, 128));
-    const unsigned stage_bytes = a_bytes + blob_cap;
-    const int nstages = static_cast<int>(std::min<int64_t>(kSlabMaxStages, (216 * 1024) / stage_bytes));
-    if (nstages < 2) return false;
-
-    Workspace& ws = ctx->ws;
-    uint8_t* blob = static_cast<uint8_t*>(ws.chunk_ent.ensure(static_cast<size_t>(chunk_stride) * nchunks));
-    uint32_t* off = static_cast<uint32_t*>(ws.chunk_ptr.ensure(sizeof(uint32_t) * nchunks * (nbands + 1)));
-    int* flag = static_cast<int*>(ws.flags.ensure(4096));
-    SLQ_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
-    const int cap = 2048 >= K * zp ? 2048 : K * zp;
-    BlobArgs ba{compact, colptr_dev, zeta_max, m, K, KB, rw, band_shift, nbands, chunk_stride, blob, off, cap, flag};
-    const size_t bsmem = sizeof(uint32_t) * (cap + nbands * kSlabWarps + 1 + nbands + 1);
-    SLQ_CUDA_CHECK(cudaFuncSetAttribute(bucketize_blob_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(bsmem)));
-    bucketize_blob_kernel<<<static_cast<unsigned>(nchunks), 1024, bsmem, ctx->stream>>>(ba);
-    SLQ_LAUNCH_CHECK(ctx);
-
-    const size_t smem = static_cast<size_t>(nstages) * stage_bytes;
-    if (C > 8 && !cluster_fits(ctx, C, smem)) return false;
-    const int64_t nslabs = ceil_div(ld, static_cast<int64_t>(32));
-    SlabArgs g{A->A, ld, m, d, K, KB, C, nstages, nchunks, chunk_stride, blob, off, nbands,
-               stage_bytes, a_bytes, val, ncols_out, Y};
-    if (exact) launch_slab<true>(ctx, g, rw, nslabs, smem);
-    else launch_slab<false>(ctx, g, rw, nslabs, smem);
-    int hflag = 0;
-    SLQ_CUDA_CHECK(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-    if (hflag) fail(SLQ_UNSUPPORTED, "sketch_apply: a chunk exceeded the bucketing capacity");
-    return true;
 }
 
 }  // namespace
@@ -1428,10 +1053,6 @@ void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const
         SLQ_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(double) * d * (A->n + 1), ctx->stream));
         return;
     }
-    // the cluster slab gather is exact without splits but, at zeta = 8 and
-    // d = 4n, slower than the register-row gather (one entry per warp
-    // instruction vs 32): opt-in for experiments only
-    if (slq_env_flag("SLQ_SLAB_GATHER") && sketch_apply_slab(ctx, A, d, compact, colptr_dev, zeta, val, exact, Y)) return;
     // fast mode: the DMMA tile gather (falls back if a bucket overflowed)
     const bool row_gather = slq_env_flag("SLQ_ROW_GATHER");  // diagnostics: register gather in fast mode
     if (!exact && !row_gather && sketch_apply_dmma(ctx, A, d, compact, colptr_dev, zeta, val, Y)) return;

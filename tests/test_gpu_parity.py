@@ -141,23 +141,6 @@ def test_apply_fast_tile_gather_tall_sketch():
     assert np.abs(Yf - Yo).max() <= tol and np.abs(Sbf - Sbo).max() <= tol
 
 
-@pytest.mark.parametrize("m,n,d,zeta", [(5000, 37, 200, 8), (4096, 64, 512, 16), (3000, 40, 9000, 4)])
-def test_apply_cluster_slab_gather(m, n, d, zeta, monkeypatch):
-    """The opt-in cluster/multicast slab gather (SLQ_SLAB_GATHER=1) is
-    bit-exact without splits in exact mode and within 1e-12 in fast mode."""
-    rng = np.random.default_rng(m + d)
-    A = np.asfortranarray(rng.standard_normal((m, n)))
-    b = rng.standard_normal(m)
-    Yo, Sbo = C.sketch_apply(d, zeta, 17, A, b)
-    dm = slq.DeviceMatrix.from_numpy(A, b)
-    monkeypatch.setenv("SLQ_SLAB_GATHER", "1")
-    Ye, Sbe = dm.sketch(d, zeta, 17, exact=True)
-    assert np.array_equal(Ye, Yo) and np.array_equal(Sbe, Sbo)
-    Yf, Sbf = dm.sketch(d, zeta, 17, exact=False)
-    tol = 1e-12 * max(1.0, np.abs(Yo).max())
-    assert np.abs(Yf - Yo).max() <= tol and np.abs(Sbf - Sbo).max() <= tol
-
-
 def test_apply_golden(golden):
     p = golden["pipeline"]
     meta = golden["meta"]["pipeline"]

@@ -6,7 +6,7 @@
 what=${1:?what}; tag=${2:-run}
 case $what in
   pass_c3)   CMD="python bench.py --no-e2e --no-cpu --steps 1 --warmup 3"; K="-k regex:fused_pass -s 6 -c 1";;
-  gather)    CMD="python tools/diag_sketch.py 1000000 1000 4000 8 fast"; K="-k gather_kernel -s 1 -c 1";;
+  gather)    CMD="python tools/diag_k2d.py 1000000 1000 4000 8"; K="-k regex:gather_dmma -s 1 -c 1";;
   panel)     CMD="python tools/diag_qr.py"; K="-k regex:panel_reg_kernel -s 4 -c 1";;
   sparse_pass) CMD="python bench.py --config c4 --no-cpu --no-e2e --steps 1 --warmup 3"; K="-k regex:sparse_pass_kernel -s 3 -c 1";;
   launches_c3) CMD="python bench.py --no-e2e --no-cpu --steps 1 --warmup 3";;
