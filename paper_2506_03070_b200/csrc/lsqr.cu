@@ -142,17 +142,35 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
             }
         }
         const double c = a.coef ? *a.coef : a.c_fixed;
+        // Short rows (many rows per warp per tile): u of this warp's rows is
+        // loaded one tile ahead, lane l holding the l-th row the warp owns
+        // (R <= 7 * 32), so no row waits on a global load.  Long rows hide the
+        // per-row load behind the row itself (and the prefetch measurably
+        // raises the sustained power draw at C3): per-row loads there.
+        const bool upre = a.u_in && a.R >= 4 * kConsumerWarps;
+        auto first_row = [&](int64_t k) {
+            return static_cast<int>(((warp - (k * a.R) % kConsumerWarps) + kConsumerWarps) % kConsumerWarps);
+        };
+        auto load_u = [&](int64_t k) -> double {
+            if (!upre || k >= nt) return 0.0;
+            const int64_t row0 = (t0 + k) * a.R;
+            const int64_t i = first_row(k) + static_cast<int64_t>(kConsumerWarps) * lane;
+            return (i < a.R && row0 + i < a.m) ? a.u_in[row0 + i] : 0.0;
+        };
+        double ucur = load_u(0);
         for (int64_t k = 0; k < nt; ++k) {
             const int s = static_cast<int>(k % a.S);
+            const double unxt = load_u(k + 1);
             mbar_wait(&full[s], static_cast<unsigned>((k / a.S) & 1));
             const double* tile = stages + s * stage_elems;
             const int64_t row0 = (t0 + k) * a.R;
             const int rows = static_cast<int>(min(static_cast<int64_t>(a.R), a.m - row0));
             // rows of this tile owned by this warp: (k*R + i) % 8 == warp
-            int i = static_cast<int>(((warp - (k * a.R) % kConsumerWarps) + kConsumerWarps) % kConsumerWarps);
-            for (; i < rows; i += kConsumerWarps) {
+            int i = first_row(k);
+            for (int t = 0; i < rows; i += kConsumerWarps, ++t) {
                 const double* row = tile + static_cast<int64_t>(i) * ld;
-                const double u = a.u_in ? a.u_in[row0 + i] : row[a.n];
+                const double u = upre ? __shfl_sync(0xffffffffu, ucur, t & 31)  // upre is CTA-uniform
+                                      : (a.u_in ? a.u_in[row0 + i] : row[a.n]);
                 double acc0 = 0.0, acc1 = 0.0;
                 double2 vr[NP];  // the row stays in registers for the z update: one shared-memory read
 #pragma unroll
@@ -178,6 +196,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
+            ucur = unxt;
         }
     }
     // park accumulators for the block reduction: stage memory is free once
@@ -504,7 +523,7 @@ PassPlan plan_pass(slq_ctx* ctx, const slq_dense* A) {
     const int64_t row_bytes = ld * static_cast<int64_t>(sizeof(double));
     int64_t R = (64 * 1024) / row_bytes;
     if (R >= 8) R = (R / 8) * 8;
-    R = std::max<int64_t>(1, std::min<int64_t>(R, 256));
+    R = std::max<int64_t>(1, std::min<int64_t>(R, 7 * 32));  // a consumer warp's rows of a tile fit one lane each
     pp.R = static_cast<int>(R);
     pp.S = 3;
     while (pp.S * pp.R < kConsumerWarps + 1) ++pp.S;  // reduction area needs >= 9 rows
