@@ -12,12 +12,17 @@
 //
 // K2 replaces csc_matrix.hpp:103-120 (spmm(csc, dense)) + csc_matrix.hpp:71-82
 // (S b): Y_aug = S [A | b].  The sketch entries are bucketed once per chunk of
-// K rows of A ("chunk-CSR": entries sorted by (target row r, k)), then each
-// CTA owns a W-column slab of Y_aug held in REGISTERS (thread t owns Y rows
-// t, t+512, ...) and streams its W-column slab of A through shared memory
-// (cp.async double buffer).  Every Y element is accumulated by one thread in
-// ascending k -- the reference's order -- with IEEE mul then add, so one
-// split reproduces the reference Y bit for bit.  No atomics anywhere.
+// K rows of A ("chunk-CSR": entries sorted by (target row r, k)).  Two gathers:
+//   * exact mode (gather_kernel): each CTA owns a W-column slab of Y_aug held
+//     in REGISTERS (thread t owns Y rows t, t+1024, ...) and streams its slab
+//     of A through shared memory (TMA / cp.async double buffer); every Y
+//     element is accumulated by one thread in ascending k -- the reference's
+//     order -- with IEEE mul then add, so one split reproduces the reference Y
+//     bit for bit;
+//   * fast mode (gather_dmma_kernel, K2d): the chunk's entries are regrouped
+//     per 8-row tile (tile_repack_kernel) and applied on the FP64 tensor cores
+//     (see the K2d section below).
+// No atomics anywhere; both are deterministic.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
