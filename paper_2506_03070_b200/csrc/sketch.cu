@@ -522,7 +522,7 @@ __global__ void reduce_splits_kernel(const double* Yw, int64_t nsplit, int64_t d
 // Fast-mode S.[A b] on the FP64 tensor cores.  A CTA owns a 16-column slab of
 // Y_aug for a block of 1024 rows, held as 128 8x8 row tiles x 2 column tiles
 // of mma.m8n8k4 accumulators (warp w owns row tiles w, w+32, w+64, w+96).  Per
-// chunk of K <= 512 rows of A, the slab segment (K x 128 B) arrives by TMA with
+// chunk of K <= 768 rows of A, the slab segment (K x 128 B) arrives by TMA with
 // the 128-byte swizzle, together with the chunk's entries for this row block
 // grouped by row tile and padded to multiples of 4 (tile_repack_kernel).  One
 // group of 4 entries is one k-step: A-fragment = the 8x4 block of S (entry j's
@@ -551,7 +551,7 @@ struct RepackArgs {
 
 // one CTA per chunk: thread (rb % 8, tile) counts its tile's entries, pads to
 // a multiple of 4, a per-row-block scan places it; entries are re-encoded as
-// k_local | row_in_tile << 9 | valid << 12 | neg << 15 (0 = padding).
+// k_local | row_in_tile << 10 | valid << 13 | neg << 15 (0 = padding).
 __global__ void __launch_bounds__(1024) tile_repack_kernel(RepackArgs a) {
     __shared__ int wsum[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(1024) tile_repack_kernel(RepackArgs a) {
                     if (r >= a.d) break;
                     for (int e = ptr[r]; e < ptr[r + 1]; ++e, ++j) {
                         const unsigned kv = ent[e];
-                        eo[j] = static_cast<uint16_t>((kv >> 1) | (rr << 9) | 0x1000u | ((kv & 1u) << 15));
+                        eo[j] = static_cast<uint16_t>((kv >> 1) | (rr << 10) | 0x2000u | ((kv & 1u) << 15));
                     }
                 }
                 for (; j < pad; ++j) eo[j] = 0;
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(1024) tile_repack_kernel(RepackArgs a) {
 
 struct TdArgs {
     int64_t m, d, ldw;
-    int K;
+    int K, box;  // rows per chunk, rows per TMA box (K is a multiple of box)
     int64_t nsplit, c_lo, c_hi;
     const uint16_t* tiles;
     int64_t blk_stride;
@@ -653,14 +653,14 @@ __global__ void __launch_bounds__(1024, 1) gather_dmma_kernel(const __grid_const
     auto issue = [&](int64_t c, int s) {  // one thread
         const int64_t k0 = c * g.K;
         const int kc = static_cast<int>(min(static_cast<int64_t>(g.K), g.m - k0));
-        const int nbox = (kc + 255) >> 8;
+        const int nbox = (kc + g.box - 1) / g.box;
         const unsigned tb = static_cast<unsigned>(g.blk_stride * 2);
-        ptx::mbar_expect_tx(&full[s], static_cast<unsigned>(nbox * 256 * 128) + tb);
+        ptx::mbar_expect_tx(&full[s], static_cast<unsigned>(nbox * g.box * 128) + tb);
         for (int bx = 0; bx < nbox; ++bx)
             asm volatile(
                 "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-                    ptx::smem_u32(As(s) + static_cast<size_t>(bx) * 256 * 128)),
-                "l"(&tmap), "r"(static_cast<int>(col0)), "r"(static_cast<int>(k0 + 256 * bx)), "r"(ptx::smem_u32(&full[s]))
+                    ptx::smem_u32(As(s) + static_cast<size_t>(bx) * g.box * 128)),
+                "l"(&tmap), "r"(static_cast<int>(col0)), "r"(static_cast<int>(k0 + g.box * bx)), "r"(ptx::smem_u32(&full[s]))
                 : "memory");
         ptx::bulk_g2s(const_cast<uint16_t*>(Ts(s)), g.tiles + (c * g.nrb + rb) * g.blk_stride, tb, &full[s]);
     };
@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(1024, 1) gather_dmma_kernel(const __grid_const
     if (tid == 0)
         for (int s = 0; s < g.ns && cb + s < ce; ++s) issue(cb + s, s);
     const unsigned vhi = static_cast<unsigned>(__double2hiint(g.val)), vlo = static_cast<unsigned>(__double2loint(g.val));
-    const unsigned rowkey = 0x1000u | (static_cast<unsigned>(lg) << 9);  // valid | row lg
+    const unsigned rowkey = 0x2000u | (static_cast<unsigned>(lg) << 10);  // valid | row lg
     const unsigned lgu = static_cast<unsigned>(lg);
     int s = 0;
     unsigned phase = 0;
@@ -690,14 +690,14 @@ __global__ void __launch_bounds__(1024, 1) gather_dmma_kernel(const __grid_const
                 // A-fragment: +-val where the entry's row is this lane's row lg
                 // (valid bit and row compared in one mask), 0 elsewhere -- built
                 // on the high word: sign flip by XOR, zero by AND
-                const unsigned hit = ((en & 0x1e00u) == rowkey) ? 0xffffffffu : 0u;
+                const unsigned hit = ((en & 0x3c00u) == rowkey) ? 0xffffffffu : 0u;
                 const unsigned hi = (vhi ^ ((en & 0x8000u) << 16)) & hit;
                 const double a = __hiloint2double(static_cast<int>(hi), static_cast<int>(vlo & hit));
                 // B-fragments: column tile 0 = the slab's even columns, tile 1 =
                 // its odd columns, so lane lg's two operands (columns 2lg and
                 // 2lg + 1 of row k) are one 16-byte unit: unit lg ^ (k & 7) of
                 // the 128-byte-swizzled row, one LDS.128 for both DMMAs
-                const unsigned k = en & 511u;
+                const unsigned k = en & 1023u;
                 const double2 bb = *reinterpret_cast<const double2*>(Ab + ((k << 7) | (((lgu ^ k) & 7u) << 4)));
                 dmma_f64(acc[q][0][0], acc[q][0][1], a, bb.x);
                 dmma_f64(acc[q][1][0], acc[q][1][1], a, bb.y);
@@ -797,7 +797,8 @@ ChunkPlan plan_chunks(int64_t m, int64_t d, int64_t zeta_max, int W) {
 // 2D tensor map over the row-major A block (inner dim = ld columns, outer = m
 // rows), boxes of 256 rows x W columns, no swizzle (the gather's entries hold
 // plain byte offsets k * 8W).
-CUtensorMap gather_tensor_map(const double* A, int64_t ld, int64_t m, int W, bool swizzle128 = false) {
+CUtensorMap gather_tensor_map(const double* A, int64_t ld, int64_t m, int W, bool swizzle128 = false,
+                              unsigned box_rows = 256) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -810,7 +811,7 @@ CUtensorMap gather_tensor_map(const double* A, int64_t ld, int64_t m, int W, boo
     if (W < 2) return map;  // 1-column slabs stage with cp.async
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(std::max<int64_t>(m, 1))};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(double)};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(W), 256u};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(W), box_rows};
     const cuuint32_t estr[2] = {1u, 1u};
     const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -895,8 +896,14 @@ bool sketch_apply_dmma(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32
     int zp = 1;
     while (zp < zeta_max) zp <<= 1;
     ChunkPlan p{};
-    p.K = 512;
-    while (p.K > 16 && static_cast<int64_t>(p.K) * zp > 16384) p.K >>= 1;
+    // K rows per chunk: 768 (k_local < 1024, 10 bits of a tile entry; 3 TMA
+    // boxes) when the chunk's K * zeta entries fit a u16 chunk-CSR, else the
+    // largest power of two that does; boxes of min(256, K) rows
+    p.K = 768;
+    if (static_cast<int64_t>(p.K) * zp > 16384) {
+        p.K = 512;
+        while (p.K > 16 && static_cast<int64_t>(p.K) * zp > 16384) p.K >>= 1;
+    }
     p.KB = 0;
     while ((1 << p.KB) < p.K) ++p.KB;
     p.cap = 16384;
@@ -941,10 +948,11 @@ bool sketch_apply_dmma(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32
     }
     double* Yw = (nsplit == 1 && ldw == ncols_out) ? Y
                  : static_cast<double*>(ws.ypart.ensure(sizeof(double) * nsplit * ldw * d));
-    TdArgs g{m, d, ldw, p.K, nsplit, 0, p.nchunks, tiles, blk_stride, nrb, ns, val, Yw};
+    const int box = std::min(256, p.K);
+    TdArgs g{m, d, ldw, p.K, box, nsplit, 0, p.nchunks, tiles, blk_stride, nrb, ns, val, Yw};
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(gather_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
-    const CUtensorMap map = gather_tensor_map(A->A, ld, m, 16, true);
+    const CUtensorMap map = gather_tensor_map(A->A, ld, m, 16, true, static_cast<unsigned>(box));
     gather_dmma_kernel<<<dim3(static_cast<unsigned>(nrb), static_cast<unsigned>(nslabs), static_cast<unsigned>(nsplit)),
                          1024, smem, ctx->stream>>>(map, g);
     SLQ_LAUNCH_CHECK(ctx);
@@ -1058,8 +1066,13 @@ void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const
         SLQ_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(double) * d * (A->n + 1), ctx->stream));
         return;
     }
-    // fast mode: the DMMA tile gather (falls back if a bucket overflowed)
-    const bool row_gather = slq_env_flag("SLQ_ROW_GATHER");  // diagnostics: register gather in fast mode
+    // fast mode: the DMMA tile gather (falls back if a bucket overflowed),
+    // except where the register gather measured faster (tools/diag_k2d.py at
+    // m = 1e6, n = 500: zeta >= 16 with d <= 2048 -- many entries per row per
+    // chunk keep its lanes busy; zeta <= 2 with d >= 2048 -- too little work
+    // per A row to repay the tile gather's per-row-block restaging)
+    const bool row_gather = slq_env_flag("SLQ_ROW_GATHER") ||  // diagnostics: register gather in fast mode
+                            (zeta >= 16 && d <= 2048) || (zeta <= 2 && d >= 2048);
     if (!exact && !row_gather && sketch_apply_dmma(ctx, A, d, compact, colptr_dev, zeta, val, Y)) return;
     DenseGather G = dense_gather_plan(ctx, m, A->n, A->ld, d, compact, colptr_dev, zeta, val, exact, Y, false);
     dense_gather_rows(ctx, G, A->A, 0, m);
