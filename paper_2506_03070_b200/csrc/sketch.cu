@@ -604,6 +604,137 @@ __global__ void __launch_bounds__(1024) tile_repack_kernel(RepackArgs a) {
     }
 }
 
+// Fused bucketing for K2d (uniform zeta, the device-generated sketch): one CTA
+// per chunk places the chunk's K*zeta entries straight into the tile layout,
+// in entry order (stable, deterministic), without the chunk-CSR round trip:
+// per-warp tile histograms (u16 pairs in smem), padded tile offsets by a scan
+// per row block, then each warp re-walks its entry range and places entries
+// at (its base for the tile) + (rank among equal tiles in the round, by
+// __match_any_sync).  d <= 16 * 1024 (2048 tiles) keeps the histograms in smem.
+struct TileBucketArgs {
+    const uint32_t* compact;
+    int64_t zeta, ncols, d;
+    int K, nrb, cap;
+    int64_t blk_stride;
+    uint16_t* out;
+    int* flag;
+};
+constexpr int kTbMaxTiles = 2048;
+
+__global__ void __launch_bounds__(1024) tile_bucketize_kernel(TileBucketArgs a) {
+    extern __shared__ int tbsm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ntile = static_cast<int>((a.d + 7) >> 3);
+    const int nhp = (ntile + 1) >> 1;                 // packed u16 pairs per warp
+    int* hist = tbsm;                                 // [32][nhp] packed counts, later bases
+    int* off = hist + 32 * nhp;                       // [ntile] padded offset in the row block
+    int* tot = off + ntile;                           // [ntile]
+    int* rbt = tot + ntile;                           // [nrb] padded total per row block
+    const int64_t c = blockIdx.x;
+    const int64_t k0 = c * a.K;
+    const int64_t kc = min(static_cast<int64_t>(a.K), a.ncols - k0);
+    const int N = static_cast<int>(kc * a.zeta);
+    const uint32_t* src = a.compact + k0 * a.zeta;
+    const int per = (N + 31) / 32;
+    const int wb = warp * per, we = min(N, wb + per);
+    for (int i = tid; i < 32 * nhp; i += 1024) hist[i] = 0;
+    __syncthreads();
+    int* hw = hist + warp * nhp;
+    for (int e = wb + lane; e < we; e += 32) {
+        const int t = static_cast<int>((src[e] & 0x7fffffffu) >> 3);
+        atomicAdd(&hw[t >> 1], 1 << (16 * (t & 1)));
+    }
+    __syncthreads();
+    auto cnt = [&](int w, int t) { return (hist[w * nhp + (t >> 1)] >> (16 * (t & 1))) & 0xffff; };
+    for (int t = tid; t < ntile; t += 1024) {
+        int s = 0;
+        for (int w = 0; w < 32; ++w) s += cnt(w, t);
+        tot[t] = s;
+    }
+    __syncthreads();
+    // padded offsets: warp r scans row block r's 128 tiles (4 per lane)
+    for (int rb = warp; rb < a.nrb; rb += 32) {
+        const int t0 = rb * kTdTiles;
+        int v[4], sum = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = t0 + 4 * lane + q;
+            v[q] = t < ntile ? (tot[t] + 3) & ~3 : 0;
+            sum += v[q];
+        }
+        int x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        int run = x - sum;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = t0 + 4 * lane + q;
+            if (t < ntile) off[t] = run;
+            run += v[q];
+        }
+        if (lane == 31) rbt[rb] = x;
+    }
+    __syncthreads();
+    // per-warp bases (in place, packed u16): base(w, t) = off[t] + counts of
+    // warps < w; one thread per word (tile pair)
+    for (int hp = tid; hp < nhp; hp += 1024) {
+        const int ta = 2 * hp, tb2 = ta + 1;
+        int runa = off[ta], runb = tb2 < ntile ? off[tb2] : 0;
+        for (int w = 0; w < 32; ++w) {
+            const int word = hist[w * nhp + hp];
+            const int ca = word & 0xffff, cb = (word >> 16) & 0xffff;
+            hist[w * nhp + hp] = (runa & 0xffff) | ((runb & 0xffff) << 16);
+            runa += ca;
+            runb += cb;
+        }
+    }
+    __syncthreads();
+    bool over = false;
+    for (int rb = 0; rb < a.nrb; ++rb) over |= rbt[rb] > a.cap;
+    if (over) {  // flag it (the caller falls back) and leave empty tiles behind
+        if (tid == 0) atomicExch(a.flag, 1);
+        for (int i = tid; i < a.nrb * (kTdTiles + 1); i += 1024)
+            a.out[(c * a.nrb + i / (kTdTiles + 1)) * a.blk_stride + i % (kTdTiles + 1)] = 0;
+        return;
+    }
+    // placement, entry order (warp range, then round, then lane)
+    const int zeta = static_cast<int>(a.zeta);
+    for (int e0 = wb; e0 < we; e0 += 32) {
+        const int e = e0 + lane;
+        const bool live = e < we;
+        const uint32_t en = live ? src[e] : 0u;
+        const int r = static_cast<int>(en & 0x7fffffffu);
+        const int t = live ? (r >> 3) : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, t);
+        if (live) {
+            const int rank = __popc(peers & ((1u << lane) - 1u));
+            const int sh = 16 * (t & 1);
+            const int base = (hw[t >> 1] >> sh) & 0xffff;
+            const int rb = t / kTdTiles;
+            const unsigned kl = static_cast<unsigned>(e / zeta);
+            a.out[(c * a.nrb + rb) * a.blk_stride + kTdHdr + base + rank] =
+                static_cast<uint16_t>(kl | (static_cast<unsigned>(r & 7) << 10) | 0x2000u | ((en >> 31) << 15));
+            if (rank == 0) atomicAdd(&hw[t >> 1], __popc(peers) << sh);  // the group's leader advances the base
+        }
+        __syncwarp();
+    }
+    // padding and headers
+    for (int t = tid; t < ntile; t += 1024) {
+        uint16_t* blk = a.out + (c * a.nrb + t / kTdTiles) * a.blk_stride;
+        blk[t % kTdTiles] = static_cast<uint16_t>(off[t]);
+        const int pe = (tot[t] + 3) & ~3;
+        for (int j = tot[t]; j < pe; ++j) blk[kTdHdr + off[t] + j] = 0;
+    }
+    for (int i = tid; i < a.nrb * kTdTiles; i += 1024) {  // tiles past d (last row block)
+        const int t = i;
+        if (t >= ntile) a.out[(c * a.nrb + t / kTdTiles) * a.blk_stride + t % kTdTiles] = static_cast<uint16_t>(rbt[t / kTdTiles]);
+    }
+    for (int rb = tid; rb < a.nrb; rb += 1024) a.out[(c * a.nrb + rb) * a.blk_stride + kTdTiles] = static_cast<uint16_t>(rbt[rb]);
+}
+
 struct TdArgs {
     int64_t m, d, ldw;
     int K, box;  // rows per chunk, rows per TMA box (K is a multiple of box)
@@ -910,8 +1041,6 @@ bool sketch_apply_dmma(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32
     p.nchunks = ceil_div(m, static_cast<int64_t>(p.K));
     p.ptr_stride = round_up(d + 1, 8);
     p.ent_stride = round_up(static_cast<int64_t>(p.K) * zeta_max, 8);
-    ChunkCsr cc = build_chunk_csr_plan(ctx, compact, colptr_dev, zeta_max, m, d, 0, p);
-
     const int nrb = static_cast<int>(ceil_div(d, static_cast<int64_t>(kTdRows)));
     const int64_t rows_rb = std::min<int64_t>(kTdRows, d);
     const int64_t expect = static_cast<int64_t>(p.K) * zeta_max * rows_rb / d;
@@ -919,11 +1048,25 @@ bool sketch_apply_dmma(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32
     const int64_t blk_stride = kTdHdr + cap;
     Workspace& ws = ctx->ws;
     uint16_t* tiles = static_cast<uint16_t*>(ws.tile_ent.ensure(sizeof(uint16_t) * p.nchunks * nrb * blk_stride));
-    int* flag = cc.flag + 1;
-    SLQ_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
-    RepackArgs ra{cc.ptr, cc.ent, p.ptr_stride, p.ent_stride, d, nrb, static_cast<int>(cap), blk_stride, tiles, flag};
-    tile_repack_kernel<<<static_cast<unsigned>(p.nchunks), 1024, 0, ctx->stream>>>(ra);
-    SLQ_LAUNCH_CHECK(ctx);
+    int* flags = static_cast<int*>(ws.flags.ensure(4096));
+    SLQ_CUDA_CHECK(cudaMemsetAsync(flags, 0, 2 * sizeof(int), ctx->stream));
+    const int64_t ntile = ceil_div(d, static_cast<int64_t>(8));
+    if (!colptr_dev && ntile <= kTbMaxTiles) {
+        // uniform zeta: one fused pass from the generator's entries to the tile layout
+        TileBucketArgs ta{compact, zeta_max, m, d, p.K, nrb, static_cast<int>(cap), blk_stride, tiles, flags + 1};
+        const int64_t nhp = (ntile + 1) / 2;
+        const size_t tsmem = sizeof(int) * (32 * nhp + 2 * ntile + nrb);
+        SLQ_CUDA_CHECK(cudaFuncSetAttribute(tile_bucketize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(tsmem)));
+        tile_bucketize_kernel<<<static_cast<unsigned>(p.nchunks), 1024, tsmem, ctx->stream>>>(ta);
+        SLQ_LAUNCH_CHECK(ctx);
+    } else {
+        ChunkCsr cc = build_chunk_csr_plan(ctx, compact, colptr_dev, zeta_max, m, d, 0, p);
+        RepackArgs ra{cc.ptr, cc.ent, p.ptr_stride, p.ent_stride, d, nrb, static_cast<int>(cap), blk_stride, tiles,
+                      flags + 1};
+        tile_repack_kernel<<<static_cast<unsigned>(p.nchunks), 1024, 0, ctx->stream>>>(ra);
+        SLQ_LAUNCH_CHECK(ctx);
+    }
 
     const int64_t ldw = round_up(ncols_out, 16);
     const int64_t nslabs = ldw / 16;
@@ -957,7 +1100,7 @@ bool sketch_apply_dmma(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32
                          1024, smem, ctx->stream>>>(map, g);
     SLQ_LAUNCH_CHECK(ctx);
     int hflag[2] = {0, 0};
-    SLQ_CUDA_CHECK(cudaMemcpyAsync(hflag, cc.flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(hflag, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     if (hflag[0] || hflag[1]) return false;
     if (Yw != Y) {
