@@ -1044,7 +1044,8 @@ bool sketch_apply_dmma(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32
     const int nrb = static_cast<int>(ceil_div(d, static_cast<int64_t>(kTdRows)));
     const int64_t rows_rb = std::min<int64_t>(kTdRows, d);
     const int64_t expect = static_cast<int64_t>(p.K) * zeta_max * rows_rb / d;
-    const int64_t cap = round_up(std::min<int64_t>(static_cast<int64_t>(p.K) * zeta_max, 2 * expect + 256) + 3 * kTdTiles, 8);
+    int64_t cap = round_up(std::min<int64_t>(static_cast<int64_t>(p.K) * zeta_max, 2 * expect + 256) + 3 * kTdTiles, 8);
+    if (const char* e = std::getenv("SLQ_TD_CAP")) cap = std::max<int64_t>(8, round_up(std::atoll(e), 8));  // tests: force overflow
     const int64_t blk_stride = kTdHdr + cap;
     Workspace& ws = ctx->ws;
     uint16_t* tiles = static_cast<uint16_t*>(ws.tile_ent.ensure(sizeof(uint16_t) * p.nchunks * nrb * blk_stride));

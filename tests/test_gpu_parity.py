@@ -128,6 +128,20 @@ def test_apply_fast_tile_gather(m, n, d, zeta, monkeypatch):
     assert np.abs(Yf - Yr).max() <= tol and np.abs(Sbf - Sbr).max() <= tol
 
 
+def test_apply_fast_tile_gather_overflow_falls_back(monkeypatch):
+    """A row block whose entries overflow the tile bucket (forced with a tiny
+    SLQ_TD_CAP) is detected and the apply is redone by the register gather."""
+    m, n, d, zeta = 3000, 20, 600, 8
+    rng = np.random.default_rng(9)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    b = rng.standard_normal(m)
+    Yo, Sbo = C.sketch_apply(d, zeta, 41, A, b)
+    monkeypatch.setenv("SLQ_TD_CAP", "64")
+    Yf, Sbf = slq.DeviceMatrix.from_numpy(A, b).sketch(d, zeta, 41, exact=False)
+    tol = 1e-12 * max(1.0, np.abs(Yo).max())
+    assert np.abs(Yf - Yo).max() <= tol and np.abs(Sbf - Sbo).max() <= tol
+
+
 def test_apply_fast_tile_gather_tall_sketch():
     """d = 20000 is past the register gather's envelope (d <= 16384); the
     tile gather covers it in fast mode (20 row blocks of 1024)."""
