@@ -109,7 +109,7 @@ def test_apply_exact(m, n, d, zeta):
 
 
 @pytest.mark.parametrize("m,n,d,zeta", [(513, 16, 1030, 8), (1, 5, 40, 3), (2000, 47, 8, 8), (7000, 15, 2100, 32),
-                                        (1537, 33, 1500, 2)])
+                                        (1537, 33, 1500, 2), (2000, 10, 3000, 64), (900, 6, 700, 1)])
 def test_apply_fast_tile_gather(m, n, d, zeta, monkeypatch):
     """Fast mode runs the DMMA tile gather (K2d); it must agree with the
     reference order to 1e-12 and with the register gather (SLQ_ROW_GATHER=1):
