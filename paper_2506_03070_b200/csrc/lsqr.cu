@@ -6,12 +6,13 @@
 //
 //   K4 fused_pass  : one HBM pass over A per iteration.  Each row tile of A
 //                    (TMA bulk copy into a 3-stage smem ring, mbarrier
-//                    full/empty pipeline, one producer warp) is used twice
-//                    from shared memory: u_hat_i = A_i p + c u_i (warp dot +
-//                    shuffle reduce), then z += A_i^T u_hat_i (register
-//                    accumulators), plus ||u_hat||^2.  u is never rescaled
-//                    in memory: u_true = su * u_hat is carried as a scalar
-//                    and folded into the next pass's coefficient c.
+//                    full/empty pipeline, one producer warp) is read once
+//                    from shared memory into registers and used twice:
+//                    u_hat_i = A_i p + c u_i (warp dot + shuffle reduce), then
+//                    z += A_i^T u_hat_i (register accumulators), plus
+//                    ||u_hat||^2.  u is never rescaled in memory: u_true =
+//                    su * u_hat is carried as a scalar and folded into the
+//                    next pass's coefficient c.
 //   reduce         : per-CTA partials -> [A^T u_hat | ||u_hat||^2] (fixed order);
 //                    multi-GPU: ONE ncclAllReduce of n+1 doubles here.
 //   mtz            : v_hat = M^T z - beta v (warp per column of M), ||v_hat||^2,
