@@ -332,6 +332,23 @@ def test_solve_pipeline_c1_small():
     assert times["kernel_launches"] > 0
 
 
+def test_solve_deterministic_across_runs_and_contexts():
+    """Every reduction is in a fixed order (no atomics on floating-point data):
+    repeated fast-mode solves -- same context and a fresh one -- return
+    bit-identical x and residual histories."""
+    m, n, d, zeta = 60000, 120, 480, 8
+    rng = np.random.default_rng(17)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    b = rng.standard_normal(m)
+    opts = slq.SolveOptions(eps=0.0, maxit=15)
+    x1, r1, _ = slq.solve(A, d, zeta, 5, opts, b=b)
+    x2, r2, _ = slq.solve(A, d, zeta, 5, opts, b=b)
+    x3, r3, _ = slq.solve(A, d, zeta, 5, opts, b=b, ctx=slq.Context(0))
+    assert np.array_equal(x1, x2) and np.array_equal(x1, x3)
+    assert np.array_equal(r1.residual_estimate, r2.residual_estimate)
+    assert np.array_equal(r1.residual_estimate, r3.residual_estimate)
+
+
 @pytest.mark.parametrize("block_rows", [None, "5000"])
 def test_solve_host_streams_blocks(block_rows, monkeypatch):
     """slq_solve_host (e2e path): A uploaded block by block from a column-major
