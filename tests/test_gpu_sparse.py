@@ -90,6 +90,9 @@ def test_sparse_solve_pipeline():
     assert rep.iterations == 25
     assert eta(x) <= max(2 * eta(xo), 1e-14)
     assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
+    # fixed-order reductions throughout: a repeat solve is bit-identical
+    x2, rep2, _ = slq.solve(Acsc, d, zeta, 9, slq.SolveOptions(eps=0.0, maxit=25), b=b)
+    assert np.array_equal(x, x2) and np.array_equal(rep.residual_estimate, rep2.residual_estimate)
 
 
 def test_sparse_lsqr_long_rows():
