@@ -1,4 +1,4 @@
-"""Multi-process (world_size 2, gloo, CPU) test of the row-partitioned path's
+"""Multi-process (world_size 2 and 7, gloo, CPU) test of the row-partitioned path's
 host logic -- the same decomposition the NCCL path runs on B200s:
 
   * rows partitioned by partition_rows (distsim.hpp:31-42, via the C-ABI);
@@ -146,10 +146,10 @@ def _worker(rank, world, port, results):
         dist.destroy_process_group()
 
 
-def test_row_partitioned_pipeline_gloo_world2():
+@pytest.mark.parametrize("world", [2, 7])  # 7: 600 rows -> 6 blocks of 85 + a last block of 90 (partition_rows)
+def test_row_partitioned_pipeline_gloo(world):
     import oracle
 
-    world = 2
     mgr = mp.Manager()
     results = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), results), nprocs=world, join=True)
@@ -179,7 +179,8 @@ def test_row_partitioned_pipeline_gloo_world2():
         assert np.linalg.norm(res["xg"] - xgs) <= 1e-10 * max(1.0, np.linalg.norm(xgs))
         assert np.allclose(res["ghist"], greps.residual_estimate, rtol=1e-9)
         assert res["g_allreduces"] == 12
-    assert np.array_equal(results[0]["xg"], results[1]["xg"])
     # replicated state is bitwise identical on every rank (allreduce/broadcast semantics)
-    assert np.array_equal(results[0]["x"], results[1]["x"])
-    assert np.array_equal(results[0]["M"], results[1]["M"])
+    for r in range(1, world):
+        assert np.array_equal(results[0]["xg"], results[r]["xg"])
+        assert np.array_equal(results[0]["x"], results[r]["x"])
+        assert np.array_equal(results[0]["M"], results[r]["M"])
