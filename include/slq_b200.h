@@ -209,8 +209,13 @@ typedef struct {
     int32_t track_true_residual; /* lsqr.hpp:18 record ||b - A x_t|| */
     int32_t one_sync;        /* lsqr_one_sync (lsqr.hpp:185) vs lsqr (lsqr.hpp:175) */
     /* extension (off by default): also stop when the backward error
-     * ||A^T r|| / (||A|| ||r||), estimated by Paige-Saunders and confirmed
-     * by one direct A^T r pass, is <= backward_tol (a_norm_est = ||A||_2). */
+     * ||A^T r|| / (||A|| ||r||) is <= backward_tol.  The device triggers on
+     * the Paige-Saunders estimate alpha_{t+1} |c_t| <= trigger (initially
+     * backward_tol); the host then measures the backward error with one
+     * direct A^T r pass (a_norm_est = ||A||_2, 1 if 0) and accepts
+     * (termination Tolerance, report.backward_error set) or resumes with a
+     * trigger tightened by the measured ratio.  a_norm_est > 0 alone only
+     * reports the backward error at exit. */
     double backward_tol;
     double a_norm_est;
     /* lsqr.hpp:21 on_bidiag hook: called after each iteration with the

@@ -325,6 +325,16 @@ int run_solve(slq_ctx* ctx, const Operand& A, int64_t d, int64_t zeta, uint64_t 
                 if (!ctx->comm) throw;
                 st = e.code;
                 g_last_error = e.what();
+            } catch (const std::bad_alloc&) {
+                // any failure on rank 0 must still reach the status broadcast,
+                // or ranks 1..N-1 would block in ncclBroadcast forever
+                if (!ctx->comm) throw;
+                st = SLQ_OOM;
+                g_last_error = "preconditioner build: host allocation failed";
+            } catch (const std::exception& e) {
+                if (!ctx->comm) throw;
+                st = SLQ_CUDA;
+                g_last_error = e.what();
             }
             if (ctx->comm) {
                 SLQ_CUDA_CHECK(cudaMemcpyAsync(P.status, &st, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
@@ -351,8 +361,8 @@ int run_solve(slq_ctx* ctx, const Operand& A, int64_t d, int64_t zeta, uint64_t 
         slq::lsqr_dev(ctx, *op, nullptr, P.M, P.Mt, P.x0, x, opts, est, nullptr, nullptr, lo);
         mark("lsqr");
         Timer t6(ctx->stream);
-        if (opts.backward_tol > 0.0 || opts.a_norm_est > 0.0)
-            lo.backward_error = slq::backward_error_dev(ctx, *op, x, opts.a_norm_est > 0.0 ? opts.a_norm_est : 1.0);
+        if ((opts.backward_tol > 0.0 || opts.a_norm_est > 0.0) && lo.backward_error < 0.0)
+            lo.backward_error = slq::backward_error_dev(ctx, *op, nullptr, x, opts.a_norm_est > 0.0 ? opts.a_norm_est : 1.0);
         if (x_out) SLQ_CUDA_CHECK(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
         fill_report(report, lo);
         mark("finish");
@@ -585,6 +595,7 @@ int slq_dense_create(slq_ctx* ctx, int64_t m, int64_t n, int64_t row_begin, slq_
         h->ld = slq::dense_ld(n);
         h->row_begin = row_begin;
         h->owned = true;
+        h->has_b = true;  // the caller fills column n (zero until then)
         cudaError_t e = cudaMalloc(&h->A, sizeof(double) * std::max<int64_t>(1, m * h->ld));
         if (e != cudaSuccess) {
             delete h;
@@ -613,6 +624,13 @@ int slq_dense_wrap(slq_ctx* ctx, double* dev_ptr, int64_t m, int64_t n, int64_t 
         h->row_begin = row_begin;
         h->owned = false;
         h->has_b = true;
+        // The passes multiply the padding columns (n, ld) by p = 0: zero them so
+        // that non-finite garbage in caller storage cannot poison u_hat (0 * NaN).
+        if (m > 0 && ld > n + 1) {
+            SLQ_CUDA_CHECK(cudaMemset2DAsync(dev_ptr + n + 1, sizeof(double) * ld, 0, sizeof(double) * (ld - n - 1), m,
+                                             ctx->stream));
+            SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        }
         *out = h;
     });
 }
@@ -842,6 +860,10 @@ int slq_solve(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, uint64_
               double* x_out, slq_report* report, slq_phase_times* times, double* residual_estimate) {
     if (!ctx || !A) {
         g_last_error = "solve: null handle";
+        return SLQ_INVALID_ARG;
+    }
+    if (!A->has_b) {
+        g_last_error = "solve: the matrix has no right-hand side (slq_dense_set_rhs)";
         return SLQ_INVALID_ARG;
     }
     return run_solve(ctx, dense_operand(ctx, A), d, zeta, seed, opts, x_out, report, times, residual_estimate);

@@ -43,13 +43,15 @@ struct LsqrState {
     double coef_x;   // phi / rho
     double coef_w;   // -theta / rho
     double eps;
+    double bw_trigger;  // opt-in backward-error rule: trigger when alpha_{t+1} |c_t| <= bw_trigger (0 = off)
+    double bw_est;      // last alpha_{t+1} |c_t| (Paige-Saunders, preconditioned relative residual)
     int64_t t;       // current iteration (1-based); 0 during init
     int64_t maxit;
     int64_t iters;
     int done;
     int term;
     int mode;
-    int pad;
+    int bw_hit;      // stopped on the backward-error trigger: the host confirms with one direct pass
     unsigned counter_mtz;
     unsigned counter_mv;
 };
@@ -364,10 +366,18 @@ __device__ void scalar_step(const MtzArgs& a, double beta, double alpha_next) {
     st.c_next = -alpha_next * (1.0 / beta);
     a.est_hist[t - 1] = st.phi_bar;
     st.mode = kModeIter;
+    // ||(AM)^T r_t|| / ||r_t|| = alpha_{t+1} |c_t| (Paige & Saunders; ||r_t|| ~ phi_bar_{t+1})
+    st.bw_est = alpha_next * fabs(c);
     if (st.phi_bar <= st.eps * st.beta1) {  // lsqr.hpp:163
         st.done = 1;
         st.term = SLQ_TERM_TOLERANCE;
         st.iters = t;
+    } else if (st.bw_trigger > 0.0 && st.bw_est <= st.bw_trigger) {
+        // extension (slq_solve_opts.backward_tol): candidate stop, confirmed on the host
+        st.done = 1;
+        st.term = SLQ_TERM_TOLERANCE;
+        st.iters = t;
+        st.bw_hit = 1;
     } else if (t >= st.maxit) {
         st.done = 1;
         st.term = SLQ_TERM_MAXITER;
@@ -623,6 +633,7 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
     LsqrState h{};
     h.eps = opts.eps;
     h.maxit = maxit;
+    h.bw_trigger = opts.backward_tol > 0.0 ? opts.backward_tol : 0.0;
     SLQ_CUDA_CHECK(cudaMemcpyAsync(B.st, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
     SLQ_CUDA_CHECK(cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
     const int* done_flag = &B.st->done;
@@ -726,30 +737,35 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
     };
 
     LsqrState hs{};
-    if (instrument) {
-        for (int64_t t = 1; t <= maxit; ++t) {
-            SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, B.st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
-            SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-            if (hs.done) break;
-            enqueue_iteration();
-            if (ctx->comm) ++allreduces;
-            SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, B.st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
-            SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-            if (opts.on_bidiag && hs.mode != kModeFinal) {
-                // recomputed norms of u_{t+1} = u_hat / beta and v_{t+1}
-                norm_scaled_kernel<<<1, 1024, 0, ctx->stream>>>(B.u, m, B.zt + n, 0, B.scal + 4);
-                norm_scaled_kernel<<<1, 1024, 0, ctx->stream>>>(B.v, n, nullptr, 1, B.scal + 5);
-                ctx->launches += 2;
-                allreduce_sum(ctx, B.scal + 4, 1);
-                double nn[2];
-                SLQ_CUDA_CHECK(cudaMemcpyAsync(nn, B.scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    // Runs iterations until the device state says done (at most `remaining`).
+    auto run_loop = [&](int64_t t_first, int64_t remaining) {
+        if (instrument) {
+            for (int64_t t = t_first; t < t_first + remaining; ++t) {
+                SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, B.st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
                 SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-                opts.on_bidiag(opts.on_bidiag_user, t, std::sqrt(nn[0]), std::sqrt(nn[1]));
+                if (hs.done) break;
+                enqueue_iteration();
+                if (ctx->comm) ++allreduces;
+                SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, B.st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+                SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+                // the reference returns before the hook on a breakdown (lsqr.hpp:120-141)
+                if (opts.on_bidiag && !(hs.done && hs.term == SLQ_TERM_BREAKDOWN)) {
+                    // recomputed norms of u_{t+1} = u_hat / beta and v_{t+1}
+                    norm_scaled_kernel<<<1, 1024, 0, ctx->stream>>>(B.u, m, B.zt + n, 0, B.scal + 4);
+                    norm_scaled_kernel<<<1, 1024, 0, ctx->stream>>>(B.v, n, nullptr, 1, B.scal + 5);
+                    ctx->launches += 2;
+                    allreduce_sum(ctx, B.scal + 4, 1);
+                    double nn[2];
+                    SLQ_CUDA_CHECK(cudaMemcpyAsync(nn, B.scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+                    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+                    opts.on_bidiag(opts.on_bidiag_user, t, std::sqrt(nn[0]), std::sqrt(nn[1]));
+                }
+                // the mv_update of this iteration has run: x_t is current
+                if (opts.x_star || opts.track_true_residual) record();
             }
-            // the mv_update of this iteration has run: x_t is current
-            if (opts.x_star || opts.track_true_residual) record();
+            return;
         }
-    } else if (maxit > 0) {
+        if (remaining <= 0) return;
         constexpr int kBatch = 8;
         const bool use_graph = ctx->stream != nullptr;
         if (use_graph) {
@@ -793,7 +809,7 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
         }
         int64_t launched = 0;
         int64_t k = 0;
-        while (launched < maxit) {
+        while (launched < remaining) {
             if (use_graph) {
                 SLQ_CUDA_CHECK(cudaGraphLaunch(exec, ctx->stream));
                 ctx->launches += 4 * kBatch;
@@ -826,6 +842,35 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
             std::fprintf(stderr, " ms\n");
             for (int i = 0; i < ntb; ++i) cudaEventDestroy(tb[i]);
         }
+    };
+    // Opt-in backward-error rule (slq_solve_opts.backward_tol): the device stops
+    // when the Paige-Saunders estimate alpha_{t+1}|c_t| reaches the trigger; the
+    // host then measures ||A^T r|| / (||A|| ||r||) with one direct pass and
+    // either accepts or resumes with a tighter trigger.
+    int64_t t_next = 1;
+    int confirms = 0;
+    for (;;) {
+        run_loop(t_next, maxit - t_next + 1);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, B.st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (!hs.bw_hit) break;
+        const double eta = backward_error_dev(ctx, op, b_dev, x, opts.a_norm_est > 0.0 ? opts.a_norm_est : 1.0);
+        out.backward_error = eta;
+        ++confirms;
+        if (eta <= opts.backward_tol) break;
+        if (hs.iters >= maxit) {
+            hs.term = SLQ_TERM_MAXITER;
+            hs.bw_hit = 0;
+            break;
+        }
+        // false trigger: tighten it by the measured ratio (off after 8 confirmations) and resume
+        hs.bw_trigger = confirms >= 8 ? 0.0 : hs.bw_trigger * std::max(1e-3, opts.backward_tol / eta);
+        hs.done = 0;
+        hs.bw_hit = 0;
+        hs.mode = kModeIter;
+        hs.term = SLQ_TERM_MAXITER;
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(B.st, &hs, sizeof(hs), cudaMemcpyHostToDevice, ctx->stream));
+        t_next = hs.t;
     }
     SLQ_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
     if (l2_window) {
@@ -834,7 +879,6 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
         cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &av);
         cudaGetLastError();
     }
-    SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, B.st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
     SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     float ms = 0.f;
     SLQ_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
@@ -1141,13 +1185,13 @@ double time_fused_pass(slq_ctx* ctx, const PassOp& op, int reps) {
     return ms * 1e-3 / std::max(reps, 1);
 }
 
-double backward_error_dev(slq_ctx* ctx, const PassOp& op, const double* x, double a_norm) {
+double backward_error_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* x, double a_norm) {
     // r = b - A x:  u_hat = A x - b = -r;  z = A^T u_hat = -A^T r
     const int64_t n = op.n;
     Workspace& ws = ctx->ws;
     double* dpart = static_cast<double*>(ws.lsqr_part.ensure(sizeof(double) * op.grid() * (n + 1)));
     double* dzt = static_cast<double*>(ws.tmp.ensure(sizeof(double) * (n + 1)));
-    op.pass(ctx, PassCall{x, nullptr, nullptr, nullptr, -1.0, dpart, 1, nullptr});
+    op.pass(ctx, PassCall{x, b_dev, nullptr, nullptr, -1.0, dpart, 1, nullptr});
     reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 32)), 256, 0, ctx->stream>>>(dpart, op.grid(), n + 1,
                                                                                              dzt, nullptr);
     SLQ_LAUNCH_CHECK(ctx);

@@ -62,8 +62,9 @@ void gd_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* M
 // Average seconds per fused-pass launch (K4), timed with CUDA events.
 double time_fused_pass(slq_ctx* ctx, const PassOp& op, int reps);
 
-// ||A^T r|| / (a_norm ||r||) for r = b - A x (one fused pass + allreduce).
-double backward_error_dev(slq_ctx* ctx, const PassOp& op, const double* x, double a_norm);
+// ||A^T r|| / (a_norm ||r||) for r = b - A x (one fused pass + allreduce);
+// b_dev == nullptr: the right-hand side stored with A.
+double backward_error_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* x, double a_norm);
 
 // comm.cu: in-place sum across ranks (no-op without a communicator).
 void allreduce_sum(slq_ctx* ctx, double* buf, int64_t count);
