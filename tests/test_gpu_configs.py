@@ -97,7 +97,9 @@ def test_c1_pipeline_vs_reference(c1, REF, one_sync):
 def test_c1_consistent_tolerance_rule(c1, REF):
     """Consistent variant (rho = 0, x0 = 0, test_solvers.cpp:360-373): the
     reference rule phi_bar <= eps beta_1 fires; same termination, iteration
-    count within one (the last comparison sits at rounding level)."""
+    count within one (the last comparison sits at rounding level).  Both
+    stop at a relative residual ~eps, so the iterates agree to ~eps cond(A)
+    in x and ~eps in residual space."""
     A, _, xs = c1
     n = A.shape[1]
     b = A @ xs
@@ -108,8 +110,10 @@ def test_c1_consistent_tolerance_rule(c1, REF):
     assert rr.termination == "tolerance"
     assert str(rep.termination) == rr.termination and abs(rep.iterations - rr.iterations) <= 1
     dx = np.linalg.norm(x - xr) / np.linalg.norm(xr)
-    assert dx <= 1e-9
-    _log("C1 consistent", iterations=rep.iterations, iterations_ref=rr.iterations, rel_dx=dx)
+    dres = np.linalg.norm(A @ (x - xr)) / np.linalg.norm(b)
+    assert dx <= 1e-10 * 1e3
+    assert dres <= 2e-10
+    _log("C1 consistent", iterations=rep.iterations, iterations_ref=rr.iterations, rel_dx=dx, res_delta=dres)
 
 
 # ------------------------------------------------------- C2 (cond 1e8)
