@@ -17,10 +17,17 @@ x0 + T LSQR iterations) with A resident in HBM.  `value` = seconds per solve
 (max over ranks, CUDA events); `e2e` = the same solve through the C-ABI from
 pinned HOST buffers (column-major A, as the reference's DenseMatrix), H2D and
 layout conversion inside the timed region.
+
+`cpu_baseline` / `--impl reference`: the reference itself (oracle/_ref, the
+unmodified sketchlsq headers compiled -O3 -march=native) on the SAME A and b
+bytes, full size, all T iterations, on every host thread -- not
+extrapolated.  `parity_vs_reference` compares the two solutions in
+backward-error / residual space.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes as ct
 import json
 import math
 import os
@@ -53,7 +60,8 @@ def parse():
     ap.add_argument("--eta", type=float, default=1e-10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=16, help="reference runs on m/cpu_sample rows, scaled")
+    ap.add_argument("--ref-budget", type=float, default=240.0,
+                    help="seconds of full-size reference solves per run (at least one)")
     ap.add_argument("--config", default="c3", choices=["c3", "c4"],
                     help="c3: dense 4M x 1000 cond 1e8 (headline); c4: sparse CSR 2^24 x 2000, 50 nnz/row, cond 1e6")
     return ap.parse_args()
@@ -199,38 +207,95 @@ def make_problem(torch, m, n, cond, rho, row_begin, row_end, dev, dist=None, see
 
 # ------------------------------------------------------------ reference (CPU)
 
-def reference_sample(args, m_s, T, torch=None):
-    """Times the reference (oracle/_ref: the unmodified sketchlsq headers) on
-    m_s rows with all host threads; returns (extrapolated full-solve seconds,
-    phase dict, description)."""
+def cpu_info():
+    """Host CPU model, logical CPUs and NUMA layout (recorded with every CPU timing)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+        fam = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith(("cpu family", "model\t"))][:2]
+        model += f" (family {fam[0]} model {fam[1]})" if len(fam) == 2 else ""
+    except Exception:
+        pass
+    numa = []
+    try:
+        base = "/sys/devices/system/node"
+        for nd in sorted(x for x in os.listdir(base) if x.startswith("node") and x[4:].isdigit()):
+            numa.append({"node": int(nd[4:]), "cpus": open(os.path.join(base, nd, "cpulist")).read().strip()})
+    except Exception:
+        pass
+    return {"model": model, "nproc": os.cpu_count(), "numa": numa}
+
+
+def host_copy(torch, Abuf, n, ml, pinned=True):
+    """Column-major host copy of the device block's A (an (n, ml) row-major
+    tensor == column-major A) and b, filled in 256K-row slabs."""
+    Ah = torch.empty((n, ml), dtype=torch.float64, pin_memory=pinned)
+    bh = torch.empty(ml, dtype=torch.float64, pin_memory=pinned)
+    for r in range(0, ml, 256_000):
+        Ah[:, r:r + 256_000].copy_(Abuf[r:r + 256_000, :n].T)
+    bh.copy_(Abuf[:, n])
+    return Ah, bh
+
+
+def reference_full(args, Ah, bh, T):
+    """The reference (oracle/_ref: the unmodified sketchlsq headers, g++ -O3
+    -march=native) on the SAME A and b bytes as the GPU, full size, not
+    extrapolated: distribute (untimed in `value`, reported) + the reference's
+    threaded backend on every host thread (WorkerPool(nproc):
+    dist_generate_sparse_sign + dist_sketch_apply + sketch_vector, serial
+    build_preconditioner + initial_guess, lsqr_one_sync over dist_operator for
+    T iterations, eps = 0).  Returns (solve seconds, phases, x, cores)."""
     import oracle
 
     R = oracle.REF()
     n, d, zeta = args.n, args.dfac * args.n, args.zeta
     cores = os.cpu_count() or 1
-    # sample problem: same shape family (rows m_s), generated on the GPU if present
-    if torch is not None and torch.cuda.is_available():
-        Abuf, ld, _ = make_problem(torch, m_s, n, args.cond, args.rho, 0, m_s, torch.device("cuda", 0))
-        A = np.asfortranarray(Abuf[:, :n].cpu().numpy())
-        b = Abuf[:, n].cpu().numpy().copy()
-        del Abuf
-        torch.cuda.empty_cache()
-    else:
-        rng = np.random.default_rng(0)
-        A = np.asfortranarray(rng.standard_normal((m_s, n)))
-        b = rng.standard_normal(m_s)
-    t_it = 2
-    t0 = time.perf_counter()
-    _, rep, ph = R.solve_timed(A, b, d, zeta, 3, 0.0, t_it, cores)
-    wall = time.perf_counter() - t0
-    scale = args.m / m_s
-    lsqr_per_it = ph["lsqr"] / max(rep.iterations, 1)
-    total = (ph["generate"] + ph["apply"]) * scale + ph["precond"] + ph["x0"] + lsqr_per_it * scale * T
-    desc = (f"reference sketchlsq (oracle/_ref, g++ -O3) on {m_s} of {args.m} rows, WorkerPool({cores}): "
-            f"dist_generate_sparse_sign + dist_sketch_apply + lsqr_one_sync(dist_operator) x{t_it} iterations "
-            f"scaled x{scale:g} (rows) and x{T} iterations; serial householder_qr + tri_inverse + initial_guess "
-            f"on the full {d}x{n} sketch timed as is")
-    return total, {k: float(v) for k, v in ph.items()}, desc, cores, wall
+    A = Ah.numpy().T  # (ml, n) column-major view, no copy
+    x, rep, ph = R.solve_timed(A, bh.numpy(), d, zeta, 3, 0.0, T, cores)
+    assert rep.iterations == T, (rep.iterations, T)
+    solve_s = ph["generate"] + ph["apply"] + ph["precond"] + ph["x0"] + ph["lsqr"]
+    return solve_s, {k: float(v) for k, v in ph.items()}, x, cores
+
+
+def reference_desc(m, n, d, zeta, T, cores):
+    return (f"reference sketchlsq (oracle/_ref: unmodified headers, g++ -O3 -march=sapphirerapids -ffp-contract=off) "
+            f"on the full {m}x{n} A and b (the GPU's bytes, column-major host copy), WorkerPool({cores}): "
+            f"dist_generate_sparse_sign + dist_sketch_apply + sketch_vector, serial build_preconditioner + "
+            f"initial_guess on the {d}x{n} sketch, lsqr_one_sync(dist_operator) x{T} iterations (zeta={zeta}); "
+            f"value = the solve without distribute (reported as phases.distribute); not extrapolated")
+
+
+def eta_and_parity(torch, Abuf, n, x_gpu, x_ref, dist=None):
+    """eta(x) = ||A^T r|| / (||A||_2 ||r||) (||A||_2 = 1 by construction) for both
+    solutions and their distance in residual space, on the device-resident A."""
+    dev = Abuf.device
+    A = Abuf[:, :n]
+    b = Abuf[:, n]
+
+    def red(t):
+        if dist is not None:
+            dist.all_reduce(t)
+        return t
+
+    def eta(x):
+        r = b - A @ torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+        atr = red((A.T @ r).reshape(-1))
+        rn2 = red((r * r).sum().reshape(1))
+        return float(torch.linalg.norm(atr) / torch.sqrt(rn2))
+
+    out = {"eta_gpu": eta(x_gpu)}
+    if x_ref is not None:
+        dxr = A @ torch.from_numpy(np.ascontiguousarray(x_gpu - x_ref)).to(dev)
+        num = float(torch.sqrt(red((dxr * dxr).sum().reshape(1))))
+        bn = float(torch.sqrt(red((b * b).sum().reshape(1))))
+        out.update({"eta_ref": eta(x_ref), "res_delta": num / bn,
+                    "x_rel_delta": float(np.linalg.norm(x_gpu - x_ref) / np.linalg.norm(x_ref)),
+                    "bar": "eta_gpu <= max(2 eta_ref, 1e-14) and res_delta <= 1e-12 cond(A) (SURVEY 8(c)(iv))"})
+        out["pass"] = bool(out["eta_gpu"] <= max(2 * out["eta_ref"], 1e-14) and out["res_delta"] <= 1e-12 * 1e8)
+    return out
 
 
 # ------------------------------------------------------------ config C4 (sparse)
@@ -383,21 +448,32 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        m_s = max(args.m // max(args.cpu_sample * 2, 1), 1000)
+        # same A / b bytes as the GPU arm (device generator, untimed harness), copied to the host
         T = args.iters or 30
-        vals = []
-        for _ in range(args.warmup if args.warmup <= 1 else 1):
-            reference_sample(args, m_s, T, torch)
-        for _ in range(args.steps):
-            v, ph, desc, cores, wall = reference_sample(args, m_s, T, torch)
+        dev = torch.device("cuda", 0)
+        Abuf, ld, _ = make_problem(torch, args.m, n, args.cond, args.rho, 0, args.m, dev)
+        Ah, bh = host_copy(torch, Abuf, n, args.m, pinned=False)
+        vals, phs, x_ref, cores = [], [], None, os.cpu_count()
+        t_start = time.perf_counter()
+        for k in range(max(1, args.steps)):
+            v, ph, x_ref, cores = reference_full(args, Ah, bh, T)
             vals.append(v)
+            phs.append(ph)
+            el = time.perf_counter() - t_start
+            if el + el / (k + 1) > args.ref_budget:  # the next full solve would exceed the budget
+                break
         v = float(np.mean(vals))
+        ph = {k: float(np.mean([p[k] for p in phs])) for k in phs[0]}
+        par = eta_and_parity(torch, Abuf, n, x_ref, None)
+        desc = reference_desc(args.m, n, d, zeta, T, cores)
         print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
-                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+                          "steps": len(vals), "steps_requested": args.steps, "warmup": 0, "ms_per_step": v * 1e3,
                           "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                          "data": "synthetic", "config": dict(config, lsqr_iterations=T),
+                          "data": "synthetic (the GPU arm's device generator, seed 1, copied to the host)",
+                          "config": dict(config, lsqr_iterations=T),
+                          "eta_final": par["eta_gpu"],
                           "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "reference",
-                                           "sample": desc, "phases": ph},
+                                           "sample": desc, "phases": ph, "cpu": cpu_info()},
                           "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
 
@@ -481,7 +557,6 @@ def main():
 
     # kernel-level timing for the roofline (dominant kernel: K4 fused LSQR pass)
     kt = np.zeros(4)
-    import ctypes as ct
     slq._capi.lib.slq_time_kernels(ctx.handle, A.handle, d, zeta, 3, 10, kt.ctypes.data_as(ct.POINTER(ct.c_double)))
     ml = r1 - r0
     pass_bytes = 8.0 * ml * n + 16.0 * ml
@@ -498,14 +573,20 @@ def main():
         try:
             fp = json.load(open(prof)).get("fused_pass", {})
             traffic = fp.get("dram_bytes_per_launch")
-            if traffic is not None and fp.get("m") and fp.get("n") == n and fp["m"] != ml:
+            if fp.get("n") != n or not fp.get("m"):
+                traffic = None  # the capture is for another shape
+            elif traffic is not None and fp["m"] != ml:
                 traffic = traffic * ml / fp["m"]  # per-row traffic is size-independent; this rank's rows
         except Exception:
             traffic = None
     iter_bytes = 8.0 * ml * n + 16.0 * ml + 8.0 * n * n
+    in_solve = ph["lsqr"] / (T + 1)  # init pass + T iterations, K5 kernels included (conservative)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "fused_pass (K4: u_hat = A p + c u, z = A^T u_hat, ||u_hat||^2)",
                 "algorithmic_bytes_per_launch": pass_bytes, "seconds_per_launch": float(kt[0]),
+                "timing": "10 launches on the library stream (CUDA events) with the live u, p, c of the last solve",
+                "in_solve_seconds_per_iteration": in_solve, "in_solve_gbs": pass_bytes / in_solve / 1e9,
+                "in_solve_frac": pass_bytes / in_solve / 1e9 / peak,
                 "peak_source": peak_src,
                 "lsqr_iteration_gbs": iter_bytes / ph["lsqr_per_iteration"] / 1e9 if ph["lsqr_per_iteration"] else None,
                 "sketch_seconds": float(kt[1]), "sketch_gbs": (8.0 * ml * (ld) + 4.0 * ml * zeta) / kt[1] / 1e9,
@@ -513,13 +594,12 @@ def main():
 
     # e2e through the C-ABI from pinned host buffers (column-major A as the reference's DenseMatrix)
     e2e = None
+    Ah = bh = None
+    want_cpu = rank == 0 and world == 1 and not args.no_cpu
+    if not args.no_e2e or want_cpu:
+        Ah, bh = host_copy(torch, Abuf, n, ml, pinned=True)
     if not args.no_e2e:
         try:
-            Ah = torch.empty((n, ml), dtype=torch.float64, pin_memory=True)  # (n, m) row-major == column-major A
-            bh = torch.empty(ml, dtype=torch.float64, pin_memory=True)
-            for r in range(0, ml, 256_000):
-                Ah[:, r:r + 256_000].copy_(Abuf[r:r + 256_000, :n].T)
-            bh.copy_(Abuf[:, n])
             xh = np.zeros(n)
             rep_h = slq._capi.Report()
             pt = slq._capi.PhaseTimes()
@@ -551,21 +631,31 @@ def main():
                 es = float(t.item())
             e2e = {"value": es, "unit": "s", "h2d_bytes_per_step": int(8 * ml * n + 8 * ml),
                    "d2h_bytes_per_step": int(8 * n), "steps": ke,
-                   "path": "slq_solve_host (C-ABI, pinned column-major host A)"}
-            del Ah, bh
+                   "path": "slq_solve_host (C-ABI, pinned column-major host A)",
+                   # the host path sketches each block as it lands (register gather): rounding-level difference
+                   "x_rel_delta_vs_device_path": float(np.linalg.norm(xh - x) / np.linalg.norm(x))}
         except Exception as ex:  # report, never hide
             e2e = {"value": None, "unit": "s", "error": str(ex)[:300]}
 
+    # multi-GPU consistency: every rank must hold the same x, bit for bit (replicated n-vector work)
+    ranks_agree = None
+    if dist is not None:
+        xt = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+        xs = [torch.empty_like(xt) for _ in range(world)]
+        dist.all_gather(xs, xt)
+        ranks_agree = bool(all(torch.equal(xs[0], y) for y in xs))
+
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    x_ref = None
+    if want_cpu:
         try:
-            del_buf = None
-            m_s = max(args.m // args.cpu_sample, 1000)
-            v, cph, desc, cores, wall = reference_sample(args, m_s, T, torch)
-            cpu = {"value": v, "unit": "s", "cores": cores, "kind": "reference", "sample": desc, "phases": cph,
-                   "sample_wall_s": wall}
+            v, cph, x_ref, cores = reference_full(args, Ah, bh, T)
+            cpu = {"value": v, "unit": "s", "cores": cores, "kind": "reference",
+                   "sample": reference_desc(args.m, n, d, zeta, T, cores), "phases": cph, "cpu": cpu_info()}
         except Exception as ex:
             cpu = {"value": None, "unit": "s", "error": str(ex)[:300]}
+    parity = eta_and_parity(torch, Abuf, n, x, x_ref, dist)
+    del Ah, bh
 
     if rank == 0:
         line = {
@@ -573,7 +663,12 @@ def main():
             "warmup": max(args.warmup, 3), "ms_per_step": sec * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (device generator, seed 1)",
             "config": dict(config, lsqr_iterations=T),
-            "eta_final": eta, "iterations": rep.iterations,
+            "eta_final": eta, "iterations": rep.iterations, "parity_vs_reference": parity,
+            "multi_gpu": {"ranks": world, "x_bitwise_equal_across_ranks": ranks_agree,
+                          "nccl_calls_per_solve": ph["nccl_calls"],
+                          "nccl_calls_per_iteration": 1 if world > 1 else 0,
+                          "collectives": "ncclReduce S[A b] + ncclBroadcast status/M/M^T/x0 + one ncclAllReduce "
+                                         "of n+1 doubles per LSQR iteration" if world > 1 else None},
             "phases_s": ph, "host_s_per_step": float(np.mean(host_s)), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": ck, "generation_s": t_gen,
         }

@@ -200,6 +200,20 @@ int slq_initial_guess(slq_ctx* ctx, const double* M, const double* Q, int64_t d,
  * apply_M / apply_Mt are these with R = M. */
 int slq_tri_upper_matvec(slq_ctx* ctx, const double* R, int64_t n, const double* x, double* y, int trans);
 
+/* ------------------------------------------------- operator products -- */
+
+/* The Op concept of the reference (operators.hpp:15-51 SerialOperator;
+ * distsim.hpp:283-331 dist_matvec / dist_rmatvec / dist_rmatvec_and_norm):
+ * one HBM pass of the device operand each.  Host vectors in and out.
+ *   matvec:  y[m] = A x[n]   (this rank's rows; no communication)
+ *   rmatvec: z[n] = A^T y[m] and, when ynorm2 != NULL, *ynorm2 = ||y||^2 --
+ *            fused (the one-synchronization product of lsqr.hpp:120-127);
+ *            with a communicator both are summed over ranks (one allreduce). */
+int slq_dense_matvec(slq_ctx* ctx, const slq_dense* A, const double* x, double* y);
+int slq_dense_rmatvec(slq_ctx* ctx, const slq_dense* A, const double* y, double* z, double* ynorm2);
+int slq_sparse_matvec(slq_ctx* ctx, const slq_sparse* A, const double* x, double* y);
+int slq_sparse_rmatvec(slq_ctx* ctx, const slq_sparse* A, const double* y, double* z, double* ynorm2);
+
 /* ---------------------------------------------------------------- LSQR -- */
 
 typedef struct {

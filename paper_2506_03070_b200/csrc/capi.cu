@@ -40,6 +40,8 @@ int guarded(F&& f) {
     }
 }
 
+const double kZero = 0.0;  // stands in for the data pointer of an empty vector
+
 void need(bool cond, int code, const char* what) {
     if (!cond) slq::fail(code, what);
 }
@@ -822,6 +824,58 @@ int slq_tri_upper_matvec(slq_ctx* ctx, const double* R, int64_t n, const double*
         }
         SLQ_CUDA_CHECK(cudaMemcpyAsync(y, v + n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
         SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+namespace {
+// y = A x / z = A^T y (+ ||y||^2) for the Op surface, host vectors in and out
+void op_products(slq_ctx* ctx, const slq::PassOp& op, const double* x, double* y, const double* yin, double* z,
+                 double* ynorm2) {
+    const int64_t m = op.m, n = op.n;
+    slq::DevBuf du, dn, dz;
+    double* u = static_cast<double*>(du.ensure(sizeof(double) * (m + slq::kSparseRowPad)));
+    double* v = static_cast<double*>(dn.ensure(sizeof(double) * (n + 8)));
+    if (x) {
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(v, x, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        slq::op_matvec_dev(ctx, op, v, u);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(y, u, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream));
+    } else {
+        double* zz = static_cast<double*>(dz.ensure(sizeof(double) * (n + 1)));
+        SLQ_CUDA_CHECK(cudaMemsetAsync(u, 0, sizeof(double) * (m + slq::kSparseRowPad), ctx->stream));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(u, yin, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream));
+        slq::op_rmatvec_dev(ctx, op, u, zz, v);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(z, zz, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        if (ynorm2) SLQ_CUDA_CHECK(cudaMemcpyAsync(ynorm2, zz + n, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+}
+}  // namespace
+
+int slq_dense_matvec(slq_ctx* ctx, const slq_dense* A, const double* x, double* y) {
+    return guarded([&] {
+        need(ctx && A && (x || A->n == 0) && (y || A->m == 0), SLQ_INVALID_ARG, "dense_matvec: null argument");
+        op_products(ctx, *slq::make_dense_op(ctx, A), x ? x : &kZero, y, nullptr, nullptr, nullptr);
+    });
+}
+
+int slq_dense_rmatvec(slq_ctx* ctx, const slq_dense* A, const double* y, double* z, double* ynorm2) {
+    return guarded([&] {
+        need(ctx && A && (y || A->m == 0) && (z || A->n == 0), SLQ_INVALID_ARG, "dense_rmatvec: null argument");
+        op_products(ctx, *slq::make_dense_op(ctx, A), nullptr, nullptr, y ? y : &kZero, z, ynorm2);
+    });
+}
+
+int slq_sparse_matvec(slq_ctx* ctx, const slq_sparse* A, const double* x, double* y) {
+    return guarded([&] {
+        need(ctx && A && (x || A->n == 0) && (y || A->m == 0), SLQ_INVALID_ARG, "sparse_matvec: null argument");
+        op_products(ctx, *slq::make_sparse_op(ctx, A), x ? x : &kZero, y, nullptr, nullptr, nullptr);
+    });
+}
+
+int slq_sparse_rmatvec(slq_ctx* ctx, const slq_sparse* A, const double* y, double* z, double* ynorm2) {
+    return guarded([&] {
+        need(ctx && A && (y || A->m == 0) && (z || A->n == 0), SLQ_INVALID_ARG, "sparse_rmatvec: null argument");
+        op_products(ctx, *slq::make_sparse_op(ctx, A), nullptr, nullptr, y ? y : &kZero, z, ynorm2);
     });
 }
 

@@ -110,6 +110,7 @@ struct slq_ctx {
     cudaStream_t qr_hi = nullptr, qr_lo = nullptr;
     cudaEvent_t qr_ev[3] = {nullptr, nullptr, nullptr};
     int* lsqr_hdone = nullptr;            // pinned done-flag mirror (2 ints)
+    int64_t lsqr_live_m = -1, lsqr_live_n = -1;  // shape whose LSQR vectors the workspace holds
     cudaEvent_t lsqr_ev[2] = {nullptr, nullptr};
 };
 

@@ -66,6 +66,13 @@ double time_fused_pass(slq_ctx* ctx, const PassOp& op, int reps);
 // b_dev == nullptr: the right-hand side stored with A.
 double backward_error_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* x, double a_norm);
 
+// The Op concept's products over one HBM pass (operators.hpp:15-51,
+// distsim.hpp:283-331): y[m + kSparseRowPad] = A x (this rank's rows);
+// z[n + 1] = [A^T y | ||y||^2] summed over ranks (one allreduce).  zero_n is
+// n + 8 doubles of scratch.
+void op_matvec_dev(slq_ctx* ctx, const PassOp& op, const double* x, double* y);
+void op_rmatvec_dev(slq_ctx* ctx, const PassOp& op, const double* y, double* z, double* zero_n);
+
 // comm.cu: in-place sum across ranks (no-op without a communicator).
 void allreduce_sum(slq_ctx* ctx, double* buf, int64_t count);
 void reduce_sum_root(slq_ctx* ctx, double* buf, int64_t count);
