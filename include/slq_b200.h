@@ -127,7 +127,10 @@ int slq_sketch_apply(slq_ctx* ctx, const slq_dense* A, int64_t d, int64_t zeta, 
 
 /* csc_matrix.hpp:103-120 spmm(csc, dense) for a caller-given CSC S (d x m)
  * and host column-major A (m x n, lda): Y = S A (column-major d x n).
- * Same accumulation order as the reference (bit-identical). */
+ * Same accumulation order as the reference (bit-identical).  A sparse-sign S
+ * (all |values| equal) runs the sketch gather; any other values the general
+ * kernel (row-sorted entries, one thread per Y entry).  The entries are
+ * validated on the device (SLQ_INVALID_ARG for a row out of range). */
 int slq_spmm_csc_dense(slq_ctx* ctx, int64_t d, int64_t m, const int64_t* row_indices,
                        const double* values, const int64_t* col_pointers, const double* A,
                        int64_t n, int64_t lda, double* Y);
@@ -166,8 +169,9 @@ int slq_sparse_free(slq_sparse* A);
 int slq_sketch_apply_sparse(slq_ctx* ctx, const slq_sparse* A, int64_t d, int64_t zeta, uint64_t seed,
                             double* Y, double* Sb);
 
-/* csc_matrix.hpp:123-136 spmm(csc, csc): Y = S A for a caller CSC sketch S
- * (d x m, +-v values) and a host CSC A (m x n); reference order (bit-identical). */
+/* csc_matrix.hpp:123-136 spmm(csc, csc): Y = S A for a caller CSC S (d x m;
+ * sparse-sign or arbitrary values, as slq_spmm_csc_dense) and a host CSC A
+ * (m x n); reference order (bit-identical). */
 int slq_spmm_csc_csc(slq_ctx* ctx, int64_t d, int64_t m, const int64_t* s_rows, const double* s_vals,
                      const int64_t* s_colptr, int64_t n, const int64_t* a_colptr, const int64_t* a_rows,
                      const double* a_vals, double* Y);

@@ -18,6 +18,7 @@
 #include "qr.cuh"
 #include "sketch.cuh"
 #include "sparse.cuh"
+#include "spmm_general.cuh"
 
 namespace {
 
@@ -692,13 +693,6 @@ int slq_spmm_csc_dense(slq_ctx* ctx, int64_t d, int64_t m, const int64_t* row_in
         need(lda >= m, SLQ_INVALID_DIMS, "spmm: lda < m");
         const int64_t nnz = col_pointers[m];
         need(col_pointers[0] == 0 && nnz >= 0, SLQ_INVALID_ARG, "spmm: bad col_pointers");
-        double val = 0.0;
-        for (int64_t e = 0; e < nnz; ++e) {
-            const double a = std::fabs(values[e]);
-            if (e == 0) val = a;
-            else if (a != val) slq::fail(SLQ_UNSUPPORTED, "spmm: device path needs +-v sketch values");
-            if (row_indices[e] < 0 || row_indices[e] >= d) slq::fail(SLQ_INVALID_ARG, "spmm: row index out of range");
-        }
         slq_dense* Ad = nullptr;
         int st = slq_dense_upload(ctx, A, m, n, lda, nullptr, 0, &Ad);
         if (st != SLQ_OK) slq::fail(st, g_last_error);
@@ -710,19 +704,32 @@ int slq_spmm_csc_dense(slq_ctx* ctx, int64_t d, int64_t m, const int64_t* row_in
         int64_t* r = static_cast<int64_t*>(drows.ensure(sizeof(int64_t) * std::max<int64_t>(1, nnz)));
         double* v = static_cast<double*>(dvals.ensure(sizeof(double) * std::max<int64_t>(1, nnz)));
         int64_t* cp = static_cast<int64_t*>(dcp.ensure(sizeof(int64_t) * (m + 1)));
-        uint32_t* comp = static_cast<uint32_t*>(dcomp.ensure(sizeof(uint32_t) * std::max<int64_t>(1, nnz)));
-        double* Yd = static_cast<double*>(dY.ensure(sizeof(double) * d * (n + 1)));
-        SLQ_CUDA_CHECK(cudaMemcpyAsync(r, row_indices, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, ctx->stream));
-        SLQ_CUDA_CHECK(cudaMemcpyAsync(v, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->stream));
-        SLQ_CUDA_CHECK(cudaMemcpyAsync(cp, col_pointers, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, ctx->stream));
+        double* Yd = static_cast<double*>(dY.ensure(sizeof(double) * std::max<int64_t>(1, d * (n + 1))));
         if (nnz > 0) {
-            csc_to_compact_kernel<<<static_cast<unsigned>(slq::ceil_div(nnz, 256)), 256, 0, ctx->stream>>>(r, v, nnz, comp);
-            SLQ_LAUNCH_CHECK(ctx);
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(r, row_indices, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, ctx->stream));
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(v, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->stream));
         }
-        int64_t zmax = 1;
-        for (int64_t j = 0; j < m; ++j) zmax = std::max(zmax, col_pointers[j + 1] - col_pointers[j]);
-        slq::sketch_apply_compact_dev(ctx, Ad, d, comp, cp, zmax, val, true, Yd);
-        SLQ_CUDA_CHECK(cudaMemcpyAsync(Y, Yd, sizeof(double) * d * n, cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(cp, col_pointers, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, ctx->stream));
+        const slq::SpmmCheck chk = slq::csc_check_dev(ctx, r, v, nnz, d);
+        need(!chk.row_out_of_range, SLQ_INVALID_ARG, "spmm: row index out of range");
+        if (chk.mixed_magnitudes) {
+            // arbitrary values: the general kernel (reference order, bit-identical)
+            slq::spmm_general_dev(ctx, d, m, nnz, r, v, cp, n, Ad->A, Ad->ld, nullptr, nullptr, nullptr, Yd);
+        } else {
+            // a sparse-sign matrix (one magnitude): the sketch gather in exact mode
+            const double val = nnz > 0 ? std::fabs(values[0]) : 0.0;
+            uint32_t* comp = static_cast<uint32_t*>(dcomp.ensure(sizeof(uint32_t) * std::max<int64_t>(1, nnz)));
+            if (nnz > 0) {
+                csc_to_compact_kernel<<<static_cast<unsigned>(slq::ceil_div(nnz, 256)), 256, 0, ctx->stream>>>(r, v, nnz,
+                                                                                                            comp);
+                SLQ_LAUNCH_CHECK(ctx);
+            }
+            int64_t zmax = 1;
+            for (int64_t j = 0; j < m; ++j) zmax = std::max(zmax, col_pointers[j + 1] - col_pointers[j]);
+            slq::sketch_apply_compact_dev(ctx, Ad, d, comp, cp, zmax, val, true, Yd);
+        }
+        if (d * n > 0)
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(Y, Yd, sizeof(double) * d * n, cudaMemcpyDeviceToHost, ctx->stream));
         SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     });
 }
@@ -1054,37 +1061,53 @@ int slq_spmm_csc_csc(slq_ctx* ctx, int64_t d, int64_t m, const int64_t* s_rows, 
     return guarded([&] {
         need(ctx && s_colptr && a_colptr && Y, SLQ_INVALID_ARG, "spmm_csc_csc: null argument");
         const int64_t snnz = s_colptr[m];
-        double val = 0.0;
-        int64_t zmax = 1;
-        for (int64_t j = 0; j < m; ++j) zmax = std::max(zmax, s_colptr[j + 1] - s_colptr[j]);
-        for (int64_t e = 0; e < snnz; ++e) {
-            const double a = std::fabs(s_vals[e]);
-            if (e == 0) val = a;
-            else if (a != val) slq::fail(SLQ_UNSUPPORTED, "spmm: device path needs +-v sketch values");
-            if (s_rows[e] < 0 || s_rows[e] >= d) slq::fail(SLQ_INVALID_ARG, "spmm: row index out of range");
-        }
-        slq_sparse* As = nullptr;
-        int st = slq_sparse_upload_csc(ctx, m, n, a_colptr, a_rows, a_vals, nullptr, 0, &As);
-        if (st != SLQ_OK) slq::fail(st, g_last_error);
-        struct Free {
-            slq_sparse* p;
-            ~Free() { slq_sparse_free(p); }
-        } fr{As};
+        const int64_t annz = a_colptr[n];
+        need(s_colptr[0] == 0 && snnz >= 0 && a_colptr[0] == 0 && annz >= 0, SLQ_INVALID_ARG,
+             "spmm_csc_csc: bad col_pointers");
         slq::DevBuf drows, dvals, dcp, dcomp, dY;
         int64_t* r = static_cast<int64_t*>(drows.ensure(sizeof(int64_t) * std::max<int64_t>(1, snnz)));
         double* v = static_cast<double*>(dvals.ensure(sizeof(double) * std::max<int64_t>(1, snnz)));
         int64_t* cp = static_cast<int64_t*>(dcp.ensure(sizeof(int64_t) * (m + 1)));
-        uint32_t* comp = static_cast<uint32_t*>(dcomp.ensure(sizeof(uint32_t) * std::max<int64_t>(1, snnz)));
-        double* Yd = static_cast<double*>(dY.ensure(sizeof(double) * d * (n + 1)));
-        SLQ_CUDA_CHECK(cudaMemcpyAsync(r, s_rows, sizeof(int64_t) * snnz, cudaMemcpyHostToDevice, ctx->stream));
-        SLQ_CUDA_CHECK(cudaMemcpyAsync(v, s_vals, sizeof(double) * snnz, cudaMemcpyHostToDevice, ctx->stream));
-        SLQ_CUDA_CHECK(cudaMemcpyAsync(cp, s_colptr, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, ctx->stream));
+        double* Yd = static_cast<double*>(dY.ensure(sizeof(double) * std::max<int64_t>(1, d * (n + 1))));
         if (snnz > 0) {
-            csc_to_compact_kernel<<<static_cast<unsigned>(slq::ceil_div(snnz, 256)), 256, 0, ctx->stream>>>(r, v, snnz, comp);
-            SLQ_LAUNCH_CHECK(ctx);
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(r, s_rows, sizeof(int64_t) * snnz, cudaMemcpyHostToDevice, ctx->stream));
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(v, s_vals, sizeof(double) * snnz, cudaMemcpyHostToDevice, ctx->stream));
         }
-        slq::sketch_apply_sparse_compact_dev(ctx, As, d, comp, cp, zmax, val, Yd);
-        SLQ_CUDA_CHECK(cudaMemcpyAsync(Y, Yd, sizeof(double) * d * n, cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(cp, s_colptr, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, ctx->stream));
+        const slq::SpmmCheck chk = slq::csc_check_dev(ctx, r, v, snnz, d);
+        need(!chk.row_out_of_range, SLQ_INVALID_ARG, "spmm: row index out of range");
+        if (chk.mixed_magnitudes) {
+            slq::DevBuf dacp, dar, dav;
+            int64_t* acp = static_cast<int64_t*>(dacp.ensure(sizeof(int64_t) * (n + 1)));
+            int64_t* ar = static_cast<int64_t*>(dar.ensure(sizeof(int64_t) * std::max<int64_t>(1, annz)));
+            double* av = static_cast<double*>(dav.ensure(sizeof(double) * std::max<int64_t>(1, annz)));
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(acp, a_colptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, ctx->stream));
+            if (annz > 0) {
+                SLQ_CUDA_CHECK(cudaMemcpyAsync(ar, a_rows, sizeof(int64_t) * annz, cudaMemcpyHostToDevice, ctx->stream));
+                SLQ_CUDA_CHECK(cudaMemcpyAsync(av, a_vals, sizeof(double) * annz, cudaMemcpyHostToDevice, ctx->stream));
+            }
+            slq::spmm_general_dev(ctx, d, m, snnz, r, v, cp, n, nullptr, 0, acp, ar, av, Yd);
+        } else {
+            slq_sparse* As = nullptr;
+            int st = slq_sparse_upload_csc(ctx, m, n, a_colptr, a_rows, a_vals, nullptr, 0, &As);
+            if (st != SLQ_OK) slq::fail(st, g_last_error);
+            struct Free {
+                slq_sparse* p;
+                ~Free() { slq_sparse_free(p); }
+            } fr{As};
+            const double val = snnz > 0 ? std::fabs(s_vals[0]) : 0.0;
+            int64_t zmax = 1;
+            for (int64_t j = 0; j < m; ++j) zmax = std::max(zmax, s_colptr[j + 1] - s_colptr[j]);
+            uint32_t* comp = static_cast<uint32_t*>(dcomp.ensure(sizeof(uint32_t) * std::max<int64_t>(1, snnz)));
+            if (snnz > 0) {
+                csc_to_compact_kernel<<<static_cast<unsigned>(slq::ceil_div(snnz, 256)), 256, 0, ctx->stream>>>(r, v, snnz,
+                                                                                                             comp);
+                SLQ_LAUNCH_CHECK(ctx);
+            }
+            slq::sketch_apply_sparse_compact_dev(ctx, As, d, comp, cp, zmax, val, Yd);
+        }
+        if (d * n > 0)
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(Y, Yd, sizeof(double) * d * n, cudaMemcpyDeviceToHost, ctx->stream));
         SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     });
 }

@@ -172,6 +172,31 @@ def test_apply_identity_sketch():
     assert np.array_equal(Y, A)
 
 
+@pytest.mark.parametrize("d,m,n,dens", [(9, 12, 5, 0.3), (300, 2000, 17, 0.01), (64, 5000, 40, 0.05)])
+def test_spmm_general_values_bit_exact(d, m, n, dens):
+    """spmm(csc, dense) / spmm(csc, csc) with arbitrary S values (not a sparse
+    sign matrix) -- the reference's order, bit for bit (test_core_linalg.cpp:192-224)."""
+    rng = np.random.default_rng(d + m)
+    mask = rng.random((d, m)) < dens
+    Sd = np.where(mask, rng.standard_normal((d, m)), 0.0)
+    cols = [np.nonzero(mask[:, k])[0] for k in range(m)]
+    rows = np.concatenate(cols).astype(np.int64) if cols else np.zeros(0, np.int64)
+    vals = np.concatenate([Sd[c, k] for k, c in enumerate(cols)])
+    colptr = np.concatenate([[0], np.cumsum([len(c) for c in cols])]).astype(np.int64)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    A[rng.random((m, n)) < 0.2] = 0.0
+    S = slq.CscMatrix(d, m, vals, rows, colptr)
+    Y = slq.apply(slq.SparseSignSketch(S, 1, 0), A)
+    assert np.array_equal(Y, C.spmm(d, rows, vals, colptr, A))
+    amask = rng.random((m, n)) < 0.1
+    acols = [np.nonzero(amask[:, j])[0] for j in range(n)]
+    arows = np.concatenate(acols).astype(np.int64)
+    avals = rng.standard_normal(arows.size)
+    acp = np.concatenate([[0], np.cumsum([len(c) for c in acols])]).astype(np.int64)
+    Ya = slq.apply(slq.SparseSignSketch(S, 1, 0), slq.CscMatrix(m, n, avals, arows, acp))
+    assert np.array_equal(Ya, C.spmm_csc(d, rows, vals, colptr, m, n, arows, avals, acp))
+
+
 def test_apply_dimension_mismatch():
     S = slq.generate_sparse_sign(10, 20, 2, 1)
     with pytest.raises(slq.DimensionMismatch):
