@@ -115,6 +115,10 @@ _SIGS = {
     "slq_build_preconditioner": (ct.c_int, [vp, dp, i64, i64, i64, dp, dp, dp, dp, dp]),
     "slq_initial_guess": (ct.c_int, [vp, dp, dp, i64, i64, dp, dp]),
     "slq_tri_upper_matvec": (ct.c_int, [vp, dp, i64, dp, dp, ct.c_int]),
+    "slq_dense_matvec": (ct.c_int, [vp, vp, dp, dp]),
+    "slq_dense_rmatvec": (ct.c_int, [vp, vp, dp, dp, dp]),
+    "slq_sparse_matvec": (ct.c_int, [vp, vp, dp, dp]),
+    "slq_sparse_rmatvec": (ct.c_int, [vp, vp, dp, dp, dp]),
     "slq_lsqr": (ct.c_int, [vp, vp, dp, dp, dp, ct.POINTER(SolveOpts), dp, ct.POINTER(Report), dp, dp, dp]),
     "slq_solve": (ct.c_int, [vp, vp, i64, i64, u64, ct.POINTER(SolveOpts), dp, ct.POINTER(Report),
                              ct.POINTER(PhaseTimes), dp]),

@@ -465,8 +465,7 @@ __global__ void __launch_bounds__(32 * kSpMaxWarps, 1) sparse_pass_kernel(SPassA
     // ssq: lanes 0, 8, 16, 24 hold partial sums
     ssq += __shfl_xor_sync(0xffffffffu, ssq, 8);
     ssq += __shfl_xor_sync(0xffffffffu, ssq, 16);
-    __syncthreads();
-    double* red = p_s;  // p is no longer needed
+    __shared__ double red[kSpMaxWarps];  // own array: p's n doubles may be fewer than the warps
     if (lane == 0) red[warp] = ssq;
     __syncthreads();
     double* outp = a.part + static_cast<int64_t>(blockIdx.x) * (n + 1);
@@ -615,7 +614,6 @@ public:
         W_ = static_cast<int>(std::min<int64_t>(kSpMaxWarps, budget / std::max<int64_t>(zrow, 1) - 1));
         if (W_ < 1) fail(SLQ_UNSUPPORTED, "sparse lsqr: n too large for shared-memory z copies");
         smem_ = static_cast<size_t>(zrow) * (W_ + 1);
-        if (smem_ < static_cast<size_t>(W_) * sizeof(double)) smem_ = static_cast<size_t>(W_) * sizeof(double);
         grid_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, ceil_div(std::max<int64_t>(m, 1), 4 * W_))));
         SLQ_CUDA_CHECK(cudaFuncSetAttribute(sparse_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem_)));

@@ -114,3 +114,39 @@ def test_sparse_lsqr_long_rows():
                           one_sync=True)
     assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
     assert np.allclose(rep.residual_estimate, repo.residual_estimate, rtol=1e-9)
+
+
+@pytest.mark.parametrize("m,n,dens", [(50, 13, 0.08), (400, 13, 0.08), (7, 3, 0.5), (1000, 40, 0.02), (3000, 200, 0.3)])
+def test_sparse_operator_products(m, n, dens):
+    """slq_sparse_matvec / slq_sparse_rmatvec (the Op surface of operators.hpp
+    over a CSC operand): A x and A^T y (+ ||y||^2) against numpy, including
+    empty rows and columns."""
+    import ctypes as ct
+
+    from paper_2506_03070_b200 import _capi as CA
+
+    rng = np.random.default_rng(m * 31 + n)
+    D = np.where(rng.random((m, n)) < dens, rng.standard_normal((m, n)), 0.0)
+    cols = [np.nonzero(D[:, j])[0] for j in range(n)]
+    rows = np.concatenate(cols).astype(np.int64)
+    vals = np.concatenate([D[c, j] for j, c in enumerate(cols)])
+    cp = np.concatenate([[0], np.cumsum([len(c) for c in cols])]).astype(np.int64)
+    A = slq.SparseDeviceMatrix.from_csc(slq.CscMatrix(m, n, vals, rows, cp))
+    x = rng.standard_normal(n)
+    y = rng.standard_normal(m)
+    ax = np.zeros(m)
+    aty = np.zeros(n)
+    ss = ct.c_double(0.0)
+    assert CA.lib.slq_sparse_matvec(A.ctx.handle, A.handle, x.ctypes.data_as(CA.dp), ax.ctypes.data_as(CA.dp)) == 0
+    assert CA.lib.slq_sparse_rmatvec(A.ctx.handle, A.handle, y.ctypes.data_as(CA.dp), aty.ctypes.data_as(CA.dp),
+                                     ct.byref(ss)) == 0
+    assert np.allclose(ax, D @ x, rtol=1e-13, atol=1e-13)
+    assert np.allclose(aty, D.T @ y, rtol=1e-12, atol=1e-13), np.abs(aty - D.T @ y).max()
+    assert abs(ss.value - y @ y) <= 1e-12 * (y @ y)
+    Dd = np.asfortranarray(D)
+    dm = slq.DeviceMatrix.from_numpy(Dd)
+    assert CA.lib.slq_dense_matvec(dm.ctx.handle, dm.handle, x.ctypes.data_as(CA.dp), ax.ctypes.data_as(CA.dp)) == 0
+    assert CA.lib.slq_dense_rmatvec(dm.ctx.handle, dm.handle, y.ctypes.data_as(CA.dp), aty.ctypes.data_as(CA.dp),
+                                    ct.byref(ss)) == 0
+    assert np.allclose(ax, D @ x, rtol=1e-13, atol=1e-13)
+    assert np.allclose(aty, D.T @ y, rtol=1e-12, atol=1e-13)
