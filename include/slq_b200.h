@@ -68,6 +68,20 @@ int64_t slq_ctx_kernel_launches(const slq_ctx* ctx);
 int slq_comm_unique_id(unsigned char id_out[128]);
 int slq_ctx_init_comm(slq_ctx* ctx, const unsigned char id[128], int rank, int nranks);
 
+/* Host-side collectives (an alternative to NCCL, for tests and for callers
+ * that bring their own transport): in-place operations on host buffers of
+ * `count` doubles, called by the library with the stream synchronized (each
+ * call is a host round trip; the iteration graphs are not used).  Every rank
+ * calls them in the same order; return 0 on success.  reduce_sum_root needs
+ * the sum on rank 0 only; broadcast_root copies rank 0's buffer to all. */
+typedef struct {
+    int (*allreduce_sum)(void* user, double* buf, int64_t count);
+    int (*reduce_sum_root)(void* user, double* buf, int64_t count);
+    int (*broadcast_root)(void* user, double* buf, int64_t count);
+    void* user;
+} slq_host_comm;
+int slq_ctx_set_host_comm(slq_ctx* ctx, const slq_host_comm* comm, int rank, int nranks);
+
 /* distsim.hpp:31-42 partition_rows: boundaries[0..p] */
 int slq_partition_rows(int64_t m, int p, int64_t* boundaries);
 

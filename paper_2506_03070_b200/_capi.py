@@ -48,6 +48,14 @@ class SolveOpts(ct.Structure):
     ]
 
 
+HostCollective = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.POINTER(ct.c_double), ct.c_int64)
+
+
+class HostComm(ct.Structure):
+    _fields_ = [("allreduce_sum", HostCollective), ("reduce_sum_root", HostCollective),
+                ("broadcast_root", HostCollective), ("user", ct.c_void_p)]
+
+
 class Report(ct.Structure):
     _fields_ = [
         ("iterations", i64),
@@ -115,6 +123,7 @@ _SIGS = {
     "slq_build_preconditioner": (ct.c_int, [vp, dp, i64, i64, i64, dp, dp, dp, dp, dp]),
     "slq_initial_guess": (ct.c_int, [vp, dp, dp, i64, i64, dp, dp]),
     "slq_tri_upper_matvec": (ct.c_int, [vp, dp, i64, dp, dp, ct.c_int]),
+    "slq_ctx_set_host_comm": (ct.c_int, [vp, ct.POINTER(HostComm), ct.c_int, ct.c_int]),
     "slq_dense_matvec": (ct.c_int, [vp, vp, dp, dp]),
     "slq_dense_rmatvec": (ct.c_int, [vp, vp, dp, dp, dp]),
     "slq_sparse_matvec": (ct.c_int, [vp, vp, dp, dp]),

@@ -161,6 +161,31 @@ class Context:
         _check(C.lib.slq_ctx_init_comm(self.handle, uid, rank, nranks))
         self.rank, self.nranks = rank, nranks
 
+    def set_host_comm(self, comm, rank: int, nranks: int):
+        """Collectives through the caller's host transport instead of NCCL
+        (slq_ctx_set_host_comm): ``comm`` has allreduce_sum(buf),
+        reduce_sum_root(buf) and broadcast_root(buf), each in place on a float64
+        numpy view of the library's pinned staging buffer.  Every rank's solve
+        then runs the same per-rank sequence as with NCCL (reduce of the sketch
+        partials, rank-0 preconditioner, status / M / M^T / x0 broadcasts, one
+        allreduce per LSQR iteration), one host round trip per collective."""
+        import traceback
+
+        def wrap(fn):
+            def cb(_user, buf, count):
+                try:
+                    fn(np.ctypeslib.as_array(buf, shape=(count,)))
+                    return 0
+                except Exception:  # a failed collective surfaces as SLQ_NCCL on this rank
+                    traceback.print_exc()
+                    return 1
+            return C.HostCollective(cb)
+
+        self._host_comm = [wrap(comm.allreduce_sum), wrap(comm.reduce_sum_root), wrap(comm.broadcast_root)]
+        hc = C.HostComm(*self._host_comm, None)
+        _check(C.lib.slq_ctx_set_host_comm(self.handle, ct.byref(hc), rank, nranks))
+        self.rank, self.nranks = rank, nranks
+
 
 _tls = threading.local()
 

@@ -170,6 +170,7 @@ struct Timer {
         SLQ_CUDA_CHECK(cudaEventRecord(e, s));
     }
     ~Timer() { cudaEventDestroy(e); }
+    void record(cudaStream_t s) { SLQ_CUDA_CHECK(cudaEventRecord(e, s)); }
     double since(const Timer& o) const {
         float ms = 0.f;
         SLQ_CUDA_CHECK(cudaEventSynchronize(e));
@@ -189,20 +190,17 @@ PrecondBufs precond_bufs(slq_ctx* ctx, int64_t n) {
 }
 
 // QR of Yaug (d x (n+1) incl. Sb) -> M, Mt, x0 on the device; times in t[3].
+// marks (may be null): four timers re-recorded before QR, before R^-1, before
+// x0 and at the end -- read by the caller after its final sync (no host wait here)
 void build_precond_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, bool with_sb, double* Q,
-                       const PrecondBufs& P, double* t) {
-    Timer t0(ctx->stream);
+                       const PrecondBufs& P, Timer* const* marks) {
+    if (marks) marks[0]->record(ctx->stream);
     slq::qr_factor_dev(ctx, Yaug, d, n, with_sb ? n + 1 : n, d, P.R, with_sb ? P.qtb : nullptr, Q, nullptr);
-    Timer t1(ctx->stream);
+    if (marks) marks[1]->record(ctx->stream);
     slq::tri_inverse_dev(ctx, P.R, n, P.M, P.Mt);
-    Timer t2(ctx->stream);
+    if (marks) marks[2]->record(ctx->stream);
     if (with_sb) slq::trmv_upper_dev(ctx, P.Mt, n, P.qtb, P.x0);
-    Timer t3(ctx->stream);
-    if (t) {
-        t[0] = t1.since(t0);
-        t[1] = t2.since(t1);
-        t[2] = t3.since(t2);
-    }
+    if (marks) marks[3]->record(ctx->stream);
 }
 
 void fill_report(slq_report* r, const slq::LsqrOut& o) {
@@ -288,9 +286,17 @@ Operand host_dense_operand(slq_ctx* ctx, slq_dense* Ad, const double* Ah, int64_
     return o;
 }
 
+// RAII: inside a solve, device-detected errors go to P.status (no mid-solve
+// host reads); restored on every exit path
+struct DeferGuard {
+    slq_ctx* ctx;
+    DeferGuard(slq_ctx* c, double* status) : ctx(c) { ctx->defer_status = status; }
+    ~DeferGuard() { ctx->defer_status = nullptr; }
+};
+
 int run_solve(slq_ctx* ctx, const Operand& A, int64_t d, int64_t zeta, uint64_t seed, const slq_solve_opts* opts_in,
               double* x_out, slq_report* report, slq_phase_times* times, double* est) {
-    return guarded([&] {
+    const int rc = guarded([&] {
         need(ctx != nullptr, SLQ_INVALID_ARG, "solve: null handle");
         slq_solve_opts opts;
         if (opts_in) opts = *opts_in;
@@ -302,6 +308,13 @@ int run_solve(slq_ctx* ctx, const Operand& A, int64_t d, int64_t zeta, uint64_t 
         const int64_t launches0 = ctx->launches, nccl0 = ctx->nccl_calls;
         slq::Workspace& ws = ctx->ws;
         double* Yaug = static_cast<double*>(ws.yaug.ensure(sizeof(double) * d * (n + 1)));
+        PrecondBufs P = precond_bufs(ctx, n);
+        // The whole solve is enqueued without a host round trip: device-side
+        // error conditions land in P.status (broadcast with M on multiple
+        // GPUs; LSQR turns into no-ops when it is set) and are read once at
+        // the end together with x.
+        SLQ_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(double), ctx->stream));
+        DeferGuard defer(ctx, P.status);
 
         // SLQ_TRACE=1: host timestamps per phase on stderr (diagnostics)
         static const bool trace = std::getenv("SLQ_TRACE") != nullptr;
@@ -318,40 +331,36 @@ int run_solve(slq_ctx* ctx, const Operand& A, int64_t d, int64_t zeta, uint64_t 
         Timer t2(ctx->stream);
         slq::reduce_sum_root(ctx, Yaug, d * (n + 1));
         Timer t3(ctx->stream);
-        PrecondBufs P = precond_bufs(ctx, n);
-        double tq[3] = {0, 0, 0};
+        Timer q0(ctx->stream), q1(ctx->stream), q2(ctx->stream), q3(ctx->stream);
+        Timer* const qm[4] = {&q0, &q1, &q2, &q3};
+        std::string root_error;
         if (ctx->rank == 0) {
-            double st = 0.0;
+            int code = SLQ_OK;
             try {
-                build_precond_dev(ctx, Yaug, d, n, true, nullptr, P, tq);
+                build_precond_dev(ctx, Yaug, d, n, true, nullptr, P, qm);
             } catch (const slq::Error& e) {
-                if (!ctx->comm) throw;
-                st = e.code;
-                g_last_error = e.what();
+                code = e.code;
+                root_error = e.what();
             } catch (const std::bad_alloc&) {
                 // any failure on rank 0 must still reach the status broadcast,
                 // or ranks 1..N-1 would block in ncclBroadcast forever
-                if (!ctx->comm) throw;
-                st = SLQ_OOM;
-                g_last_error = "preconditioner build: host allocation failed";
+                code = SLQ_OOM;
+                root_error = "preconditioner build: host allocation failed";
             } catch (const std::exception& e) {
-                if (!ctx->comm) throw;
-                st = SLQ_CUDA;
-                g_last_error = e.what();
+                code = SLQ_CUDA;
+                root_error = e.what();
             }
-            if (ctx->comm) {
+            if (code != SLQ_OK) {
+                if (!slq::has_comm(ctx)) slq::fail(code, root_error);
+                const double st = code;
                 SLQ_CUDA_CHECK(cudaMemcpyAsync(P.status, &st, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-                SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
             }
         }
         Timer t4(ctx->stream);
-        if (ctx->comm) {
-            // status first so no rank waits on a broadcast that will never come
+        if (slq::has_comm(ctx)) {
+            // status travels with M, M^T, x0: every rank learns of a rank-0
+            // failure from the same broadcasts, without a host round trip
             slq::broadcast_root(ctx, P.status, 1);
-            double st = 0.0;
-            SLQ_CUDA_CHECK(cudaMemcpyAsync(&st, P.status, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-            SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-            if (st != 0.0) slq::fail(static_cast<int>(st), ctx->rank == 0 ? g_last_error : "preconditioner build failed on rank 0");
             slq::broadcast_root(ctx, P.M, n * n);
             slq::broadcast_root(ctx, P.Mt, n * n);
             slq::broadcast_root(ctx, P.x0, n);
@@ -361,21 +370,35 @@ int run_solve(slq_ctx* ctx, const Operand& A, int64_t d, int64_t zeta, uint64_t 
         double* x = static_cast<double*>(ws.xbuf.ensure(sizeof(double) * (n + 8)));
         slq::LsqrOut lo;
         auto op = A.make_op();
-        slq::lsqr_dev(ctx, *op, nullptr, P.M, P.Mt, P.x0, x, opts, est, nullptr, nullptr, lo);
+        slq::lsqr_dev(ctx, *op, nullptr, P.M, P.Mt, P.x0, x, opts, est, nullptr, nullptr, lo, P.status);
         mark("lsqr");
         Timer t6(ctx->stream);
+        double st = 0.0;
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(&st, P.status, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (st != 0.0) {
+            const int code = static_cast<int>(st);
+            if (code == slq::kStatusSketchOverflow) slq::fail(code, "sketch bucket overflow");
+            if (!root_error.empty()) slq::fail(code, root_error);
+            slq::fail(code, code == SLQ_RANK_DEFICIENT     ? "householder_qr: the sketch is numerically rank deficient"
+                            : code == SLQ_SINGULAR_TRIANGULAR ? "tri_inverse: zero diagonal"
+                            : ctx->rank == 0                  ? "solve failed on the device"
+                                                              : "preconditioner build failed on rank 0");
+        }
         if ((opts.backward_tol > 0.0 || opts.a_norm_est > 0.0) && lo.backward_error < 0.0)
             lo.backward_error = slq::backward_error_dev(ctx, *op, nullptr, x, opts.a_norm_est > 0.0 ? opts.a_norm_est : 1.0);
         if (x_out) SLQ_CUDA_CHECK(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
         fill_report(report, lo);
         mark("finish");
         if (times) {
+            // QR / R^-1 / x0 split from the events build_precond_dev recorded
+            const double tq[3] = {q1.since(q0), q2.since(q1), q3.since(q2)};
             times->generate = t1.since(t0);
             times->apply = t2.since(t1);
             times->reduce = t3.since(t2);
-            times->qr = tq[0];
-            times->inverse = tq[1];
-            times->x0 = tq[2] + t5.since(t4);
+            times->qr = ctx->rank == 0 ? tq[0] : 0.0;
+            times->inverse = ctx->rank == 0 ? tq[1] : 0.0;
+            times->x0 = (ctx->rank == 0 ? tq[2] : 0.0) + t5.since(t4);
             times->lsqr = t6.since(t5);
             times->total = t6.since(t0);
             times->lsqr_per_iteration = lo.iterations > 0 ? lo.seconds / static_cast<double>(lo.iterations) : 0.0;
@@ -383,6 +406,14 @@ int run_solve(slq_ctx* ctx, const Operand& A, int64_t d, int64_t zeta, uint64_t 
             times->kernel_launches = ctx->launches - launches0;
         }
     });
+    if (rc == slq::kStatusSketchOverflow && ctx && !ctx->force_row_gather) {
+        // a K2d bucket overflowed (recorded on the device): redo with the register gather
+        ctx->force_row_gather = true;
+        const int rc2 = run_solve(ctx, A, d, zeta, seed, opts_in, x_out, report, times, est);
+        ctx->force_row_gather = false;
+        return rc2;
+    }
+    return rc;
 }
 
 }  // namespace
@@ -487,6 +518,13 @@ int slq_ctx_synchronize(slq_ctx* ctx) {
 }
 
 int64_t slq_ctx_kernel_launches(const slq_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int slq_ctx_set_host_comm(slq_ctx* ctx, const slq_host_comm* comm, int rank, int nranks) {
+    return guarded([&] {
+        need(ctx && comm, SLQ_INVALID_ARG, "set_host_comm: null argument");
+        slq::comm_set_host(ctx, *comm, rank, nranks);
+    });
+}
 
 int slq_comm_unique_id(unsigned char id_out[128]) {
     return guarded([&] { slq::comm_unique_id(id_out); });
@@ -780,13 +818,14 @@ int slq_build_preconditioner(slq_ctx* ctx, const double* Y, int64_t d, int64_t n
         slq::DevBuf dQ;
         double* q = Q ? static_cast<double*>(dQ.ensure(sizeof(double) * std::max<int64_t>(1, d * n))) : nullptr;
         PrecondBufs P = precond_bufs(ctx, n);
-        double t[3] = {0, 0, 0};
-        build_precond_dev(ctx, Yaug, d, n, with_sb, q, P, t);
+        Timer q0(ctx->stream), q1(ctx->stream), q2(ctx->stream), q3(ctx->stream);
+        Timer* const qm[4] = {&q0, &q1, &q2, &q3};
+        build_precond_dev(ctx, Yaug, d, n, with_sb, q, P, qm);
         SLQ_CUDA_CHECK(cudaMemcpyAsync(M, P.M, sizeof(double) * n * n, cudaMemcpyDeviceToHost, ctx->stream));
         if (Q) SLQ_CUDA_CHECK(cudaMemcpyAsync(Q, q, sizeof(double) * d * n, cudaMemcpyDeviceToHost, ctx->stream));
         if (x0 && with_sb) SLQ_CUDA_CHECK(cudaMemcpyAsync(x0, P.x0, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
         SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-        if (build_time) *build_time = t[0] + t[1];
+        if (build_time) *build_time = q2.since(q0);  // QR + inversion
     });
 }
 

@@ -56,7 +56,33 @@ void nccl_check(ncclResult_t r, const char* what) {
     if (r != ncclSuccess) fail(SLQ_NCCL, std::string(what) + ": " + api().errorString(r));
 }
 
+// Host collectives: stream sync, D2H into pinned staging, the caller's
+// callback, H2D back (stream-ordered).
+void host_collective(slq_ctx* ctx, double* buf, int64_t count, int (*fn)(void*, double*, int64_t)) {
+    if (count > ctx->host_stage_n) {
+        if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+        ctx->host_stage = nullptr;
+        SLQ_CUDA_CHECK(cudaMallocHost(&ctx->host_stage, sizeof(double) * count));
+        ctx->host_stage_n = count;
+    }
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(ctx->host_stage, buf, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (fn(ctx->host_comm.user, ctx->host_stage, count) != 0) fail(SLQ_NCCL, "host collective failed");
+    SLQ_CUDA_CHECK(cudaMemcpyAsync(buf, ctx->host_stage, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->nccl_calls++;
+}
+
 }  // namespace
+
+void comm_set_host(slq_ctx* ctx, const slq_host_comm& hc, int rank, int nranks) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(SLQ_INVALID_DIMS, "set_host_comm: bad rank / size");
+    if (!hc.allreduce_sum || !hc.reduce_sum_root || !hc.broadcast_root)
+        fail(SLQ_INVALID_ARG, "set_host_comm: all three collectives are required");
+    comm_destroy(ctx);
+    ctx->host_comm = hc;
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+}
 
 void comm_unique_id(unsigned char out[128]) {
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
@@ -67,10 +93,7 @@ void comm_unique_id(unsigned char out[128]) {
 
 void comm_init(slq_ctx* ctx, const unsigned char id[128], int rank, int nranks) {
     if (nranks < 1 || rank < 0 || rank >= nranks) fail(SLQ_INVALID_DIMS, "comm_init: bad rank / size");
-    if (ctx->comm) {
-        api().commDestroy(static_cast<ncclComm_t>(ctx->comm));
-        ctx->comm = nullptr;
-    }
+    comm_destroy(ctx);
     ctx->rank = rank;
     ctx->nranks = nranks;
     // single rank: collectives are identities and are skipped, unless
@@ -88,11 +111,16 @@ void comm_init(slq_ctx* ctx, const unsigned char id[128], int rank, int nranks) 
 void comm_destroy(slq_ctx* ctx) {
     if (ctx->comm) api().commDestroy(static_cast<ncclComm_t>(ctx->comm));
     ctx->comm = nullptr;
+    ctx->host_comm = slq_host_comm{};
+    if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+    ctx->host_stage = nullptr;
+    ctx->host_stage_n = 0;
 }
 
 // distsim.hpp:312-331 dist_rmatvec_and_norm's one reduction: sum of the
 // per-rank {A^T u partial, ||u||^2 partial}, result on every rank.
 void allreduce_sum(slq_ctx* ctx, double* buf, int64_t count) {
+    if (ctx->host_comm.allreduce_sum) return host_collective(ctx, buf, count, ctx->host_comm.allreduce_sum);
     if (!ctx->comm) return;
     nccl_check(api().allReduce(buf, buf, static_cast<size_t>(count), ncclDouble, ncclSum,
                                static_cast<ncclComm_t>(ctx->comm), ctx->stream),
@@ -102,6 +130,7 @@ void allreduce_sum(slq_ctx* ctx, double* buf, int64_t count) {
 
 // distsim.hpp:383-396 dist_sketch_apply's reduction of d x n partials (to rank 0).
 void reduce_sum_root(slq_ctx* ctx, double* buf, int64_t count) {
+    if (ctx->host_comm.reduce_sum_root) return host_collective(ctx, buf, count, ctx->host_comm.reduce_sum_root);
     if (!ctx->comm) return;
     nccl_check(api().reduce(buf, buf, static_cast<size_t>(count), ncclDouble, ncclSum, 0,
                             static_cast<ncclComm_t>(ctx->comm), ctx->stream),
@@ -111,6 +140,7 @@ void reduce_sum_root(slq_ctx* ctx, double* buf, int64_t count) {
 
 // The preconditioner hand-off (SPEC: worker 0 builds, everyone uses).
 void broadcast_root(slq_ctx* ctx, double* buf, int64_t count) {
+    if (ctx->host_comm.broadcast_root) return host_collective(ctx, buf, count, ctx->host_comm.broadcast_root);
     if (!ctx->comm) return;
     nccl_check(api().broadcast(buf, buf, static_cast<size_t>(count), ncclDouble, 0,
                                static_cast<ncclComm_t>(ctx->comm), ctx->stream),

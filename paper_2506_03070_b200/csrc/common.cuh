@@ -100,6 +100,9 @@ struct slq_ctx {
     slq::Workspace ws;
     // multi-GPU (NCCL communicator stored as void* to keep nccl.h local to comm.cu)
     void* comm = nullptr;
+    slq_host_comm host_comm{};     // caller-provided host collectives (instead of NCCL)
+    double* host_stage = nullptr;  // pinned staging for host collectives
+    int64_t host_stage_n = 0;
     int rank = 0;
     int nranks = 1;
     int64_t nccl_calls = 0;
@@ -111,6 +114,12 @@ struct slq_ctx {
     cudaEvent_t qr_ev[3] = {nullptr, nullptr, nullptr};
     int* lsqr_hdone = nullptr;            // pinned done-flag mirror (2 ints)
     int64_t lsqr_live_m = -1, lsqr_live_n = -1;  // shape whose LSQR vectors the workspace holds
+    // Inside slq_solve: error conditions found on the device (rank-deficient
+    // sketch, zero diagonal of R, a sketch bucket overflow) are recorded in
+    // this device word instead of being read back mid-solve; the solve checks
+    // it once at the end (and broadcasts it with M on multiple GPUs).
+    double* defer_status = nullptr;
+    bool force_row_gather = false;  // rerun after a K2d bucket overflow
     cudaEvent_t lsqr_ev[2] = {nullptr, nullptr};
 };
 
@@ -142,6 +151,19 @@ struct slq_sparse {
 namespace slq {
 
 constexpr int64_t kSparseRowPad = 256;
+
+// a communicator of either kind is attached (collectives are issued)
+inline bool has_comm(const slq_ctx* c) { return c->comm != nullptr || c->host_comm.allreduce_sum != nullptr; }
+
+// Internal (non-C-ABI) device status: a K2d bucket overflowed; the solve is
+// redone with the register gather.
+constexpr int kStatusSketchOverflow = 1000;
+
+// Record `code` in ctx->defer_status (first error wins) when the device int
+// `flag` meets the condition: kCondNonzero (flag[0] != 0), kCondNotBig
+// (flag[0] != INT_MAX), kCondAny2 (flag[0] | flag[1]).  Stream-ordered, no sync.
+enum DeferCond : int { kCondNonzero = 0, kCondNotBig = 1, kCondAny2 = 2 };
+void defer_status_dev(slq_ctx* ctx, const int* flag, int cond, int code);
 
 // Row stride of the device layout: [A | b | zero pad], 32-byte aligned rows.
 inline int64_t dense_ld(int64_t n) { return round_up(n + 1, 4); }

@@ -28,6 +28,8 @@
 #include <cmath>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "lsqr.cuh"
 #include "ptx.cuh"
 
@@ -83,6 +85,7 @@ struct PassArgs {
     int want_z;
     const int* skip;       // nonzero -> no-op
     int R, S;              // rows per tile, stages
+    int keep_l2;           // A small enough to stay L2-resident across passes: evict_last, else evict_first
 };
 
 template <int NP, bool P_SMEM>
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
     if (warp == kConsumerWarps) {
         // ---------------- producer: one elected lane streams row tiles
         if (lane == 0) {
-            const uint64_t pol = evict_first_policy();
+            const uint64_t pol = a.keep_l2 ? evict_last_policy() : evict_first_policy();
             for (int64_t k = 0; k < nt; ++k) {
                 const int s = static_cast<int>(k % a.S);
                 const int64_t r = k / a.S;
@@ -237,6 +240,16 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
     }
 }
 
+// a failed preconditioner build (device status != 0): the whole solve becomes no-ops
+__global__ void lsqr_abort_kernel(const double* status, LsqrState* st) {
+    if (threadIdx.x == 0 && *status != 0.0) {
+        st->done = 1;
+        st->term = SLQ_TERM_MAXITER;
+        st->iters = 0;
+        st->mode = kModeSkip;
+    }
+}
+
 // partials [G][n+1] -> out[n+1], fixed order: thread (c, g) sums partials
 // g, g+8, ... of column c, then the 8 sums are added in order g = 0..7.
 __global__ void __launch_bounds__(256) reduce_partials_kernel(const double* part, int G, int64_t n1, double* out,
@@ -305,9 +318,10 @@ struct MtzArgs {
     int init;
 };
 
-__device__ void scalar_step(const MtzArgs& a, double beta, double alpha_next) {
-    LsqrState& st = *a.st;
-    if (a.init) {
+// The scalar recurrence of one iteration (lsqr.hpp:58-94 init, :98-166 step)
+// on a state copy; est_hist may be null (redundant copies in the fused K5).
+__device__ void scalar_step_state(LsqrState& st, int init, double* est_hist, double beta, double alpha_next) {
+    if (init) {
         st.beta1 = beta;
         st.t = 1;
         if (beta == 0.0 || alpha_next == 0.0) {
@@ -338,7 +352,7 @@ __device__ void scalar_step(const MtzArgs& a, double beta, double alpha_next) {
         const double phi = c * st.phi_bar;
         st.phi_bar = s * st.phi_bar;
         st.coef_x = phi / rho;
-        a.est_hist[t - 1] = st.phi_bar;
+        if (est_hist) est_hist[t - 1] = st.phi_bar;
         st.done = 1;
         st.term = SLQ_TERM_BREAKDOWN;
         st.iters = t;
@@ -364,7 +378,7 @@ __device__ void scalar_step(const MtzArgs& a, double beta, double alpha_next) {
     st.coef_w = -theta / rho;
     st.alpha = alpha_next;
     st.c_next = -alpha_next * (1.0 / beta);
-    a.est_hist[t - 1] = st.phi_bar;
+    if (est_hist) est_hist[t - 1] = st.phi_bar;
     st.mode = kModeIter;
     // ||(AM)^T r_t|| / ||r_t|| = alpha_{t+1} |c_t| (Paige & Saunders; ||r_t|| ~ phi_bar_{t+1})
     st.bw_est = alpha_next * fabs(c);
@@ -418,7 +432,7 @@ __global__ void __launch_bounds__(256) mtz_kernel(MtzArgs a) {
         const double s = block0_sum_fixed(a.part2, gridDim.x);
         if (threadIdx.x == 0) {
             a.st->counter_mtz = 0;
-            scalar_step(a, beta, sqrt(s));
+            scalar_step_state(*a.st, a.init, a.est_hist, beta, sqrt(s));
         }
     }
 }
@@ -473,6 +487,133 @@ __global__ void __launch_bounds__(256) mv_update_kernel(MvArgs a) {
     if (last && threadIdx.x == 0) {
         a.st->counter_mv = 0;
         if (a.st->done) a.st->mode = kModeSkip;
+    }
+}
+
+// ------------------------------------------------------- K5 fused (one launch)
+//
+// reduce_partials + mtz + mv_update as ONE cooperative kernel with two grid
+// barriers: (A, single GPU only) the per-CTA pass partials summed into z in a
+// fixed order, 8 lanes per column; (B) v_hat = M^T z / beta - beta v, warp per
+// column, and per-CTA sums of v_hat^2; (C) every CTA sums those in the same
+// fixed order and runs the scalar recurrence on its own copy of the state
+// (identical bits everywhere, so no broadcast is needed), then v = v_hat /
+// alpha, p = M v (warp per row of M^T), x += (phi/rho) w, w = p - (theta/rho) w
+// for its rows; CTA 0 writes the state back.  Replaces three launches and two
+// "last CTA" handoffs per iteration.
+
+struct K5Args {
+    const double* M;    // column-major n x n upper
+    const double* Mt;   // row-major copy
+    int64_t n;
+    const double* part; // pass partials [G_part][n+1], or null: zt already summed (NCCL allreduce)
+    int G_part;
+    double* zt;         // [n+1]: A^T u_hat | ||u_hat||^2
+    double* v;
+    double* vhat;
+    double* p;
+    double* w;
+    double* x;
+    double* part2;      // [gridDim]
+    LsqrState* st;
+    double* est_hist;
+    int init;
+};
+
+__global__ void __launch_bounds__(256) k5_fused_kernel(K5Args a) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ LsqrState s;
+    __shared__ double wsum[8];
+    if (a.st->done) return;  // written by an earlier kernel: the same value in every CTA
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * 8;
+    const int64_t n = a.n;
+    if (threadIdx.x == 0) s = *a.st;  // read before any CTA writes the state (after the last barrier)
+    // (A) z = sum of the pass partials: 8 lanes per column, each summing every 8th
+    // partial with 4 loads in flight, then a fixed xor tree inside the group
+    if (a.part) {
+        const int sub = lane & 7;
+        const int64_t n1 = n + 1;
+        for (int64_t j0 = gwarp * 4; j0 < n1; j0 += nwarps * 4) {
+            const int64_t j = j0 + (lane >> 3);
+            double acc[4] = {0, 0, 0, 0};
+            if (j < n1) {
+                int g = sub;
+                for (; g + 24 < a.G_part; g += 32) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc[u] += __ldcg(a.part + static_cast<int64_t>(g + 8 * u) * n1 + j);
+                }
+                for (int u = 0; g < a.G_part; g += 8, ++u) acc[u & 3] += __ldcg(a.part + static_cast<int64_t>(g) * n1 + j);
+            }
+            // the 8 group sums added in ascending order: the same bits as
+            // reduce_partials_kernel (so a one-rank NCCL run equals this one)
+            const double gs = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+            double t = gs;
+#pragma unroll
+            for (int q = 1; q < 8; ++q) {
+                const double o = __shfl_sync(0xffffffffu, gs, (lane & ~7) + q);
+                t += o;
+            }
+            if (sub == 0 && j < n1) a.zt[j] = t;
+        }
+        grid.sync();
+    }
+    // (B) v_hat_j = M(:, j)^T (z * zs) [- beta v_j], warp per column
+    const double beta = sqrt(__ldcg(a.zt + n));
+    const double zs = a.init ? (-1.0 / beta) : (1.0 / beta);
+    double ss = 0.0;
+    for (int64_t j = gwarp; j < n; j += nwarps) {
+        const double* col = a.M + j * n;
+        double d = lane_dot(0, j + 1, lane, [&](int64_t i) { return col[i] * (__ldcg(a.zt + i) * zs); });
+        d = warp_sum(d);
+        const double vh = a.init ? d : __dadd_rn(d, __dmul_rn(-beta, a.v[j]));  // lsqr.hpp:137
+        if (lane == 0) a.vhat[j] = vh;
+        ss += vh * vh;  // lane 0's value is the one kept (identical on every lane)
+    }
+    if (lane == 0) wsum[warp] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int q = 0; q < 8; ++q) t += wsum[q];
+        a.part2[blockIdx.x] = t;
+    }
+    grid.sync();
+    // (C) alpha from the per-CTA sums (same order in every CTA), scalar step on the local copy
+    if (warp == 0) {
+        const double t = block0_sum_fixed(a.part2, gridDim.x);
+        if (lane == 0) scalar_step_state(s, a.init, blockIdx.x == 0 ? a.est_hist : nullptr, beta, sqrt(t));
+    }
+    __syncthreads();
+    const int mode = s.mode;
+    if (mode == kModeFinal) {
+        for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            a.x[i] = __dadd_rn(a.x[i], __dmul_rn(s.coef_x, a.w[i]));
+    } else if (mode != kModeSkip) {
+        const double inv_alpha = 1.0 / s.alpha;  // lsqr.hpp:141 scal(1/alpha, v_hat)
+        for (int64_t i = gwarp; i < n; i += nwarps) {
+            const double* row = a.Mt + i * n;
+            double d = lane_dot(i, n, lane, [&](int64_t j) { return row[j] * (__ldcg(a.vhat + j) * inv_alpha); });
+            d = warp_sum(d);
+            if (lane == 0) {
+                a.v[i] = __ldcg(a.vhat + i) * inv_alpha;
+                a.p[i] = d;
+                if (mode == kModeInit) {
+                    a.w[i] = d;  // lsqr.hpp:92
+                } else {
+                    const double wi = a.w[i];
+                    a.x[i] = __dadd_rn(a.x[i], __dmul_rn(s.coef_x, wi));  // lsqr.hpp:155
+                    a.w[i] = __dadd_rn(d, __dmul_rn(s.coef_w, wi));       // lsqr.hpp:156-158
+                }
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        LsqrState out = s;
+        if (out.done) out.mode = kModeSkip;
+        *a.st = out;
     }
 }
 
@@ -575,22 +716,30 @@ public:
     DenseOp(slq_ctx* ctx, const slq_dense* A) : A_(A), pp_(plan_pass(ctx, A)) {
         m = A->m;
         n = A->n;
+        // an A that fits comfortably in L2 (126 MB; e.g. config C1's 80 MB) is
+        // kept there across the LSQR passes instead of streamed evict-first
+        // (SLQ_L2_KEEP_MB overrides the threshold, diagnostics)
+        double keep_mb = 96.0;
+        if (const char* e = std::getenv("SLQ_L2_KEEP_MB")) keep_mb = std::atof(e);
+        keep_l2_ = 8.0 * static_cast<double>(A->m) * static_cast<double>(A->ld) <= keep_mb * 1048576.0 ? 1 : 0;
     }
     int grid() const override { return pp_.grid; }
     void pass(slq_ctx* ctx, const PassCall& c) const override {
-        PassArgs a{A_->A, A_->ld, m, n, c.p, c.u_in, c.u_out, c.coef, c.c_fixed, c.part, c.want_z, c.skip, 0, 0};
+        PassArgs a{A_->A, A_->ld, m, n, c.p, c.u_in, c.u_out, c.coef, c.c_fixed, c.part, c.want_z, c.skip, 0, 0,
+                   keep_l2_};
         launch_pass(ctx, pp_, a);
     }
     std::vector<uint64_t> key() const override {
         return {1, reinterpret_cast<uint64_t>(A_->A), static_cast<uint64_t>(m), static_cast<uint64_t>(n),
                 static_cast<uint64_t>(A_->ld), static_cast<uint64_t>(pp_.grid), static_cast<uint64_t>(pp_.R),
-                static_cast<uint64_t>(pp_.S)};
+                static_cast<uint64_t>(pp_.S), static_cast<uint64_t>(keep_l2_)};
     }
     double pass_bytes() const override { return 8.0 * m * n + 16.0 * m; }
 
 private:
     const slq_dense* A_;
     PassPlan pp_;
+    int keep_l2_ = 0;
 };
 
 struct LsqrBufs {
@@ -606,12 +755,22 @@ std::unique_ptr<PassOp> make_dense_op(slq_ctx* ctx, const slq_dense* A) {
 
 void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* M, const double* Mt,
               const double* x0, double* x, const slq_solve_opts& opts, double* est_hist,
-              double* err_hist, double* true_hist, LsqrOut& out) {
+              double* err_hist, double* true_hist, LsqrOut& out, const double* abort) {
     const int64_t m = op.m, n = op.n;
     const int64_t maxit = std::max<int64_t>(0, opts.maxit);
     Workspace& ws = ctx->ws;
     const int grid = op.grid();
     const int mtz_grid = static_cast<int>(std::max<int64_t>(1, ceil_div(n, 8)));
+    // fused K5: one cooperative launch per iteration (SLQ_NO_FUSED_K5=1: the
+    // three-kernel form, kept for A/B measurements)
+    static const bool no_fused = slq_env_flag("SLQ_NO_FUSED_K5");
+    int k5_grid = 0;
+    if (!no_fused) {
+        int per_sm = 0;
+        SLQ_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k5_fused_kernel, 256, 0));
+        k5_grid = static_cast<int>(std::min<int64_t>(mtz_grid, static_cast<int64_t>(per_sm) * ctx->num_sms));
+    }
+    const bool fused = k5_grid > 0;
 
     // workspace layout
     const size_t nvec = static_cast<size_t>(n + 8);
@@ -637,6 +796,10 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
     SLQ_CUDA_CHECK(cudaMemcpyAsync(B.st, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
     SLQ_CUDA_CHECK(cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
     const int* done_flag = &B.st->done;
+    if (abort) {
+        lsqr_abort_kernel<<<1, 32, 0, ctx->stream>>>(abort, B.st);
+        SLQ_LAUNCH_CHECK(ctx);
+    }
 
     cudaEvent_t e0, e1;
     SLQ_CUDA_CHECK(cudaEventCreate(&e0));
@@ -703,37 +866,62 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
         }
     };
 
-    // ---- init: u_hat = A x0 - b, z = A^T u_hat, ||u_hat||^2 (one pass)
-    int64_t allreduces = 0;
-    {
-        op.pass(ctx, PassCall{x0, b_dev, B.u, nullptr, -1.0, B.part, 1, nullptr});
-        reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 32)), 256, 0, ctx->stream>>>(
-            B.part, grid, n + 1, B.zt, nullptr);
-        SLQ_LAUNCH_CHECK(ctx);
-        allreduce_sum(ctx, B.zt, n + 1);
-        if (ctx->comm) ++allreduces;
-        if (instrument) record();
-        MtzArgs ma{M, n, B.zt, B.v, B.vhat, B.part2, B.st, B.hist, 1};
+    // K5 after the partials of a pass: fused cooperative kernel, or mtz + mv_update
+    auto k5 = [&](int init) {
+        if (fused) {
+            // with NCCL (or at init, where zt is summed above) z is already reduced
+            const bool sum_here = !init && !has_comm(ctx);
+            K5Args ka{M, Mt, n, sum_here ? B.part : nullptr, grid, B.zt, B.v, B.vhat, B.p, B.w, x, B.part2, B.st,
+                      B.hist, init};
+            void* args[] = {&ka};
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<unsigned>(k5_grid));
+            cfg.blockDim = dim3(256);
+            cfg.stream = ctx->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeCooperative;
+            at[0].val.cooperative = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            SLQ_CUDA_CHECK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k5_fused_kernel), args));
+            SLQ_LAUNCH_CHECK(ctx);
+            return;
+        }
+        MtzArgs ma{M, n, B.zt, B.v, B.vhat, B.part2, B.st, B.hist, init};
         mtz_kernel<<<mtz_grid, 256, 0, ctx->stream>>>(ma);
         SLQ_LAUNCH_CHECK(ctx);
         MvArgs va{Mt, n, B.vhat, B.v, B.p, B.w, x, B.st};
         mv_update_kernel<<<mtz_grid, 256, 0, ctx->stream>>>(va);
         SLQ_LAUNCH_CHECK(ctx);
+    };
+
+    // ---- init: u_hat = A x0 - b, z = A^T u_hat, ||u_hat||^2 (one pass)
+    int64_t allreduces = 0;
+    {
+        op.pass(ctx, PassCall{x0, b_dev, B.u, nullptr, -1.0, B.part, 1, abort ? done_flag : nullptr});
+        reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 32)), 256, 0, ctx->stream>>>(
+            B.part, grid, n + 1, B.zt, abort ? done_flag : nullptr);
+        SLQ_LAUNCH_CHECK(ctx);
+        allreduce_sum(ctx, B.zt, n + 1);
+        if (has_comm(ctx)) ++allreduces;
+        if (instrument) record();
+        k5(1);
     }
     const int64_t init_allreduces = allreduces;
 
+    // kernels per iteration: pass + (reduce + allreduce when multi-GPU) + fused K5, or the 3-kernel K5
+    const int launches_per_iter = 1 + (fused ? (has_comm(ctx) ? 2 : 1) : 3);
     auto enqueue_iteration = [&]() {
         op.pass(ctx, PassCall{B.p, B.u, B.u, &B.st->c_next, 0.0, B.part, 1, done_flag});
+        if (fused && !has_comm(ctx)) {
+            k5(0);  // sums the pass partials itself
+            return;
+        }
         reduce_partials_kernel<<<static_cast<unsigned>(ceil_div(n + 1, 32)), 256, 0, ctx->stream>>>(
             B.part, grid, n + 1, B.zt, done_flag);
         SLQ_LAUNCH_CHECK(ctx);
         allreduce_sum(ctx, B.zt, n + 1);
-        MtzArgs ma{M, n, B.zt, B.v, B.vhat, B.part2, B.st, B.hist, 0};
-        mtz_kernel<<<mtz_grid, 256, 0, ctx->stream>>>(ma);
-        SLQ_LAUNCH_CHECK(ctx);
-        MvArgs va{Mt, n, B.vhat, B.v, B.p, B.w, x, B.st};
-        mv_update_kernel<<<mtz_grid, 256, 0, ctx->stream>>>(va);
-        SLQ_LAUNCH_CHECK(ctx);
+        k5(0);
     };
 
     LsqrState hs{};
@@ -745,7 +933,7 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
                 SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
                 if (hs.done) break;
                 enqueue_iteration();
-                if (ctx->comm) ++allreduces;
+                if (has_comm(ctx)) ++allreduces;
                 SLQ_CUDA_CHECK(cudaMemcpyAsync(&hs, B.st, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
                 SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
                 // the reference returns before the hook on a breakdown (lsqr.hpp:120-141)
@@ -767,14 +955,17 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
         }
         if (remaining <= 0) return;
         constexpr int kBatch = 8;
-        const bool use_graph = ctx->stream != nullptr;
+        // host collectives synchronize inside each iteration: no graph
+        const bool use_graph = ctx->stream != nullptr && !ctx->host_comm.allreduce_sum;
         if (use_graph) {
             std::vector<uint64_t> key = op.key();
             const uint64_t extra[] = {
                 reinterpret_cast<uint64_t>(b_dev), reinterpret_cast<uint64_t>(M), reinterpret_cast<uint64_t>(Mt),
                 reinterpret_cast<uint64_t>(x), reinterpret_cast<uint64_t>(B.u), reinterpret_cast<uint64_t>(B.p),
                 reinterpret_cast<uint64_t>(B.part), reinterpret_cast<uint64_t>(B.st), reinterpret_cast<uint64_t>(B.hist),
-                reinterpret_cast<uint64_t>(ctx->comm), reinterpret_cast<uint64_t>(ctx->stream)};
+                reinterpret_cast<uint64_t>(ctx->comm), reinterpret_cast<uint64_t>(ctx->stream),
+                reinterpret_cast<uint64_t>(ctx->host_comm.allreduce_sum),
+                static_cast<uint64_t>(k5_grid)};
             key.insert(key.end(), std::begin(extra), std::end(extra));
             if (!ctx->lsqr_exec || ctx->lsqr_key != key) {
                 if (ctx->lsqr_exec) cudaGraphExecDestroy(ctx->lsqr_exec);
@@ -786,7 +977,7 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
                 SLQ_CUDA_CHECK(cudaGraphInstantiate(&ctx->lsqr_exec, graph, 0));
                 cudaGraphDestroy(graph);
                 ctx->lsqr_key = key;
-                ctx->launches -= 4 * kBatch;  // captured, not launched
+                ctx->launches -= launches_per_iter * kBatch;  // captured, not launched
             }
         }
         cudaGraphExec_t exec = use_graph ? ctx->lsqr_exec : nullptr;
@@ -812,7 +1003,7 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
         while (launched < remaining) {
             if (use_graph) {
                 SLQ_CUDA_CHECK(cudaGraphLaunch(exec, ctx->stream));
-                ctx->launches += 4 * kBatch;
+                ctx->launches += launches_per_iter * kBatch;
             } else {
                 for (int b = 0; b < kBatch; ++b) enqueue_iteration();
             }
@@ -893,7 +1084,7 @@ void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double*
     if (hs.term == SLQ_TERM_TOLERANCE && hs.iters == 0) out.n_estimate = 0;
     if (est_hist && out.n_estimate > 0)
         SLQ_CUDA_CHECK(cudaMemcpy(est_hist, B.hist, sizeof(double) * out.n_estimate, cudaMemcpyDeviceToHost));
-    if (ctx->comm) allreduces = init_allreduces + (instrument ? allreduces - init_allreduces : hs.iters);
+    if (has_comm(ctx)) allreduces = init_allreduces + (instrument ? allreduces - init_allreduces : hs.iters);
     out.allreduces = allreduces;
     out.init_allreduces = init_allreduces;
     out.seconds = ms * 1e-3;
@@ -1095,7 +1286,7 @@ void gd_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* M
                                                                                                 zt, &st->done);
         SLQ_LAUNCH_CHECK(ctx);
         allreduce_sum(ctx, zt, n + 1);
-        if (ctx->comm) ++allreduces;
+        if (has_comm(ctx)) ++allreduces;
         gd_h_kernel<<<vgrid, 256, 0, ctx->stream>>>(M, n, zt, h, vpart, st);
         SLQ_LAUNCH_CHECK(ctx);
         gd_x_kernel<<<vgrid, 256, 0, ctx->stream>>>(Mt, n, h, vpart, vgrid, alpha, beta, x, xp, hist, st);
@@ -1149,7 +1340,7 @@ void gd_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* M
     out.n_estimate = out.iterations;
     if (est_hist && out.n_estimate > 0)
         SLQ_CUDA_CHECK(cudaMemcpy(est_hist, hist, sizeof(double) * out.n_estimate, cudaMemcpyDeviceToHost));
-    out.allreduces = ctx->comm ? (instrument ? allreduces : out.iterations) : 0;
+    out.allreduces = has_comm(ctx) ? (instrument ? allreduces : out.iterations) : 0;
     out.init_allreduces = 0;
     out.seconds = ms * 1e-3;
     out.n_err = static_cast<int64_t>(herr.size());

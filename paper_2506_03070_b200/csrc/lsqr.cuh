@@ -49,9 +49,11 @@ struct LsqrOut {
     double backward_error = -1.0;
 };
 
+// abort (device, may be null): when *abort != 0 at the start the solve is a
+// no-op (the preconditioner build failed; the caller reports the error).
 void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* M, const double* Mt,
               const double* x0, double* x, const slq_solve_opts& opts, double* est_hist,
-              double* err_hist, double* true_hist, LsqrOut& out);
+              double* err_hist, double* true_hist, LsqrOut& out, const double* abort = nullptr);
 
 // gradient.hpp:56-115 gradient_descent_hbm (alpha, beta from hbm_params /
 // gd_params); one fused pass per iteration.  Throws SLQ_DIVERGENCE.
@@ -84,4 +86,5 @@ namespace slq {
 void comm_unique_id(unsigned char out[128]);
 void comm_init(slq_ctx* ctx, const unsigned char id[128], int rank, int nranks);
 void comm_destroy(slq_ctx* ctx);
+void comm_set_host(slq_ctx* ctx, const slq_host_comm& hc, int rank, int nranks);
 }  // namespace slq

@@ -84,5 +84,11 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     return p;
 }
 
+__device__ __forceinline__ uint64_t evict_last_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+
 }  // namespace ptx
 }  // namespace slq

@@ -856,6 +856,13 @@ __global__ void extract_r_kernel(const double* Y, int64_t ldy, int64_t n, double
     }
 }
 
+__global__ void defer_status_kernel(const int* flag, int cond, int code, double* status) {
+    if (threadIdx.x != 0 || *status != 0.0) return;
+    const bool hit = cond == kCondNonzero ? flag[0] != 0 : cond == kCondNotBig ? flag[0] != 0x7fffffff
+                                                                                : (flag[0] | flag[1]) != 0;
+    if (hit) *status = static_cast<double>(code);
+}
+
 __global__ void check_diag_kernel(const double* R, int64_t n, int* err) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n && R[i * n + i] == 0.0) atomicMin(err, static_cast<int>(i));
@@ -1316,10 +1323,14 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
     SLQ_CUDA_CHECK(cudaEventRecord(ev_p, s_hi));
     SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ev_p, 0));
     if (w_pending) SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ev_w, 0));
-    int herr = 0;
-    SLQ_CUDA_CHECK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-    if (herr) fail(SLQ_RANK_DEFICIENT, "householder_qr: column " + std::to_string(herr - 1) + " numerically dependent");
+    if (ctx->defer_status) {
+        defer_status_dev(ctx, err, kCondNonzero, SLQ_RANK_DEFICIENT);  // checked at the end of the solve
+    } else {
+        int herr = 0;
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (herr) fail(SLQ_RANK_DEFICIENT, "householder_qr: column " + std::to_string(herr - 1) + " numerically dependent");
+    }
 
     const double* qtb_col = (ncols > n && qtb) ? Yaug + n * ldy : nullptr;
     extract_r_kernel<<<static_cast<unsigned>(ceil_div(n * n, 256)), 256, 0, ctx->stream>>>(Yaug, ldy, n, R, sign,
@@ -1341,16 +1352,25 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
     }
 }
 
+void defer_status_dev(slq_ctx* ctx, const int* flag, int cond, int code) {
+    defer_status_kernel<<<1, 32, 0, ctx->stream>>>(flag, cond, code, ctx->defer_status);
+    SLQ_LAUNCH_CHECK(ctx);
+}
+
 void tri_inverse_dev(slq_ctx* ctx, const double* R, int64_t n, double* M, double* Mt) {
     int* err = static_cast<int*>(ctx->ws.flags.ensure(4096)) + 8;
     const int big = 0x7fffffff;
     SLQ_CUDA_CHECK(cudaMemcpyAsync(err, &big, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
     check_diag_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, ctx->stream>>>(R, n, err);
     SLQ_LAUNCH_CHECK(ctx);
-    int herr = 0;
-    SLQ_CUDA_CHECK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-    if (herr != big) fail(SLQ_SINGULAR_TRIANGULAR, "tri_inverse: zero diagonal at " + std::to_string(herr));
+    if (ctx->defer_status) {
+        defer_status_dev(ctx, err, kCondNotBig, SLQ_SINGULAR_TRIANGULAR);  // checked at the end of the solve
+    } else {
+        int herr = 0;
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (herr != big) fail(SLQ_SINGULAR_TRIANGULAR, "tri_inverse: zero diagonal at " + std::to_string(herr));
+    }
     if (n == 0) return;
     zero_lower_blocks_kernel<<<static_cast<unsigned>(ceil_div(n * n, 256)), 256, 0, ctx->stream>>>(M, n);
     SLQ_LAUNCH_CHECK(ctx);

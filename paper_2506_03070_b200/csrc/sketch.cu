@@ -1100,10 +1100,16 @@ bool sketch_apply_dmma(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32
     gather_dmma_kernel<<<dim3(static_cast<unsigned>(nrb), static_cast<unsigned>(nslabs), static_cast<unsigned>(nsplit)),
                          1024, smem, ctx->stream>>>(map, g);
     SLQ_LAUNCH_CHECK(ctx);
-    int hflag[2] = {0, 0};
-    SLQ_CUDA_CHECK(cudaMemcpyAsync(hflag, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-    if (hflag[0] || hflag[1]) return false;
+    if (ctx->defer_status) {
+        // inside a solve: an overflow (never seen at the shipped capacities) is
+        // recorded on the device and the solve is redone with the register gather
+        defer_status_dev(ctx, flags, kCondAny2, kStatusSketchOverflow);
+    } else {
+        int hflag[2] = {0, 0};
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(hflag, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        if (hflag[0] || hflag[1]) return false;
+    }
     if (Yw != Y) {
         if (nsplit == 1) {
             SLQ_CUDA_CHECK(cudaMemcpyAsync(Y, Yw, sizeof(double) * d * ncols_out, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1120,6 +1126,10 @@ bool sketch_apply_dmma(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32
 }  // namespace
 
 void check_chunk_csr(slq_ctx* ctx, const ChunkCsr& cc) {
+    if (ctx->defer_status) {  // inside a solve: checked once at the end
+        defer_status_dev(ctx, cc.flag, kCondNonzero, SLQ_UNSUPPORTED);
+        return;
+    }
     int hflag = 0;
     SLQ_CUDA_CHECK(cudaMemcpyAsync(&hflag, cc.flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
@@ -1216,7 +1226,7 @@ void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const
     // chunk keep its lanes busy; zeta <= 2 with d >= 2048 -- too little work
     // per A row to repay the tile gather's per-row-block restaging)
     const bool row_gather = slq_env_flag("SLQ_ROW_GATHER") ||  // diagnostics: register gather in fast mode
-                            (zeta >= 16 && d <= 2048) || (zeta <= 2 && d >= 2048);
+                            ctx->force_row_gather || (zeta >= 16 && d <= 2048) || (zeta <= 2 && d >= 2048);
     if (!exact && !row_gather && sketch_apply_dmma(ctx, A, d, compact, colptr_dev, zeta, val, Y)) return;
     DenseGather G = dense_gather_plan(ctx, m, A->n, A->ld, d, compact, colptr_dev, zeta, val, exact, Y, false);
     dense_gather_rows(ctx, G, A->A, 0, m);

@@ -598,7 +598,6 @@ void sketch_apply_sparse_compact_dev(slq_ctx* ctx, const slq_sparse* A, int64_t 
     SGatherArgs g{A->rowptr, A->colidx, A->vals, A->b, n, d, srow_ptr, sent, val, Y, warps};
     sparse_gather_kernel<<<static_cast<unsigned>(ceil_div(d, warps)), 32 * warps, smem, ctx->stream>>>(g);
     SLQ_LAUNCH_CHECK(ctx);
-    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
 }
 
 namespace {
