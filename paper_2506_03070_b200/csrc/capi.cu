@@ -699,10 +699,10 @@ int slq_dense_set_rhs(slq_dense* A, const double* b) {
 int slq_dense_free(slq_dense* A) {
     return guarded([&] {
         if (!A) return;
-        if (A->owned && A->A) {
-            cudaStreamSynchronize(A->ctx->stream);
-            cudaFree(A->A);
-        }
+        // no access to A->ctx: the matrix may outlive its context (e.g. a
+        // garbage collector finalizing both in any order); cudaFree itself
+        // waits for the device work that still reads the buffer
+        if (A->owned && A->A) cudaFree(A->A);
         delete A;
     });
 }
@@ -1074,8 +1074,7 @@ int slq_sparse_set_rhs(slq_sparse* A, const double* b) {
 int slq_sparse_free(slq_sparse* A) {
     return guarded([&] {
         if (!A) return;
-        cudaStreamSynchronize(A->ctx->stream);
-        slq::sparse_free(A);
+        slq::sparse_free(A);  // cudaFree waits for pending device work; A->ctx may be gone
         delete A;
     });
 }

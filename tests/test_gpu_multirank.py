@@ -26,7 +26,7 @@ class ThreadGroup:
 
     def __init__(self, p):
         self.p = p
-        self.bar = threading.Barrier(p, timeout=300)
+        self.bar = threading.Barrier(p, timeout=120)  # a mismatched collective sequence fails, not hangs
         self.slots = [None] * p
         self.calls = [0] * p
 
@@ -73,8 +73,10 @@ def _run_ranks(p, body):
             ctx.set_host_comm(group.comm(r), r, p)
             out[r] = body(r, ctx)
         except BaseException as e:  # noqa: BLE001 -- reported below
+            # no barrier abort here: a rank that finished (even with an error)
+            # has passed all its collectives; aborting could break a peer that
+            # was released from the last barrier but not yet woken
             errs[r] = e
-            group.bar.abort()
 
     ts = [threading.Thread(target=worker, args=(r,)) for r in range(p)]
     for t in ts:
@@ -118,15 +120,18 @@ def test_multirank_solve_matches_single_rank(p):
         assert ph["nccl_calls"] > 0
     # collectives per rank: reduce + status/M/M^T/x0 broadcasts + init allreduce + T + no-op tail of the last batch
     assert len(set(group.calls)) == 1 and group.calls[0] >= 1 + 4 + 1 + T
+    # against one rank: the sketch partials are summed in another order, which
+    # moves x by ~1e-8 at cond 1e4 -- compared in residual / backward-error space
     x1, rep1, _ = slq.solve(A, d, zeta, 11, opts, b=b)
-    assert np.linalg.norm(xs[0] - x1) <= 1e-9 * np.linalg.norm(x1)  # sketch partials summed in another order
+    assert np.linalg.norm(A @ (xs[0] - x1)) <= 1e-10 * np.linalg.norm(b)
     assert _eta(A, b, xs[0]) <= max(2 * _eta(A, b, x1), 1e-14)
     # the reference's distributed sketch (distsim.hpp:383-396) + serial pipeline, same seed
     Yr, Sbr = oracle.REF().dist_sketch_apply(d, zeta, 11, A, b, p) if oracle.ref_available() else C.sketch_apply(
         d, zeta, 11, A, b)
     M, Q = C.build_preconditioner(Yr)
     xo, _ = C.lsqr(A, M, b, C.initial_guess(M, Q, Sbr), eps=0.0, maxit=T, one_sync=True)
-    assert np.linalg.norm(xs[0] - xo) <= 1e-9 * np.linalg.norm(xo)
+    assert np.linalg.norm(A @ (xs[0] - xo)) <= 1e-10 * np.linalg.norm(b)
+    assert _eta(A, b, xs[0]) <= max(2 * _eta(A, b, xo), 1e-14)
 
 
 def test_multirank_gradient_descent():
