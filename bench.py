@@ -434,6 +434,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        # NCCL's init lines (communicator size, rank, transport) document the N-rank run
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.config == "c4" and args.impl == "ours":
         return run_sparse(args, world, rank, local_rank)
     n, d, zeta = args.n, args.dfac * args.n, args.zeta

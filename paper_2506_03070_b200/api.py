@@ -485,15 +485,17 @@ def tri_upper_rmatvec(R, x, ctx=None) -> np.ndarray:
     return y
 
 
-def build_preconditioner(Y, ctx=None, Sb=None):
+def build_preconditioner(Y, ctx=None, Sb=None, want_q=True):
     """preconditioner.hpp:35-44.  With ``Sb`` also returns x0 = M Q^T Sb
-    (preconditioner.hpp:48-53) computed from the same factorization."""
+    (preconditioner.hpp:48-53) computed from the same factorization.
+    want_q=False never forms Q (P.Q is None) -- the solve path's form, and the
+    only one for d > 12400 (TSQR)."""
     Y = _f64(Y)
     d, n = Y.shape
     if d < n:
         raise DimensionMismatch("householder_qr: need rows >= cols")
     M = np.zeros((n, n), order="F")
-    Q = np.zeros((d, n), order="F")
+    Q = np.zeros((d, n), order="F") if want_q else None
     bt = np.zeros(1)
     x0 = np.zeros(n) if Sb is not None else None
     _check(C.lib.slq_build_preconditioner(_ctx(ctx).handle, _d(Y), d, n, max(d, 1),

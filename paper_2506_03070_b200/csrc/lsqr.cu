@@ -250,6 +250,135 @@ __global__ void lsqr_abort_kernel(const double* status, LsqrState* st) {
     }
 }
 
+// ------------------------------------------------- K4 wide rows (n > 2046)
+//
+// Rows wider than one warp can hold in registers: the 7 consumer warps split
+// the COLUMNS of every row (lane L of the 224 consumer threads owns the
+// double2 units 2L + 448q, q < NQ, of each row and the matching z and p
+// entries), so all warps work on every row of a tile:
+//   1. per row of the tile, each warp's partial A_i p over its columns
+//      (shared-memory reads, warp shuffle sum) -> red[parity][row][warp];
+//   2. one named barrier among the 224 consumer threads;
+//   3. u_hat_i = (sum of the 7 partials, fixed order) + c u_i, computed by
+//      every thread, then z_seg += A_i,seg u_hat_i re-reading the row from
+//      shared memory (plenty of bandwidth: one A read from HBM per pass stays
+//      the bound), ||u_hat||^2 by thread 0.
+// The red buffer alternates between two halves by tile parity, so the next
+// tile's writes never race with slow readers of this one.  z needs no
+// cross-warp reduction: each column belongs to exactly one thread.
+template <int NQ>
+__global__ void __launch_bounds__(kPassThreads, 1) fused_pass_wide_kernel(PassArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (a.skip && *a.skip) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t ld = a.ld;
+    const size_t stage_elems = static_cast<size_t>(a.R) * ld;
+    double* stages = reinterpret_cast<double*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.S * stage_elems * sizeof(double));
+    uint64_t* empty = full + a.S;
+    double* red = reinterpret_cast<double*>(empty + a.S);  // [2][R][8]
+
+    const int64_t ntiles = (a.m + a.R - 1) / a.R;
+    const int64_t t0 = blockIdx.x * ntiles / gridDim.x;
+    const int64_t t1 = (blockIdx.x + 1) * ntiles / gridDim.x;
+    const int64_t nt = t1 - t0;
+    if (tid == 0) {
+        for (int s = 0; s < a.S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kConsumerWarps) {
+        if (lane == 0) {
+            const uint64_t pol = a.keep_l2 ? evict_last_policy() : evict_first_policy();
+            for (int64_t k = 0; k < nt; ++k) {
+                const int s = static_cast<int>(k % a.S);
+                const int64_t r = k / a.S;
+                if (r > 0) mbar_wait(&empty[s], static_cast<unsigned>((r - 1) & 1));
+                const int64_t row0 = (t0 + k) * a.R;
+                const int64_t rows = min(static_cast<int64_t>(a.R), a.m - row0);
+                const unsigned bytes = static_cast<unsigned>(rows * ld * sizeof(double));
+                mbar_expect_tx(&full[s], bytes);
+                bulk_g2s(stages + s * stage_elems, a.A + row0 * ld, bytes, &full[s], pol);
+            }
+        }
+        __syncwarp();
+        return;
+    }
+    const int L = tid;  // 0 .. 223
+    double pr[2 * NQ], z[2 * NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int64_t j = 2 * L + 448 * q;
+        pr[2 * q] = (j < a.n) ? a.p[j] : 0.0;
+        pr[2 * q + 1] = (j + 1 < a.n) ? a.p[j + 1] : 0.0;
+        z[2 * q] = z[2 * q + 1] = 0.0;
+    }
+    const double c = a.coef ? *a.coef : a.c_fixed;
+    double ssq = 0.0;
+    for (int64_t k = 0; k < nt; ++k) {
+        const int s = static_cast<int>(k % a.S);
+        mbar_wait(&full[s], static_cast<unsigned>((k / a.S) & 1));
+        const double* tile = stages + s * stage_elems;
+        const int64_t row0 = (t0 + k) * a.R;
+        const int rows = static_cast<int>(min(static_cast<int64_t>(a.R), a.m - row0));
+        double* rb = red + (k & 1) * a.R * 8;
+        for (int i = 0; i < rows; ++i) {
+            const double* row = tile + static_cast<int64_t>(i) * ld;
+            double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int64_t j = 2 * L + 448 * q;
+                if (j < ld) {
+                    const double2 v = *reinterpret_cast<const double2*>(row + j);
+                    acc0 = fma(v.x, pr[2 * q], acc0);
+                    acc1 = fma(v.y, pr[2 * q + 1], acc1);
+                }
+            }
+            const double y = warp_sum(acc0 + acc1);
+            if (lane == 0) rb[i * 8 + warp] = y;
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(kConsumerWarps * 32) : "memory");
+        for (int i = 0; i < rows; ++i) {
+            double y = rb[i * 8];
+#pragma unroll
+            for (int w = 1; w < kConsumerWarps; ++w) y += rb[i * 8 + w];
+            const double u = a.u_in ? a.u_in[row0 + i] : tile[static_cast<int64_t>(i) * ld + a.n];
+            const double uh = __dadd_rn(y, __dmul_rn(c, u));
+            if (L == 0) {
+                if (a.u_out) a.u_out[row0 + i] = uh;
+                ssq = fma(uh, uh, ssq);
+            }
+            if (a.want_z) {
+                const double* row = tile + static_cast<int64_t>(i) * ld;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const int64_t j = 2 * L + 448 * q;
+                    if (j < ld) {
+                        const double2 v = *reinterpret_cast<const double2*>(row + j);
+                        z[2 * q] = fma(v.x, uh, z[2 * q]);
+                        z[2 * q + 1] = fma(v.y, uh, z[2 * q + 1]);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    double* outp = a.part + static_cast<int64_t>(blockIdx.x) * (a.n + 1);
+    if (a.want_z) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int64_t j = 2 * L + 448 * q;
+            if (j < a.n) outp[j] = z[2 * q];
+            if (j + 1 < a.n) outp[j + 1] = z[2 * q + 1];
+        }
+    }
+    if (L == 0) outp[a.n] = ssq;
+}
+
 // partials [G][n+1] -> out[n+1], fixed order: thread (c, g) sums partials
 // g, g+8, ... of column c, then the 8 sums are added in order g = 0..7.
 __global__ void __launch_bounds__(256) reduce_partials_kernel(const double* part, int G, int64_t n1, double* out,
@@ -663,12 +792,30 @@ struct PassPlan {
     int R, S;
     size_t smem;
     int grid;
+    int NQ;  // > 0: wide-row kernel (columns split across the consumer warps)
 };
 
 PassPlan plan_pass(slq_ctx* ctx, const slq_dense* A) {
     PassPlan pp{};
     const int64_t ld = A->ld;
-    if (ld > 2048) fail(SLQ_UNSUPPORTED, "lsqr: n > 2046 not supported by the fused pass");
+    if (ld > 2048) {
+        // wide rows: NQ double2 units per consumer thread, 448 columns per unit index
+        const int64_t nq = ceil_div(ld, 448);
+        pp.NQ = nq <= 6 ? 6 : nq <= 9 ? 9 : nq <= 12 ? 12 : nq <= 18 ? 18 : 0;
+        if (pp.NQ == 0) fail(SLQ_UNSUPPORTED, "lsqr: n > 8062 not supported by the fused pass");
+        const int64_t row_bytes = ld * static_cast<int64_t>(sizeof(double));
+        pp.R = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, (64 * 1024) / row_bytes)));
+        pp.S = 3;
+        auto size = [&](int S) {
+            return static_cast<size_t>(S) * pp.R * row_bytes + 2 * S * sizeof(uint64_t) + 2 * pp.R * 8 * sizeof(double) + 64;
+        };
+        while (size(pp.S) > 227 * 1024 && pp.S > 2) --pp.S;
+        if (size(pp.S) > 227 * 1024) fail(SLQ_UNSUPPORTED, "lsqr: row too wide for the pass stages");
+        pp.smem = size(pp.S);
+        const int64_t ntiles = ceil_div(std::max<int64_t>(A->m, 1), pp.R);
+        pp.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, ntiles)));
+        return pp;
+    }
     pp.NP = 1;
     while (64 * pp.NP < ld) pp.NP <<= 1;
     pp.p_smem = pp.NP >= 32;
@@ -698,9 +845,26 @@ void launch_pass_t(slq_ctx* ctx, const PassPlan& pp, const PassArgs& a) {
     SLQ_LAUNCH_CHECK(ctx);
 }
 
+template <int NQ>
+void launch_pass_wide_t(slq_ctx* ctx, const PassPlan& pp, const PassArgs& a) {
+    auto k = fused_pass_wide_kernel<NQ>;
+    SLQ_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pp.smem)));
+    k<<<pp.grid, kPassThreads, pp.smem, ctx->stream>>>(a);
+    SLQ_LAUNCH_CHECK(ctx);
+}
+
 void launch_pass(slq_ctx* ctx, const PassPlan& pp, PassArgs a) {
     a.R = pp.R;
     a.S = pp.S;
+    if (pp.NQ) {
+        switch (pp.NQ) {
+            case 6: launch_pass_wide_t<6>(ctx, pp, a); break;
+            case 9: launch_pass_wide_t<9>(ctx, pp, a); break;
+            case 12: launch_pass_wide_t<12>(ctx, pp, a); break;
+            default: launch_pass_wide_t<18>(ctx, pp, a); break;
+        }
+        return;
+    }
     switch (pp.NP) {
         case 1: launch_pass_t<1, false>(ctx, pp, a); break;
         case 2: launch_pass_t<2, false>(ctx, pp, a); break;

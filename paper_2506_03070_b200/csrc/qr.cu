@@ -1215,8 +1215,20 @@ void qr_streams(slq_ctx* ctx, cudaStream_t& hi, cudaStream_t& lo, cudaEvent_t& e
 
 }  // namespace
 
-void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t ncols, int64_t ldy,
-                   double* R, double* qtb, double* Q, double* sign_out) {
+namespace {
+
+__global__ void rank_tol_copy_kernel(const double* src, double* dst) {
+    if (threadIdx.x == 0) *dst = src ? *src : 0.0;
+}
+
+}  // namespace
+
+// The blocked Householder QR of one panel-able matrix (d <= kMaxPanelRows).
+// tol (device, may be null): rank tolerance to use instead of 1e-12 max|Y| --
+// TSQR leaves pass 0 (only an exactly zero column fails there) and the top of
+// the tree the tolerance of the ORIGINAL Y.
+void qr_factor_core(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t ncols, int64_t ldy, double* R,
+                    double* qtb, double* Q, double* sign_out, const double* tol, bool tol_given) {
     if (d < n) fail(SLQ_DIMENSION_MISMATCH, "householder_qr: need rows >= cols");
     Workspace& ws = ctx->ws;
     const int64_t npanels = ceil_div(n, kNbMax);
@@ -1232,10 +1244,15 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
 
     const int nmax = 1024;
     const int nb_blocks = static_cast<int>(std::min<int64_t>(nmax, ceil_div(d * n, 256)));
-    maxabs_kernel<<<nb_blocks, 256, 0, ctx->stream>>>(Yaug, d, n, ldy, part);
-    SLQ_LAUNCH_CHECK(ctx);
-    maxabs_final_kernel<<<1, 32, 0, ctx->stream>>>(part, nb_blocks, rank_tol);
-    SLQ_LAUNCH_CHECK(ctx);
+    if (tol_given) {
+        rank_tol_copy_kernel<<<1, 32, 0, ctx->stream>>>(tol, rank_tol);
+        SLQ_LAUNCH_CHECK(ctx);
+    } else {
+        maxabs_kernel<<<nb_blocks, 256, 0, ctx->stream>>>(Yaug, d, n, ldy, part);
+        SLQ_LAUNCH_CHECK(ctx);
+        maxabs_final_kernel<<<1, 32, 0, ctx->stream>>>(part, nb_blocks, rank_tol);
+        SLQ_LAUNCH_CHECK(ctx);
+    }
 
     // Look-ahead schedule (depth 1) on two streams: s_hi runs the panels and the
     // narrow update N(p) of the next panel's 32 columns (one cluster launch,
@@ -1350,6 +1367,74 @@ void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nco
         scale_cols_kernel<<<static_cast<unsigned>(ceil_div(d * n, 256)), 256, 0, ctx->stream>>>(Q, d, n, sign);
         SLQ_LAUNCH_CHECK(ctx);
     }
+}
+
+// Sketches taller than one panel cluster can hold (d > kMaxPanelRows): TSQR.
+// Row blocks of <= kLeafRows rows are factored independently (same blocked
+// Householder, rank test off), their R factors -- with Q_k^T (S b)_k in the
+// extra column -- are stacked and factored again (recursively while the stack
+// is still too tall).  R is unique up to row signs, fixed by diag(R) >= 0 at
+// the top, and Q^T Sb composes through the tree, so the preconditioner and
+// x0 are those of the one-level factorization; the rank test runs at the top
+// against 1e-12 max|Y| of the original Y (|R_kk| is the norm it tests).
+constexpr int64_t kMaxPanelRows = 12400;
+constexpr int64_t kLeafRows = 8192;
+
+namespace {
+
+// one TSQR level (and the levels above it); tol = rank tolerance of the original Y
+void qr_tsqr(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t ncols, int64_t ldy, double* R, double* qtb,
+             double* sign_out, const double* tol) {
+    const int64_t leaf = std::min<int64_t>(kLeafRows, d);
+    const int64_t nblk = ceil_div(d, leaf);
+    if (ceil_div(d, nblk) < 2 * n)
+        fail(SLQ_UNSUPPORTED, "householder_qr: d > 12400 needs n <= 4096 (TSQR leaves of >= 2n rows)");
+    DevBuf zero, leafbuf, stackbuf, rk;
+    double* z0 = static_cast<double*>(zero.ensure(sizeof(double)));
+    SLQ_CUDA_CHECK(cudaMemsetAsync(z0, 0, sizeof(double), ctx->stream));
+    const int64_t srows = nblk * n;
+    double* S = static_cast<double*>(stackbuf.ensure(sizeof(double) * srows * ncols));
+    SLQ_CUDA_CHECK(cudaMemsetAsync(S, 0, sizeof(double) * srows * ncols, ctx->stream));
+    double* Rk = static_cast<double*>(rk.ensure(sizeof(double) * (n * n + n)));
+    const int64_t dk_max = ceil_div(d, nblk);
+    double* Yk = static_cast<double*>(leafbuf.ensure(sizeof(double) * dk_max * ncols));
+    for (int64_t k = 0; k < nblk; ++k) {
+        const int64_t r0 = k * d / nblk, r1 = (k + 1) * d / nblk, dk = r1 - r0;
+        SLQ_CUDA_CHECK(cudaMemcpy2DAsync(Yk, sizeof(double) * dk, Yaug + r0, sizeof(double) * ldy, sizeof(double) * dk,
+                                         ncols, cudaMemcpyDeviceToDevice, ctx->stream));
+        qr_factor_core(ctx, Yk, dk, n, ncols, dk, Rk, ncols > n ? Rk + n * n : nullptr, nullptr, nullptr, z0, true);
+        // rows [k n, (k+1) n) of the stack: [R_k | Q_k^T (S b)_k]
+        SLQ_CUDA_CHECK(cudaMemcpy2DAsync(S + k * n, sizeof(double) * srows, Rk, sizeof(double) * n, sizeof(double) * n, n,
+                                         cudaMemcpyDeviceToDevice, ctx->stream));
+        if (ncols > n)
+            SLQ_CUDA_CHECK(cudaMemcpyAsync(S + n * srows + k * n, Rk + n * n, sizeof(double) * n,
+                                           cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    if (srows <= kMaxPanelRows) qr_factor_core(ctx, S, srows, n, ncols, srows, R, qtb, nullptr, sign_out, tol, true);
+    else qr_tsqr(ctx, S, srows, n, ncols, srows, R, qtb, sign_out, tol);
+    SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // the leaf / stack buffers are freed on return
+}
+
+}  // namespace
+
+void qr_factor_dev(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t ncols, int64_t ldy, double* R,
+                   double* qtb, double* Q, double* sign_out) {
+    if (d <= kMaxPanelRows) {
+        qr_factor_core(ctx, Yaug, d, n, ncols, ldy, R, qtb, Q, sign_out, nullptr, false);
+        return;
+    }
+    if (d < n) fail(SLQ_DIMENSION_MISMATCH, "householder_qr: need rows >= cols");
+    if (Q) fail(SLQ_UNSUPPORTED, "householder_qr: forming Q for d > 12400 (tall sketch, TSQR) is not supported");
+    if (ncols > n + 1) fail(SLQ_UNSUPPORTED, "householder_qr: at most one appended column for d > 12400");
+    // rank tolerance of the original Y (qr.hpp:26)
+    DevBuf tolbuf;
+    double* tol = static_cast<double*>(tolbuf.ensure(sizeof(double) * (1024 + 8)));
+    const int nb_blocks = static_cast<int>(std::min<int64_t>(1024, ceil_div(d * n, 256)));
+    maxabs_kernel<<<nb_blocks, 256, 0, ctx->stream>>>(Yaug, d, n, ldy, tol + 8);
+    SLQ_LAUNCH_CHECK(ctx);
+    maxabs_final_kernel<<<1, 32, 0, ctx->stream>>>(tol + 8, nb_blocks, tol);
+    SLQ_LAUNCH_CHECK(ctx);
+    qr_tsqr(ctx, Yaug, d, n, ncols, ldy, R, qtb, sign_out, tol);
 }
 
 void defer_status_dev(slq_ctx* ctx, const int* flag, int cond, int code) {
