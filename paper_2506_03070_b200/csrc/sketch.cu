@@ -862,239 +862,6 @@ __global__ void __launch_bounds__(1024, 1) gather_dmma_kernel(const __grid_const
     }
 }
 
-// ------------------------------------------------- K2w lane-column gather
-//
-// Fast-mode S.[A b] on the FP64 CUDA cores, one sketch entry per WARP
-// instruction: lane l owns column col0 + l of a 32-column slab, a warp owns RW
-// consecutive Y rows (its accumulators acc[0..RW)), a CTA of 8 warps owns a row
-// block.  Per chunk of 256 A rows the slab segment (256 rows x 256 B) arrives
-// by TMA; the chunk's entries for this row block are sorted by (row, k) per
-// warp (warp_bucket_kernel), so a warp walks its rows j = 0..RW-1 in a fully
-// unrolled loop -- the accumulator index is static -- and for each entry of row
-// j loads A[k][col0 + l] (the 32 lanes read one contiguous 256-byte row
-// segment: no bank conflicts) and adds it with the entry's sign.  Against K2d:
-// no 7/8-zero S fragments, no padded groups, no conflicted 16-byte gathers.
-constexpr int kKwRows = 384;   // A rows per chunk (3 TMA boxes of 128 rows; entry byte offsets k * 256 < 2^17)
-constexpr int kKwBox = 128;
-constexpr int kKwHdr = 32;     // u32 header per (chunk, row block): warp segment starts
-constexpr int kKwMaxStages = 3;
-constexpr uint32_t kKwSentinel = 0x7f000000u;
-
-struct WarpBucketArgs {
-    const uint32_t* compact;  // generator entries (row | neg << 31), column order, uniform zeta
-    int64_t zeta, ncols, d;
-    int rblk, rw, nw, nrb, cap;  // rows per row block, rows per warp, warps per row block, row blocks,
-                                // u32 per (chunk, rb) block
-    uint32_t* out;            // [nchunks][nrb][cap]
-    int* flag;
-};
-
-// One CTA per chunk: bitonic sort of the chunk's K * zeta keys (r, k, sign) in
-// shared memory (deterministic: keys are unique), warp-segment bounds by binary
-// search, then each entry is written to its (row block, warp) segment as
-// neg << 31 | row_in_warp << 24 | k * 256, each segment closed by a sentinel
-// whose row field (127) matches no row and whose offset (0) is a valid address.
-__global__ void __launch_bounds__(1024) warp_bucket_kernel(WarpBucketArgs a) {
-    extern __shared__ uint32_t wkeys[];
-    const int tid = threadIdx.x, T = blockDim.x;
-    const int64_t c = blockIdx.x;
-    const int64_t k0 = c * kKwRows;
-    const int kc = static_cast<int>(min(static_cast<int64_t>(kKwRows), a.ncols - k0));
-    const int N = kc * static_cast<int>(a.zeta);
-    int NP = 2;
-    while (NP < N) NP <<= 1;
-    const uint32_t* src = a.compact + k0 * a.zeta;
-    int* bnd = reinterpret_cast<int*>(wkeys + NP);  // [nrb * nw + 1]
-    for (int i = tid; i < NP; i += T) {
-        if (i < N) {
-            const uint32_t ent = src[i];
-            const uint32_t kl = static_cast<uint32_t>(i / a.zeta);
-            wkeys[i] = ((ent & 0x7fffffffu) << 10) | (kl << 1) | (ent >> 31);
-        } else {
-            wkeys[i] = kPad;
-        }
-    }
-    __syncthreads();
-    for (int k = 2; k <= NP; k <<= 1) {
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
-            for (int i = tid; i < (NP >> 1); i += T) {
-                const int lo = ((i & ~(jj - 1)) << 1) | (i & (jj - 1));
-                const int hi = lo + jj;
-                const bool asc = (lo & k) == 0;
-                const uint32_t x = wkeys[lo], y = wkeys[hi];
-                if ((x > y) == asc) {
-                    wkeys[lo] = y;
-                    wkeys[hi] = x;
-                }
-            }
-            __syncthreads();
-        }
-    }
-    // bnd[g] = #entries with row < first row of global warp segment g
-    const int nseg = a.nrb * a.nw;
-    auto seg_row = [&](int g) -> int64_t {
-        const int rb = g / a.nw, w = g % a.nw;
-        return min(min(static_cast<int64_t>(rb) * a.rblk + static_cast<int64_t>(w) * a.rw,
-                       static_cast<int64_t>(rb + 1) * a.rblk),
-                   a.d);
-    };
-    for (int g = tid; g <= nseg; g += T) {
-        const uint32_t key = g == nseg ? 0xffffffffu : static_cast<uint32_t>(seg_row(g)) << 10;
-        int lo = 0, hi = N;  // first i with keys[i] >= key
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (wkeys[mid] < key) lo = mid + 1;
-            else hi = mid;
-        }
-        bnd[g] = g == nseg ? N : lo;
-    }
-    __syncthreads();
-    bool over = false;
-    for (int rb = 0; rb < a.nrb; ++rb)
-        over |= kKwHdr + (bnd[(rb + 1) * a.nw] - bnd[rb * a.nw]) + a.nw + 2 > a.cap;  // + 2: the gather reads two entries ahead
-    uint32_t* out = a.out + c * a.nrb * static_cast<int64_t>(a.cap);
-    if (over) {  // flag it (the caller redoes the sketch elsewhere); leave empty, well-formed segments
-        if (tid == 0) atomicExch(a.flag, 1);
-        for (int g = tid; g < nseg; g += T) {
-            uint32_t* blk = out + static_cast<int64_t>(g / a.nw) * a.cap;
-            blk[g % a.nw] = static_cast<uint32_t>(kKwHdr + g % a.nw);
-            blk[kKwHdr + g % a.nw] = kKwSentinel;
-        }
-        return;
-    }
-    // headers + sentinels
-    for (int g = tid; g < nseg; g += T) {
-        const int rb = g / a.nw, w = g % a.nw;
-        const int start = kKwHdr + (bnd[g] - bnd[rb * a.nw]) + w;
-        uint32_t* blk = out + static_cast<int64_t>(rb) * a.cap;
-        blk[w] = static_cast<uint32_t>(start);
-        blk[start + bnd[g + 1] - bnd[g]] = kKwSentinel;
-    }
-    for (int i = tid; i < N; i += T) {
-        const uint32_t key = wkeys[i];
-        const int64_t r = key >> 10;
-        const int rb = static_cast<int>(r / a.rblk);
-        const int w = static_cast<int>((r - static_cast<int64_t>(rb) * a.rblk) / a.rw);
-        const int g = rb * a.nw + w;
-        const int pos = kKwHdr + (i - bnd[rb * a.nw]) + w;
-        const uint32_t jl = static_cast<uint32_t>(r - seg_row(g));
-        const uint32_t kl = (key >> 1) & 0x1ffu;
-        out[static_cast<int64_t>(rb) * a.cap + pos] = ((key & 1u) << 31) | (jl << 24) | (kl << 8);
-    }
-}
-
-__device__ __forceinline__ uint32_t lds_u32(unsigned a) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ double lds_f64(unsigned a) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a) : "memory");
-    return v;
-}
-
-struct KwArgs {
-    int64_t m, d, ldw;
-    int64_t nsplit, c_lo, c_hi;
-    const uint32_t* ent;  // [nchunks][nrb][cap]
-    int cap, nrb, rblk, rw, ns;
-    double val;
-    double* Yw;  // [nsplit][ldw][d]
-};
-
-template <int NW, int RW, bool EXACT>
-__global__ void __launch_bounds__(NW * 32, 1) gather_warp_kernel(const __grid_constant__ CUtensorMap tmap, KwArgs g) {
-    extern __shared__ __align__(128) unsigned char kwsm[];
-    __shared__ __align__(8) uint64_t full[kKwMaxStages];
-    __shared__ int done[kKwMaxStages];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int rb = blockIdx.x;
-    const int64_t col0 = static_cast<int64_t>(blockIdx.y) * 32;
-    const int64_t split = blockIdx.z;
-    const int64_t cb = g.c_lo + split * (g.c_hi - g.c_lo) / g.nsplit;
-    const int64_t ce = g.c_lo + (split + 1) * (g.c_hi - g.c_lo) / g.nsplit;
-    constexpr unsigned a_bytes = kKwRows * 256u;
-    const unsigned e_bytes = static_cast<unsigned>(g.cap) * 4u;
-    const unsigned st_bytes = a_bytes + ((e_bytes + 127u) & ~127u);
-    const unsigned sm0 = ptx::smem_u32(kwsm);
-    if (tid == 0) {
-        for (int s = 0; s < g.ns; ++s) {
-            ptx::mbar_init(&full[s], 1);
-            done[s] = 0;
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    auto issue = [&](int64_t c, int s) {  // one thread
-        const int64_t k0 = c * kKwRows;
-        // boxes that start past the last row are not issued (their rows are never referenced)
-        const int nbox = static_cast<int>(min(static_cast<int64_t>(kKwRows / kKwBox), (g.m - k0 + kKwBox - 1) / kKwBox));
-        ptx::mbar_expect_tx(&full[s], static_cast<unsigned>(nbox) * kKwBox * 256u + e_bytes);
-        for (int bx = 0; bx < nbox; ++bx)
-            asm volatile(
-                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-                    sm0 + s * st_bytes + bx * kKwBox * 256u),
-                "l"(&tmap), "r"(static_cast<int>(col0)), "r"(static_cast<int>(k0 + bx * kKwBox)), "r"(ptx::smem_u32(&full[s]))
-                : "memory");
-        ptx::bulk_g2s(kwsm + s * st_bytes + a_bytes, g.ent + (c * g.nrb + rb) * static_cast<int64_t>(g.cap), e_bytes,
-                      &full[s]);
-    };
-    double acc[RW];
-#pragma unroll
-    for (int j = 0; j < RW; ++j) acc[j] = 0.0;
-    if (tid == 0)
-        for (int s = 0; s < g.ns && cb + s < ce; ++s) issue(cb + s, s);
-    const unsigned vhi = static_cast<unsigned>(__double2hiint(g.val)), vlo = static_cast<unsigned>(__double2loint(g.val));
-    const unsigned lane8 = static_cast<unsigned>(lane) * 8u;
-    int s = 0;
-    unsigned phase = 0;
-    for (int64_t c = cb; c < ce; ++c) {
-        ptx::mbar_wait(&full[s], phase);
-        const unsigned ab = sm0 + s * st_bytes + lane8;  // this lane's column of A row 0
-        const unsigned eb = sm0 + s * st_bytes + a_bytes;
-        // entries are warp-uniform: broadcast through a shuffle so the row
-        // loops compile to uniform branches (no reconvergence bookkeeping)
-        unsigned ea = eb + 4u * lds_u32(eb + 4u * warp);
-        uint32_t e = __shfl_sync(0xffffffffu, lds_u32(ea), 0);
-#pragma unroll
-        for (int j = 0; j < RW; ++j) {
-            // row test in one LOP3: the entry's row field equals j
-            while (((e ^ (static_cast<uint32_t>(j) << 24)) & 0x7f000000u) == 0u) {
-                const double av = lds_f64(ab + (e & 0x1ff00u));
-                const uint32_t en = lds_u32(ea + 4u);
-                ea += 4u;
-                const unsigned sg = e & 0x80000000u;
-                if (EXACT) {
-                    // the reference's y += v * a (csc_matrix.hpp:116), two roundings
-                    const double v = __hiloint2double(static_cast<int>(vhi ^ sg), static_cast<int>(vlo));
-                    acc[j] = __dadd_rn(acc[j], __dmul_rn(v, av));
-                } else {
-                    acc[j] += __hiloint2double(__double2hiint(av) ^ static_cast<int>(sg), __double2loint(av));
-                }
-                e = __shfl_sync(0xffffffffu, en, 0);
-            }
-        }
-        __syncwarp();
-        if (lane == 0 && atomicAdd(&done[s], 1) == NW - 1) {
-            done[s] = 0;
-            if (c + g.ns < ce) issue(c + g.ns, s);
-        }
-        if (++s == g.ns) {
-            s = 0;
-            phase ^= 1u;
-        }
-    }
-    double* Y = g.Yw + split * g.ldw * g.d;
-    const int64_t r0 = static_cast<int64_t>(rb) * g.rblk + static_cast<int64_t>(warp) * g.rw;
-    const int64_t r1 = min(min(r0 + g.rw, static_cast<int64_t>(rb + 1) * g.rblk), g.d);
-    const int64_t col = col0 + lane;
-    if (col < g.ldw)
-#pragma unroll
-        for (int j = 0; j < RW; ++j)
-            if (r0 + j < r1) Y[col * g.d + r0 + j] = EXACT ? acc[j] : acc[j] * g.val;
-}
-
 uint64_t lemire_thresh(uint64_t d) { return (0 - d) % d; }
 
 }  // namespace
@@ -1356,111 +1123,6 @@ bool sketch_apply_dmma(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32
     return true;
 }
 
-template <int NW, int RW, bool EXACT>
-void launch_kw(slq_ctx* ctx, const CUtensorMap& map, const KwArgs& g, dim3 grid, size_t smem) {
-    auto kern = gather_warp_kernel<NW, RW, EXACT>;
-    SLQ_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, NW * 32, smem, ctx->stream>>>(map, g);
-    SLQ_LAUNCH_CHECK(ctx);
-}
-
-template <bool EXACT>
-void launch_kw_rw(slq_ctx* ctx, int nw, int rw, const CUtensorMap& map, const KwArgs& g, dim3 grid, size_t smem) {
-    if (nw == 24) {
-        if (rw <= 8) launch_kw<24, 8, EXACT>(ctx, map, g, grid, smem);
-        else if (rw <= 16) launch_kw<24, 16, EXACT>(ctx, map, g, grid, smem);
-        else launch_kw<24, 32, EXACT>(ctx, map, g, grid, smem);
-    } else if (nw == 16) {
-        if (rw <= 8) launch_kw<16, 8, EXACT>(ctx, map, g, grid, smem);
-        else if (rw <= 16) launch_kw<16, 16, EXACT>(ctx, map, g, grid, smem);
-        else if (rw <= 32) launch_kw<16, 32, EXACT>(ctx, map, g, grid, smem);
-        else launch_kw<16, 48, EXACT>(ctx, map, g, grid, smem);
-    } else {
-        if (rw <= 16) launch_kw<8, 16, EXACT>(ctx, map, g, grid, smem);
-        else if (rw <= 32) launch_kw<8, 32, EXACT>(ctx, map, g, grid, smem);
-        else if (rw <= 64) launch_kw<8, 64, EXACT>(ctx, map, g, grid, smem);
-        else launch_kw<8, 96, EXACT>(ctx, map, g, grid, smem);
-    }
-}
-
-// K2w (warp-uniform lane-column gather).  Uniform zeta <= 64, d < 2^23.
-// Returns false if a (chunk, row block) overflowed its entry capacity (the
-// caller falls back to another gather).
-bool sketch_apply_warp(slq_ctx* ctx, const slq_dense* A, int64_t d, const uint32_t* compact, int64_t zeta,
-                       double val, bool exact, double* Y) {
-    const int64_t m = A->m, ld = A->ld, ncols_out = A->n + 1;
-    int nw = 16, rwmax = 48;
-    if (const char* e = std::getenv("SLQ_KW_NW")) {
-        if (std::atoi(e) == 8) nw = 8, rwmax = 96;
-        if (std::atoi(e) == 24) nw = 24, rwmax = 32;
-    }
-    const int nrb = static_cast<int>(ceil_div(d, static_cast<int64_t>(nw) * rwmax));
-    const int rblk = static_cast<int>(ceil_div(d, static_cast<int64_t>(nrb)));
-    const int rw = static_cast<int>(ceil_div(static_cast<int64_t>(rblk), static_cast<int64_t>(nw)));
-    const int64_t nchunks = ceil_div(m, static_cast<int64_t>(kKwRows));
-    const double expect = static_cast<double>(kKwRows) * zeta * rblk / static_cast<double>(d);
-    int cap = static_cast<int>(round_up(static_cast<int64_t>(kKwHdr + nw + 2 + expect + 8.0 * std::sqrt(expect) + 32), 32));
-    if (const char* e = std::getenv("SLQ_KW_CAP")) cap = std::max(kKwHdr + nw + 2, std::atoi(e));  // tests: force overflow
-    Workspace& ws = ctx->ws;
-    uint32_t* ent = static_cast<uint32_t*>(ws.tile_ent.ensure(sizeof(uint32_t) * nchunks * nrb * cap));
-    int* flags = static_cast<int*>(ws.flags.ensure(4096));
-    SLQ_CUDA_CHECK(cudaMemsetAsync(flags, 0, 2 * sizeof(int), ctx->stream));
-    int NP = 2;
-    while (NP < kKwRows * zeta) NP <<= 1;
-    if (d >= (int64_t(1) << 22)) return false;  // bucket keys: r << 10
-    WarpBucketArgs wa{compact, zeta, m, d, rblk, rw, nw, nrb, cap, ent, flags + 1};
-    const size_t bsmem = sizeof(uint32_t) * NP + sizeof(int) * (static_cast<size_t>(nrb) * nw + 1);
-    SLQ_CUDA_CHECK(cudaFuncSetAttribute(warp_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(bsmem)));
-    warp_bucket_kernel<<<static_cast<unsigned>(nchunks), 1024, bsmem, ctx->stream>>>(wa);
-    SLQ_LAUNCH_CHECK(ctx);
-
-    const int64_t ldw = round_up(ncols_out, 32);
-    const int64_t nslabs = ldw / 32;
-    const size_t st = kKwRows * 256 + round_up(static_cast<int64_t>(cap) * 4, 128);
-    const int ns = static_cast<int>(std::min<size_t>(kKwMaxStages, (227 * 1024 - 256) / st));
-    const size_t smem = ns * st;
-    int64_t nsplit = 1;
-    if (!exact) {
-        double best = 1e30;
-        const int64_t ctas = nslabs * nrb;
-        for (int64_t s = 1; s <= 16 && s <= nchunks; ++s) {
-            const double waves = std::ceil(static_cast<double>(ctas * s) / ctx->num_sms);
-            const double cost = waves / s + 0.02 * s;
-            if (cost < best - 1e-9) {
-                best = cost;
-                nsplit = s;
-            }
-        }
-    }
-    double* Yw = (nsplit == 1 && ldw == ncols_out) ? Y
-                 : static_cast<double*>(ws.ypart.ensure(sizeof(double) * nsplit * ldw * d));
-    KwArgs g{m, d, ldw, nsplit, 0, nchunks, ent, cap, nrb, rblk, rw, ns, val, Yw};
-    const CUtensorMap map = gather_tensor_map(A->A, ld, m, 32, false, kKwBox);
-    const dim3 grid(static_cast<unsigned>(nrb), static_cast<unsigned>(nslabs), static_cast<unsigned>(nsplit));
-    if (exact) launch_kw_rw<true>(ctx, nw, rw, map, g, grid, smem);
-    else launch_kw_rw<false>(ctx, nw, rw, map, g, grid, smem);
-    if (ctx->defer_status) {
-        defer_status_dev(ctx, flags, kCondAny2, kStatusSketchOverflow);
-    } else {
-        int hflag[2] = {0, 0};
-        SLQ_CUDA_CHECK(cudaMemcpyAsync(hflag, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-        if (hflag[0] || hflag[1]) return false;
-    }
-    if (Yw != Y) {
-        if (nsplit == 1) {
-            SLQ_CUDA_CHECK(cudaMemcpyAsync(Y, Yw, sizeof(double) * d * ncols_out, cudaMemcpyDeviceToDevice, ctx->stream));
-        } else {
-            const int64_t tot = d * ncols_out;
-            reduce_splits_kernel<<<static_cast<unsigned>(ceil_div(tot, 256)), 256, 0, ctx->stream>>>(Yw, nsplit, d, ldw,
-                                                                                                    ncols_out, Y);
-            SLQ_LAUNCH_CHECK(ctx);
-        }
-    }
-    return true;
-}
-
 }  // namespace
 
 void check_chunk_csr(slq_ctx* ctx, const ChunkCsr& cc) {
@@ -1565,9 +1227,6 @@ void sketch_apply_compact_dev(slq_ctx* ctx, const slq_dense* A, int64_t d, const
     // per A row to repay the tile gather's per-row-block restaging)
     const bool row_gather = slq_env_flag("SLQ_ROW_GATHER") ||  // diagnostics: register gather in fast mode
                             ctx->force_row_gather || (zeta >= 16 && d <= 2048) || (zeta <= 2 && d >= 2048);
-    if (!colptr_dev && zeta <= 64 && slq_env_flag("SLQ_K2W") && !ctx->force_row_gather &&
-        sketch_apply_warp(ctx, A, d, compact, zeta, val, exact, Y))
-        return;
     if (!exact && !row_gather && sketch_apply_dmma(ctx, A, d, compact, colptr_dev, zeta, val, Y)) return;
     DenseGather G = dense_gather_plan(ctx, m, A->n, A->ld, d, compact, colptr_dev, zeta, val, exact, Y, false);
     dense_gather_rows(ctx, G, A->A, 0, m);
