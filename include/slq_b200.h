@@ -177,6 +177,13 @@ int slq_sparse_set_rhs(slq_sparse* A, const double* b_host);
  * +-col_scale[col] (host array of n, NULL = +-1). */
 int slq_sparse_fill_random(slq_sparse* A, int64_t nnz_per_row, uint64_t seed, const double* col_scale);
 int slq_sparse_free(slq_sparse* A);
+/* (Re)builds the row-blocked CSC copy of A that the LSQR / gradient solves
+ * stream for A^T u (the first solve on A builds it implicitly and keeps it
+ * with the matrix).  Call it after rewriting the CSR arrays of a matrix from
+ * slq_sparse_create_csr in place once a solve has run on it.  No reference
+ * counterpart: part of the device representation, like the CSC -> CSR
+ * conversion of slq_sparse_upload_csc. */
+int slq_sparse_prepare(slq_ctx* ctx, slq_sparse* A);
 
 /* sketch.hpp:298 + :304 for a sparse operand: Y = S A (d x n, column-major)
  * and Sb, bit-identical to spmm(csc, csc) / matvec(csc) on one GPU. */

@@ -630,6 +630,11 @@ class SparseDeviceMatrix:
         cs = _vec(col_scale) if col_scale is not None else None
         _check(C.lib.slq_sparse_fill_random(self.handle, nnz_per_row, seed & (2**64 - 1), _d(cs)))
 
+    def prepare(self):
+        """(Re)build the row-blocked CSC copy the solves stream for A^T u (done
+        implicitly by the first solve; needed after rewriting the CSR in place)."""
+        _check(C.lib.slq_sparse_prepare(self.ctx.handle, self.handle))
+
     def free(self):
         if self.handle:
             C.lib.slq_sparse_free(self.handle)

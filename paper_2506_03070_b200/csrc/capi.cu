@@ -253,7 +253,7 @@ Operand sparse_operand(slq_ctx* ctx, const slq_sparse* A) {
         if (t_gen) SLQ_CUDA_CHECK(cudaEventRecord(t_gen->e, ctx->stream));
         slq::sketch_apply_sparse_dev(ctx, A, d, zeta, seed, Yaug);
     };
-    o.make_op = [ctx, A] { return slq::make_sparse_op(ctx, A); };
+    o.make_op = [ctx, A] { return slq::make_sparse_op(ctx, A, true); };
     return o;
 }
 
@@ -1057,6 +1057,17 @@ int slq_sparse_fill_random(slq_sparse* A, int64_t nnz_per_row, uint64_t seed, co
         }
         slq::generate_sparse_rows_dev(ctx, A->n, nnz_per_row, seed, A->row_begin, A->m, dsc, A->rowptr, A->colidx,
                                       A->vals);
+        A->t_valid = false;
+    });
+}
+
+int slq_sparse_prepare(slq_ctx* ctx, slq_sparse* A) {
+    return guarded([&] {
+        need(ctx && A, SLQ_INVALID_ARG, "sparse_prepare: null argument");
+        SLQ_CUDA_CHECK(cudaSetDevice(ctx->device));
+        A->t_valid = false;
+        slq::prepare_two_pass(ctx, A);
+        SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     });
 }
 
@@ -1174,7 +1185,7 @@ int slq_lsqr_sparse(slq_ctx* ctx, const slq_sparse* A, const double* M, const do
         double* x = static_cast<double*>(dx.ensure(sizeof(double) * (n + 8)));
         slq::LsqrOut lo;
         const auto h0 = std::chrono::steady_clock::now();
-        slq::lsqr_dev(ctx, *slq::make_sparse_op(ctx, A), bd, P.M, P.Mt, P.x0, x, opts, residual_estimate,
+        slq::lsqr_dev(ctx, *slq::make_sparse_op(ctx, A, true), bd, P.M, P.Mt, P.x0, x, opts, residual_estimate,
                       iterates_error, residual_true, lo);
         SLQ_CUDA_CHECK(cudaMemcpy(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost));
         lo.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
@@ -1220,7 +1231,7 @@ int slq_gradient_descent_hbm_sparse(slq_ctx* ctx, const slq_sparse* A, const dou
         need(ctx && A && M && x0 && x_out && params, SLQ_INVALID_ARG, "gradient_descent_hbm_sparse: null argument");
         need(b != nullptr || A->b != nullptr, SLQ_INVALID_ARG, "gradient_descent_hbm_sparse: no right-hand side");
         gd_common(ctx, A->m, A->n, M, b, x0, params, opts, x_out, report, residual_estimate, iterates_error,
-                  residual_true, slq::kSparseRowPad, [&] { return slq::make_sparse_op(ctx, A); });
+                  residual_true, slq::kSparseRowPad, [&] { return slq::make_sparse_op(ctx, A, true); });
     });
 }
 
@@ -1252,7 +1263,7 @@ int slq_time_sparse_pass(slq_ctx* ctx, const slq_sparse* A, int reps, double* se
     return guarded([&] {
         need(ctx && A && seconds, SLQ_INVALID_ARG, "time_sparse_pass: null argument");
         SLQ_CUDA_CHECK(cudaSetDevice(ctx->device));
-        *seconds = slq::time_fused_pass(ctx, *slq::make_sparse_op(ctx, A), reps);
+        *seconds = slq::time_fused_pass(ctx, *slq::make_sparse_op(ctx, A, true), reps);
     });
 }
 

@@ -146,6 +146,16 @@ struct slq_sparse {
     double* vals = nullptr;     // nnz (+4 slack)
     double* b = nullptr;        // m (+ slack) right-hand side rows, may be null
     bool owned = true;
+    // row-blocked CSC copy for the two-pass LSQR operator (sparse.cu), built
+    // on the first solve and kept with the matrix; invalidated by the entry
+    // points that rewrite the CSR (slq_sparse_prepare rebuilds it)
+    uint32_t* t_blkcol = nullptr;  // [nblk][n + 1] column starts per row block
+    uint16_t* t_crow = nullptr;    // [nnz] row offset within the block
+    double* t_cval = nullptr;      // [nnz]
+    double* t_uscr = nullptr;      // [m + pad] u_hat scratch for passes that do not keep it
+    uint16_t* t_col16 = nullptr;   // [nnz + pad] the CSR's column indices as u16 (n < 65536)
+    int64_t t_nblk = 0;
+    bool t_valid = false;
 };
 
 namespace slq {

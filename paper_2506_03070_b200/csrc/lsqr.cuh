@@ -36,6 +36,7 @@ struct PassOp {
     virtual void pass(slq_ctx* ctx, const PassCall& c) const = 0;
     virtual std::vector<uint64_t> key() const = 0;  // identity for the graph cache
     virtual double pass_bytes() const = 0;          // algorithmic bytes of one pass
+    virtual double moved_bytes() const { return pass_bytes(); }  // bytes actually streamed (>= algorithmic)
 };
 
 std::unique_ptr<PassOp> make_dense_op(slq_ctx* ctx, const slq_dense* A);

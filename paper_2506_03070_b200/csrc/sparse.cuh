@@ -18,7 +18,12 @@ void sketch_apply_sparse_dev(slq_ctx* ctx, const slq_sparse* A, int64_t d, int64
 // K2s for a caller-given sketch already in compact form (colptr_dev null = uniform zeta)
 void sketch_apply_sparse_compact_dev(slq_ctx* ctx, const slq_sparse* A, int64_t d, const uint32_t* compact,
                                      const int64_t* colptr_dev, int64_t zeta_max, double val, double* Y);
-// K4s operator for LSQR
-std::unique_ptr<PassOp> make_sparse_op(slq_ctx* ctx, const slq_sparse* A);
+// Build (or rebuild) the row-blocked CSC copy the two-pass operator reads
+// (stream-ordered; kept with the matrix until its CSR is rewritten).
+void prepare_two_pass(slq_ctx* ctx, slq_sparse* A);
+// K4s operator for LSQR.  two_pass: u_hat over the CSR, then z = A^T u_hat over
+// a row-blocked CSC copy built here (solves: many passes amortise the build);
+// false: the single fused pass (one-off products)
+std::unique_ptr<PassOp> make_sparse_op(slq_ctx* ctx, const slq_sparse* A, bool two_pass = false);
 
 }  // namespace slq

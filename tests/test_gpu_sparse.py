@@ -150,3 +150,31 @@ def test_sparse_operator_products(m, n, dens):
                                     ct.byref(ss)) == 0
     assert np.allclose(ax, D @ x, rtol=1e-13, atol=1e-13)
     assert np.allclose(aty, D.T @ y, rtol=1e-12, atol=1e-13)
+
+
+def test_sparse_two_pass_multiblock(monkeypatch):
+    """The two-pass LSQR operator (u_hat over the CSR, z = A^T u_hat over the
+    row-blocked CSC copy, blocks of 16384 rows) across several blocks with a
+    partial last block, rows longer than 64 entries and empty rows: against the
+    oracle's CSC LSQR and the single fused pass (SLQ_SPARSE_ONEPASS=1)."""
+    m, n, d, zeta = 50_001, 300, 1200, 8
+    Acsc, A = rand_csc(m, n, 0.02, 31, long_rows=6, empty_rows=5)
+    b = np.random.default_rng(4).standard_normal(m)
+    Y, Sb = C.sketch_apply_csc(d, zeta, 5, m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, b)
+    M, Q = C.build_preconditioner(Y)
+    x0 = C.initial_guess(M, Q, Sb)
+    xo, repo = C.lsqr_csc(m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, M, b, x0, eps=0.0, maxit=10,
+                          one_sync=True)
+    x2, rep2 = slq.lsqr_one_sync(Acsc, M, b, x0, slq.SolveOptions(eps=0.0, maxit=10))
+    monkeypatch.setenv("SLQ_SPARSE_ONEPASS", "1")
+    x1, rep1 = slq.lsqr_one_sync(Acsc, M, b, x0, slq.SolveOptions(eps=0.0, maxit=10))
+    for x, rep in ((x2, rep2), (x1, rep1)):
+        assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
+        assert np.allclose(rep.residual_estimate, repo.residual_estimate, rtol=1e-9)
+    # the gradient family runs its passes without keeping u_hat (scratch vector path)
+    monkeypatch.delenv("SLQ_SPARSE_ONEPASS")
+    P = slq.hbm_params(float(np.sqrt(n / d)))
+    xg, _ = slq.gradient_descent_hbm(Acsc, M, b, x0, P, slq.SolveOptions(eps=0.0, maxit=6))
+    xgo, _ = C.gd_hbm_csc(m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, M, b, x0, P.alpha, P.beta,
+                          eps=0.0, maxit=6)
+    assert np.linalg.norm(xg - xgo) <= 1e-10 * np.linalg.norm(xgo)
