@@ -325,6 +325,9 @@ int run_solve(slq_ctx* ctx, const Operand& A, int64_t d, int64_t zeta, uint64_t 
                              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
         };
         Timer t0(ctx->stream);
+        // the operator first: a sparse A's transposed copy (if not built yet)
+        // is then built on the side stream while the sketch and QR run
+        auto op = A.make_op();
         Timer t1(ctx->stream);
         A.sketch(Yaug, d, zeta, seed, &t1);
         mark("apply");
@@ -369,7 +372,6 @@ int run_solve(slq_ctx* ctx, const Operand& A, int64_t d, int64_t zeta, uint64_t 
         Timer t5(ctx->stream);
         double* x = static_cast<double*>(ws.xbuf.ensure(sizeof(double) * (n + 8)));
         slq::LsqrOut lo;
-        auto op = A.make_op();
         slq::lsqr_dev(ctx, *op, nullptr, P.M, P.Mt, P.x0, x, opts, est, nullptr, nullptr, lo, P.status);
         mark("lsqr");
         Timer t6(ctx->stream);
@@ -490,6 +492,9 @@ int slq_ctx_destroy(slq_ctx* ctx) {
         slq::comm_destroy(ctx);
         if (ctx->lsqr_exec) cudaGraphExecDestroy(ctx->lsqr_exec);
         if (ctx->lsqr_hdone) cudaFreeHost(ctx->lsqr_hdone);
+        if (ctx->aux) cudaStreamDestroy(ctx->aux);
+        for (cudaEvent_t e : ctx->aux_ev)
+            if (e) cudaEventDestroy(e);
         if (ctx->qr_hi) cudaStreamDestroy(ctx->qr_hi);
         if (ctx->qr_lo) cudaStreamDestroy(ctx->qr_lo);
         for (cudaEvent_t e : ctx->qr_ev)
@@ -1049,6 +1054,10 @@ int slq_sparse_fill_random(slq_sparse* A, int64_t nnz_per_row, uint64_t seed, co
         need(A != nullptr, SLQ_INVALID_ARG, "null matrix");
         need(A->nnz == A->m * nnz_per_row, SLQ_DIMENSION_MISMATCH, "sparse_fill_random: nnz != m * nnz_per_row");
         slq_ctx* ctx = A->ctx;
+        if (A->t_pending) {  // a transposed-copy build may still be reading the CSR
+            SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));
+            A->t_pending = false;
+        }
         slq::DevBuf sc;
         double* dsc = nullptr;
         if (col_scale) {
@@ -1065,6 +1074,8 @@ int slq_sparse_prepare(slq_ctx* ctx, slq_sparse* A) {
     return guarded([&] {
         need(ctx && A, SLQ_INVALID_ARG, "sparse_prepare: null argument");
         SLQ_CUDA_CHECK(cudaSetDevice(ctx->device));
+        if (A->t_pending) SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));
+        A->t_pending = false;
         A->t_valid = false;
         slq::prepare_two_pass(ctx, A);
         SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));

@@ -121,6 +121,10 @@ struct slq_ctx {
     double* defer_status = nullptr;
     bool force_row_gather = false;  // rerun after a K2d bucket overflow
     cudaEvent_t lsqr_ev[2] = {nullptr, nullptr};
+    // side stream for work that overlaps the sketch (the sparse operator's
+    // transposed-copy build); aux_ev[0]: main -> aux, aux_ev[1]: aux -> main
+    cudaStream_t aux = nullptr;
+    cudaEvent_t aux_ev[2] = {nullptr, nullptr};
 };
 
 struct slq_dense {
@@ -156,6 +160,7 @@ struct slq_sparse {
     uint16_t* t_col16 = nullptr;   // [nnz + pad] the CSR's column indices as u16 (n < 65536)
     int64_t t_nblk = 0;
     bool t_valid = false;
+    bool t_pending = false;        // built on ctx->aux; the main stream has not waited for it yet
 };
 
 namespace slq {

@@ -920,6 +920,7 @@ std::unique_ptr<PassOp> make_dense_op(slq_ctx* ctx, const slq_dense* A) {
 void lsqr_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* M, const double* Mt,
               const double* x0, double* x, const slq_solve_opts& opts, double* est_hist,
               double* err_hist, double* true_hist, LsqrOut& out, const double* abort) {
+    op.ready(ctx);
     const int64_t m = op.m, n = op.n;
     const int64_t maxit = std::max<int64_t>(0, opts.maxit);
     Workspace& ws = ctx->ws;
@@ -1381,6 +1382,7 @@ __global__ void copy_vec_kernel(const double* src, double* a, double* b, int64_t
 void gd_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* M, const double* Mt,
             const double* x0, double alpha, double beta, double* x, const slq_solve_opts& opts, double* est_hist,
             double* err_hist, double* true_hist, LsqrOut& out) {
+    op.ready(ctx);
     const int64_t m = op.m, n = op.n;
     (void)m;
     const int64_t maxit = std::max<int64_t>(0, opts.maxit);
@@ -1528,6 +1530,7 @@ __global__ void fill_hash_kernel(double* v, int64_t n, uint64_t salt) {
 }  // namespace
 
 double time_fused_pass(slq_ctx* ctx, const PassOp& op, int reps) {
+    op.ready(ctx);
     // Average device time of one K4 launch in its steady-state iteration form
     // (u_hat = A p + c u, z = A^T u_hat, ||u_hat||^2), CUDA events on the
     // launching stream.  The operands are the LIVE ones of the last LSQR solve
@@ -1579,6 +1582,7 @@ double time_fused_pass(slq_ctx* ctx, const PassOp& op, int reps) {
 }
 
 void op_matvec_dev(slq_ctx* ctx, const PassOp& op, const double* x, double* y) {
+    op.ready(ctx);
     // u_hat = A x + 0 * y (y zeroed first, so no stored right-hand side is read)
     const int64_t n = op.n, m = op.m;
     double* part = static_cast<double*>(ctx->ws.lsqr_part.ensure(sizeof(double) * op.grid() * (n + 1)));
@@ -1587,6 +1591,7 @@ void op_matvec_dev(slq_ctx* ctx, const PassOp& op, const double* x, double* y) {
 }
 
 void op_rmatvec_dev(slq_ctx* ctx, const PassOp& op, const double* y, double* z, double* zero_n) {
+    op.ready(ctx);
     // p = 0, c = 1: u_hat = y, z = A^T y, ||y||^2 from the same pass
     const int64_t n = op.n;
     double* part = static_cast<double*>(ctx->ws.lsqr_part.ensure(sizeof(double) * op.grid() * (n + 1)));
@@ -1599,6 +1604,7 @@ void op_rmatvec_dev(slq_ctx* ctx, const PassOp& op, const double* y, double* z, 
 }
 
 double backward_error_dev(slq_ctx* ctx, const PassOp& op, const double* b_dev, const double* x, double a_norm) {
+    op.ready(ctx);
     // r = b - A x:  u_hat = A x - b = -r;  z = A^T u_hat = -A^T r
     const int64_t n = op.n;
     Workspace& ws = ctx->ws;

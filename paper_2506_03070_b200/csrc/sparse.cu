@@ -511,44 +511,91 @@ struct BcscArgs {
 };
 
 // One CTA per row block.  Warp w owns a contiguous range of the block's rows:
-// (1) per-warp column counts (a row's columns are distinct, so within a row
-// the lanes never collide; rows are ordered by __syncwarp), (2) column
-// starts = exclusive scan over (column, warp), (3) each warp re-walks its
-// rows in order and places entries -- ascending row within every column,
-// deterministic, no atomics.
+// (1) per-warp column counts (u16: a row's columns are distinct, so within a
+// row the lanes never collide; rows are ordered by __syncwarp), (2) column
+// starts (exclusive scan of the column totals) and per-warp bases relative to
+// them (u16, < kTbRows), (3) each warp re-walks its rows in order and places
+// entries -- ascending row within every column, deterministic, no atomics.
+// The row walks keep four rows' loads in flight (two entries per lane per
+// row; longer rows take a tail loop).
+constexpr int kBcRows = 4;
+
+struct BcRows {
+    int64_t lo[kBcRows], hi[kBcRows];
+    int c[kBcRows][2];
+    double v[kBcRows][2];
+};
+
+template <bool VALS>
+__device__ __forceinline__ void bc_load(const BcscArgs& a, int64_t r, int64_t r_end, int lane, BcRows& q) {
+    const int64_t rr = min(r + lane, r_end);
+    const int64_t rp = lane <= kBcRows ? a.rowptr[rr] : 0;
+#pragma unroll
+    for (int t = 0; t < kBcRows; ++t) {
+        q.lo[t] = __shfl_sync(0xffffffffu, rp, t);
+        q.hi[t] = r + t < r_end ? __shfl_sync(0xffffffffu, rp, t + 1) : q.lo[t];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t e = q.lo[t] + lane + 32 * h;
+            const bool ok = e < q.hi[t];
+            q.c[t][h] = ok ? __ldcs(a.colidx + e) : 0;
+            if (VALS) q.v[t][h] = ok ? __ldcs(a.vals + e) : 0.0;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(1024) bcsc_build_kernel(BcscArgs a) {
-    extern __shared__ uint32_t bcs[];  // [W][n] counts, then bases
+    extern __shared__ uint32_t bcs[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int W = a.W;
     const int64_t n = a.n;
+    uint32_t* start = bcs;                                     // [n] column start in the block
+    uint16_t* rel = reinterpret_cast<uint16_t*>(bcs + n);     // [W][n] counts, then bases
     const int64_t b = blockIdx.x;
     const int64_t r0 = b * kTbRows, r1 = min(a.m, r0 + kTbRows);
     const int64_t e0 = a.rowptr[r0];
-    for (int64_t i = tid; i < static_cast<int64_t>(W) * n; i += blockDim.x) bcs[i] = 0;
+    for (int64_t i = tid; i < static_cast<int64_t>(W) * n; i += blockDim.x) rel[i] = 0;
     __syncthreads();
     const int64_t rows = r1 - r0;
     const int64_t wr0 = r0 + warp * rows / W, wr1 = r0 + (warp + 1) * rows / W;
-    uint32_t* mine = bcs + static_cast<int64_t>(warp) * n;
+    uint16_t* mine = rel + static_cast<int64_t>(warp) * n;
     if (warp < W) {
-        for (int64_t r = wr0; r < wr1; ++r) {
-            for (int64_t e = a.rowptr[r] + lane; e < a.rowptr[r + 1]; e += 32) {
-                const int c = a.colidx[e];
-                mine[c] += 1;
-                a.col16[e] = static_cast<uint16_t>(c);
+        for (int64_t r = wr0; r < wr1; r += kBcRows) {
+            BcRows q;
+            bc_load<false>(a, r, wr1, lane, q);
+#pragma unroll
+            for (int t = 0; t < kBcRows; ++t) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    if (q.lo[t] + lane + 32 * h < q.hi[t]) {
+                        mine[q.c[t][h]] += 1;
+                        a.col16[q.lo[t] + lane + 32 * h] = static_cast<uint16_t>(q.c[t][h]);
+                    }
+                for (int64_t e = q.lo[t] + 64 + lane; e < q.hi[t]; e += 32) {  // rows of > 64 entries
+                    const int c = a.colidx[e];
+                    mine[c] += 1;
+                    a.col16[e] = static_cast<uint16_t>(c);
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
     }
     __syncthreads();
-    // exclusive scan over (column, warp) in column-major order: column j's
-    // start + the counts of warps < w.  Thread t scans a contiguous column
-    // range, then a block scan of the range totals.
+    // column totals -> per-warp relative bases; exclusive scan of the totals
     __shared__ uint32_t tot[1024];
     const int64_t per = (n + blockDim.x - 1) / blockDim.x;
     const int64_t j0 = tid * per, j1 = min(n, j0 + per);
     uint32_t run = 0;
-    for (int64_t j = j0; j < j1; ++j)
-        for (int w = 0; w < W; ++w) run += bcs[static_cast<int64_t>(w) * n + j];
+    for (int64_t j = j0; j < j1; ++j) {
+        uint32_t cj = 0;
+        for (int w = 0; w < W; ++w) {
+            const uint32_t c = rel[static_cast<int64_t>(w) * n + j];
+            rel[static_cast<int64_t>(w) * n + j] = static_cast<uint16_t>(cj);
+            cj += c;
+        }
+        start[j] = cj;  // total for now
+        run += cj;
+    }
     tot[tid] = run;
     __syncthreads();
     for (int o = 1; o < 1024; o <<= 1) {
@@ -560,25 +607,38 @@ __global__ void __launch_bounds__(1024) bcsc_build_kernel(BcscArgs a) {
     run = tot[tid] - run;  // exclusive
     uint32_t* bc = a.blkcol + b * (n + 1);
     for (int64_t j = j0; j < j1; ++j) {
+        const uint32_t cj = start[j];
+        start[j] = run;
         bc[j] = run;
-        for (int w = 0; w < W; ++w) {
-            const uint32_t c = bcs[static_cast<int64_t>(w) * n + j];
-            bcs[static_cast<int64_t>(w) * n + j] = run;
-            run += c;
-        }
+        run += cj;
     }
     if (tid == blockDim.x - 1) bc[n] = tot[tid];
     __syncthreads();
     if (warp < W) {
-        for (int64_t r = wr0; r < wr1; ++r) {
-            for (int64_t e = a.rowptr[r] + lane; e < a.rowptr[r + 1]; e += 32) {
-                const int c = a.colidx[e];
-                const uint32_t pos = mine[c];
-                mine[c] = pos + 1;
-                a.crow[e0 + pos] = static_cast<uint16_t>(r - r0);
-                a.cval[e0 + pos] = a.vals[e];
+        for (int64_t r = wr0; r < wr1; r += kBcRows) {
+            BcRows q;
+            bc_load<true>(a, r, wr1, lane, q);
+#pragma unroll
+            for (int t = 0; t < kBcRows; ++t) {
+                const uint16_t rl = static_cast<uint16_t>(r + t - r0);
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    if (q.lo[t] + lane + 32 * h < q.hi[t]) {
+                        const int c = q.c[t][h];
+                        const uint32_t pos = start[c] + mine[c];
+                        mine[c] += 1;
+                        a.crow[e0 + pos] = rl;
+                        a.cval[e0 + pos] = q.v[t][h];
+                    }
+                for (int64_t e = q.lo[t] + 64 + lane; e < q.hi[t]; e += 32) {
+                    const int c = a.colidx[e];
+                    const uint32_t pos = start[c] + mine[c];
+                    mine[c] += 1;
+                    a.crow[e0 + pos] = rl;
+                    a.cval[e0 + pos] = a.vals[e];
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
     }
 }
@@ -883,7 +943,7 @@ void sparse_free(slq_sparse* A) {
     A->t_valid = false;
 }
 
-void prepare_two_pass(slq_ctx* ctx, slq_sparse* A) {
+void prepare_two_pass(slq_ctx* ctx, slq_sparse* A, bool async) {
     if (A->t_valid) return;
     const int64_t m = A->m, n = A->n, nnz = A->nnz;
     if (!A->t_crow) {  // sizes are fixed for the handle's lifetime
@@ -896,14 +956,30 @@ void prepare_two_pass(slq_ctx* ctx, slq_sparse* A) {
         SLQ_CUDA_CHECK(cudaMemsetAsync(A->t_col16, 0, sizeof(uint16_t) * (nnz + 64), ctx->stream));
         SLQ_CUDA_CHECK(cudaMemsetAsync(A->t_uscr, 0, sizeof(double) * (m + kSparseRowPad), ctx->stream));
     }
-    int W = static_cast<int>(std::min<int64_t>(32, (200 * 1024) / (4 * std::max<int64_t>(n, 1))));
+    int W = static_cast<int>(std::min<int64_t>(32, (200 * 1024 - 4 * n) / (2 * std::max<int64_t>(n, 1))));
     if (W < 1) fail(SLQ_UNSUPPORTED, "sparse lsqr: n too large for the blocked-CSC build");
-    const size_t smem = sizeof(uint32_t) * W * n;
+    const size_t smem = sizeof(uint32_t) * n + sizeof(uint16_t) * W * n;
     SLQ_CUDA_CHECK(cudaFuncSetAttribute(bcsc_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
     BcscArgs ba{A->rowptr, A->colidx, A->vals, m, n, W, A->t_blkcol, A->t_crow, A->t_cval, A->t_col16};
-    bcsc_build_kernel<<<static_cast<unsigned>(A->t_nblk), 1024, smem, ctx->stream>>>(ba);
+    cudaStream_t st = ctx->stream;
+    if (async) {
+        // on the side stream, after everything already queued on the main one
+        // (the CSR fill); the first pass waits for it (SparseOp::ready)
+        if (!ctx->aux) {
+            SLQ_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+            for (cudaEvent_t& e : ctx->aux_ev) SLQ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        SLQ_CUDA_CHECK(cudaEventRecord(ctx->aux_ev[0], ctx->stream));
+        SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev[0], 0));
+        st = ctx->aux;
+    }
+    bcsc_build_kernel<<<static_cast<unsigned>(A->t_nblk), 1024, smem, st>>>(ba);
     SLQ_LAUNCH_CHECK(ctx);
+    if (async) {
+        SLQ_CUDA_CHECK(cudaEventRecord(ctx->aux_ev[1], ctx->aux));
+        A->t_pending = true;
+    }
     A->t_valid = true;
 }
 
@@ -981,7 +1057,7 @@ public:
                n < 65536 &&
                m > 0 && A->nnz > 0;
         if (two_) {
-            prepare_two_pass(ctx, const_cast<slq_sparse*>(A));
+            prepare_two_pass(ctx, const_cast<slq_sparse*>(A), true);
             nblk_ = A->t_nblk;
             blkcol_ = A->t_blkcol;
             crow_ = A->t_crow;
@@ -1005,6 +1081,13 @@ public:
                                             static_cast<int>(smem_)));
     }
     int grid() const override { return grid_; }
+    void ready(slq_ctx* ctx) const override {
+        slq_sparse* A = const_cast<slq_sparse*>(A_);
+        if (two_ && A->t_pending) {
+            SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));
+            A->t_pending = false;
+        }
+    }
     void pass(slq_ctx* ctx, const PassCall& c) const override {
         if (!c.u_in && !A_->b) fail(SLQ_INVALID_ARG, "sparse lsqr: no right-hand side");
         // the z pass reads u_hat back: callers that do not keep it get a scratch vector

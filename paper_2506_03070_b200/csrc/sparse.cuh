@@ -19,8 +19,9 @@ void sketch_apply_sparse_dev(slq_ctx* ctx, const slq_sparse* A, int64_t d, int64
 void sketch_apply_sparse_compact_dev(slq_ctx* ctx, const slq_sparse* A, int64_t d, const uint32_t* compact,
                                      const int64_t* colptr_dev, int64_t zeta_max, double val, double* Y);
 // Build (or rebuild) the row-blocked CSC copy the two-pass operator reads
-// (stream-ordered; kept with the matrix until its CSR is rewritten).
-void prepare_two_pass(slq_ctx* ctx, slq_sparse* A);
+// (kept with the matrix until its CSR is rewritten).  async: on ctx->aux,
+// overlapping what the main stream does next; PassOp::ready joins it.
+void prepare_two_pass(slq_ctx* ctx, slq_sparse* A, bool async = false);
 // K4s operator for LSQR.  two_pass: u_hat over the CSR, then z = A^T u_hat over
 // a row-blocked CSC copy built here (solves: many passes amortise the build);
 // false: the single fused pass (one-off products)
