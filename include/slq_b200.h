@@ -82,6 +82,16 @@ typedef struct {
 } slq_host_comm;
 int slq_ctx_set_host_comm(slq_ctx* ctx, const slq_host_comm* comm, int rank, int nranks);
 
+/* Diagnostics: with SLQ_GUARD=1 in the environment, the library's device
+ * scratch buffers are allocated with 64 KB guard bands (0xA5) on both sides;
+ * this call synchronizes the device and reports how many bands were found
+ * overwritten (live buffers now + buffers released since the process began).
+ * Without SLQ_GUARD it reports 0. */
+int slq_debug_check_guards(int64_t* corrupted);
+/* Self-test of that mechanism (SLQ_GUARD=1 only): plants one out-of-bounds
+ * write behind a scratch buffer and reports whether the release check saw it. */
+int slq_debug_guard_selftest(int* detected);
+
 /* distsim.hpp:31-42 partition_rows: boundaries[0..p] */
 int slq_partition_rows(int64_t m, int p, int64_t* boundaries);
 

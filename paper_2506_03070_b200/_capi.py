@@ -138,6 +138,8 @@ _SIGS = {
     "slq_sparse_fill_random": (ct.c_int, [vp, i64, u64, dp]),
     "slq_sparse_free": (ct.c_int, [vp]),
     "slq_sparse_prepare": (ct.c_int, [vp, vp]),
+    "slq_debug_check_guards": (ct.c_int, [ct.POINTER(i64)]),
+    "slq_debug_guard_selftest": (ct.c_int, [ct.POINTER(ct.c_int)]),
     "slq_spmm_csc_csc": (ct.c_int, [vp, i64, i64, ip, dp, ip, i64, ip, ip, dp, dp]),
     "slq_sketch_apply_sparse": (ct.c_int, [vp, vp, i64, i64, u64, dp, dp]),
     "slq_lsqr_sparse": (ct.c_int, [vp, vp, dp, dp, dp, ct.POINTER(SolveOpts), dp, ct.POINTER(Report), dp, dp, dp]),

@@ -10,6 +10,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -1307,3 +1309,98 @@ int slq_solve_host(slq_ctx* ctx, const double* A, int64_t m, int64_t n, int64_t 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------- guard bands
+
+namespace slq {
+namespace guard {
+namespace {
+struct Rec {
+    void* base;
+    size_t ub;
+};
+std::mutex g_mu;
+std::unordered_map<const void*, Rec>& live() {
+    static auto* m = new std::unordered_map<const void*, Rec>();  // never destroyed: DevBufs may outlive statics
+    return *m;
+}
+int64_t g_bad = 0;
+
+bool band_intact(const void* dev) {
+    std::vector<unsigned char> h(kBand);
+    if (cudaMemcpy(h.data(), dev, kBand, cudaMemcpyDeviceToHost) != cudaSuccess) return true;  // context gone
+    for (unsigned char c : h)
+        if (c != 0xA5) return false;
+    return true;
+}
+bool intact(const Rec& r) {
+    return band_intact(r.base) && band_intact(static_cast<const char*>(r.base) + kBand + r.ub);
+}
+}  // namespace
+
+bool enabled() {
+    static const bool on = slq_env_flag("SLQ_GUARD");
+    return on;
+}
+
+void on_alloc(void* base, size_t ub, const void* owner) {
+    SLQ_CUDA_CHECK(cudaMemset(base, 0xA5, kBand));
+    SLQ_CUDA_CHECK(cudaMemset(static_cast<char*>(base) + kBand + ub, 0xA5, kBand));
+    SLQ_CUDA_CHECK(cudaDeviceSynchronize());
+    std::lock_guard<std::mutex> lk(g_mu);
+    live()[owner] = Rec{base, ub};
+}
+
+void on_release(void* base, const void* owner) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = live().find(owner);
+    if (it == live().end() || it->second.base != base) return;
+    if (cudaDeviceSynchronize() == cudaSuccess && !intact(it->second)) {
+        ++g_bad;
+        std::fprintf(stderr, "[slq] guard band overwritten around a %zu-byte device buffer\n", it->second.ub);
+    }
+    live().erase(it);
+}
+}  // namespace guard
+}  // namespace slq
+
+int slq_debug_check_guards(int64_t* corrupted) {
+    return guarded([&] {
+        need(corrupted != nullptr, SLQ_INVALID_ARG, "debug_check_guards: null argument");
+        SLQ_CUDA_CHECK(cudaDeviceSynchronize());
+        std::lock_guard<std::mutex> lk(slq::guard::g_mu);
+        int64_t bad = 0;
+        for (auto& kv : slq::guard::live())
+            if (!slq::guard::intact(kv.second)) ++bad;
+        *corrupted = bad + slq::guard::g_bad;
+    });
+}
+
+namespace {
+__global__ void guard_selftest_kernel(double* p, int64_t i) { p[i] = 1.0; }
+}  // namespace
+
+int slq_debug_guard_selftest(int* detected) {
+    return guarded([&] {
+        need(detected != nullptr, SLQ_INVALID_ARG, "debug_guard_selftest: null argument");
+        need(slq::guard::enabled(), SLQ_INVALID_ARG, "debug_guard_selftest: needs SLQ_GUARD=1");
+        int64_t before = 0, after = 0;
+        SLQ_CUDA_CHECK(cudaDeviceSynchronize());
+        {
+            std::lock_guard<std::mutex> lk(slq::guard::g_mu);
+            before = slq::guard::g_bad;
+        }
+        {
+            slq::DevBuf b;
+            double* p = static_cast<double*>(b.ensure(1000 * sizeof(double)));
+            guard_selftest_kernel<<<1, 1>>>(p, 1024 + 3);  // one element past the 8 KB rounding: in the band
+            SLQ_CUDA_CHECK(cudaGetLastError());
+        }  // release checks the bands
+        {
+            std::lock_guard<std::mutex> lk(slq::guard::g_mu);
+            after = slq::guard::g_bad;
+            slq::guard::g_bad = before;  // the planted corruption does not count against the process
+        }
+        *detected = after > before ? 1 : 0;
+    });
+}

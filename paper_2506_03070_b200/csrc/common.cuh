@@ -45,6 +45,18 @@ inline bool slq_env_flag(const char* name) {
     return v && v[0] && !(v[0] == '0' && v[1] == 0);
 }
 
+// Guard-band mode (SLQ_GUARD=1, diagnostics): every DevBuf allocation gets
+// 64 KB bands before and after it filled with 0xA5; the bands are verified
+// when the buffer is released and on slq_debug_check_guards().  Catches
+// out-of-bounds device writes into the library's scratch (compute-sanitizer
+// is not available on every GPU pool).
+namespace guard {
+constexpr size_t kBand = 64 * 1024;
+bool enabled();
+void on_alloc(void* base, size_t user_bytes, const void* owner);
+void on_release(void* base, const void* owner);  // checks, then forgets
+}  // namespace guard
+
 // Device buffer with RAII; grow-only reuse via ensure().
 struct DevBuf {
     void* p = nullptr;
@@ -54,20 +66,38 @@ struct DevBuf {
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
+        if (p) {
+            if (base_ != p) {  // guarded allocation
+                guard::on_release(base_, this);
+                cudaFree(base_);
+            } else {
+                cudaFree(p);
+            }
+        }
+        p = base_ = nullptr;
         bytes = 0;
     }
     void* ensure(size_t b) {
         if (b <= bytes && p) return p;
         release();
         if (b == 0) b = 16;
-        SLQ_CUDA_CHECK(cudaMalloc(&p, b));
+        if (guard::enabled()) {
+            const size_t ub = (b + 255) & ~size_t(255);
+            SLQ_CUDA_CHECK(cudaMalloc(&base_, ub + 2 * guard::kBand));
+            p = static_cast<char*>(base_) + guard::kBand;
+            guard::on_alloc(base_, ub, this);
+        } else {
+            SLQ_CUDA_CHECK(cudaMalloc(&p, b));
+            base_ = p;
+        }
         bytes = b;
         return p;
     }
     template <class T>
     T* as() const { return static_cast<T*>(p); }
+
+private:
+    void* base_ = nullptr;
 };
 
 // Per-context scratch, grow-only (sizes at C3 in DESIGN.md).
