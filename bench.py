@@ -442,13 +442,14 @@ def run_sparse(args, world, rank, local_rank):
 # ------------------------------------------------------------ main
 
 def _sparse_traffic(m, n, world):
-    """DRAM bytes per sparse pass launch from the committed ncu capture
-    (profiles/ncu_summary.json), scaled to this rank's rows; None if absent."""
+    """DRAM bytes per launch of the two-pass sparse operator (u_hat pass + A^T u_hat
+    pass) from the committed ncu capture (profiles/ncu_summary.json), scaled to
+    this rank's rows; None if absent."""
     try:
-        sp = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json"))).get("sparse_pass_kernel", {})
+        sp = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json"))).get("sparse_two_pass", {})
         if sp.get("n") != n or not sp.get("m"):
             return None
-        return (sp["dram_bytes_read"] + sp["dram_bytes_write"]) * (m / world) / sp["m"]
+        return sp["dram_bytes_per_operator_launch"] * (m / world) / sp["m"]
     except Exception:
         return None
 
