@@ -1057,7 +1057,7 @@ int slq_sparse_fill_random(slq_sparse* A, int64_t nnz_per_row, uint64_t seed, co
         need(A->nnz == A->m * nnz_per_row, SLQ_DIMENSION_MISMATCH, "sparse_fill_random: nnz != m * nnz_per_row");
         slq_ctx* ctx = A->ctx;
         if (A->t_pending) {  // a transposed-copy build may still be reading the CSR
-            SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));
+            SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, A->t_ready, 0));
             A->t_pending = false;
         }
         slq::DevBuf sc;
@@ -1076,7 +1076,7 @@ int slq_sparse_prepare(slq_ctx* ctx, slq_sparse* A) {
     return guarded([&] {
         need(ctx && A, SLQ_INVALID_ARG, "sparse_prepare: null argument");
         SLQ_CUDA_CHECK(cudaSetDevice(ctx->device));
-        if (A->t_pending) SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));
+        if (A->t_pending) SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, A->t_ready, 0));
         A->t_pending = false;
         A->t_valid = false;
         slq::prepare_two_pass(ctx, A);

@@ -152,7 +152,8 @@ struct slq_ctx {
     bool force_row_gather = false;  // rerun after a K2d bucket overflow
     cudaEvent_t lsqr_ev[2] = {nullptr, nullptr};
     // side stream for work that overlaps the sketch (the sparse operator's
-    // transposed-copy build); aux_ev[0]: main -> aux, aux_ev[1]: aux -> main
+    // transposed-copy build); aux_ev[0]: main -> aux (the join back is the
+    // matrix's own event, slq_sparse::t_ready)
     cudaStream_t aux = nullptr;
     cudaEvent_t aux_ev[2] = {nullptr, nullptr};
 };
@@ -190,7 +191,8 @@ struct slq_sparse {
     uint16_t* t_col16 = nullptr;   // [nnz + pad] the CSR's column indices as u16 (n < 65536)
     int64_t t_nblk = 0;
     bool t_valid = false;
-    bool t_pending = false;        // built on ctx->aux; the main stream has not waited for it yet
+    bool t_pending = false;        // built on a side stream; nobody has waited for it yet
+    cudaEvent_t t_ready = nullptr; // recorded after the side-stream build
 };
 
 namespace slq {

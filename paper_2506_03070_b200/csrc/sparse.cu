@@ -935,6 +935,8 @@ void sparse_free(slq_sparse* A) {
     cudaFree(A->t_cval);
     cudaFree(A->t_uscr);
     cudaFree(A->t_col16);
+    if (A->t_ready) cudaEventDestroy(A->t_ready);
+    A->t_ready = nullptr;
     A->t_col16 = nullptr;
     A->t_blkcol = nullptr;
     A->t_crow = nullptr;
@@ -968,7 +970,7 @@ void prepare_two_pass(slq_ctx* ctx, slq_sparse* A, bool async) {
         // (the CSR fill); the first pass waits for it (SparseOp::ready)
         if (!ctx->aux) {
             SLQ_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
-            for (cudaEvent_t& e : ctx->aux_ev) SLQ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            SLQ_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->aux_ev[0], cudaEventDisableTiming));
         }
         SLQ_CUDA_CHECK(cudaEventRecord(ctx->aux_ev[0], ctx->stream));
         SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev[0], 0));
@@ -977,7 +979,8 @@ void prepare_two_pass(slq_ctx* ctx, slq_sparse* A, bool async) {
     bcsc_build_kernel<<<static_cast<unsigned>(A->t_nblk), 1024, smem, st>>>(ba);
     SLQ_LAUNCH_CHECK(ctx);
     if (async) {
-        SLQ_CUDA_CHECK(cudaEventRecord(ctx->aux_ev[1], ctx->aux));
+        if (!A->t_ready) SLQ_CUDA_CHECK(cudaEventCreateWithFlags(&A->t_ready, cudaEventDisableTiming));
+        SLQ_CUDA_CHECK(cudaEventRecord(A->t_ready, ctx->aux));
         A->t_pending = true;
     }
     A->t_valid = true;
@@ -1084,7 +1087,7 @@ public:
     void ready(slq_ctx* ctx) const override {
         slq_sparse* A = const_cast<slq_sparse*>(A_);
         if (two_ && A->t_pending) {
-            SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));
+            SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, A->t_ready, 0));
             A->t_pending = false;
         }
     }

@@ -158,7 +158,10 @@ def test_sparse_two_pass_multiblock(monkeypatch):
     partial last block, rows longer than 64 entries and empty rows: against the
     oracle's CSC LSQR and the single fused pass (SLQ_SPARSE_ONEPASS=1)."""
     m, n, d, zeta = 50_001, 300, 1200, 8
-    Acsc, A = rand_csc(m, n, 0.02, 31, long_rows=6, empty_rows=5)
+    # 40 long rows in the first 128-row chunk: > 8192 entries, so that chunk takes the
+    # u_hat pass's direct (unstaged) path
+    Acsc, A = rand_csc(m, n, 0.02, 31, long_rows=40, empty_rows=5)
+    assert Acsc.col_pointers[-1] > 0 and (A.tocsr()[:128].nnz > 8192)
     b = np.random.default_rng(4).standard_normal(m)
     Y, Sb = C.sketch_apply_csc(d, zeta, 5, m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, b)
     M, Q = C.build_preconditioner(Y)
