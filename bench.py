@@ -187,12 +187,14 @@ def make_problem(torch, m, n, cond, rho, row_begin, row_end, dev, dist=None, see
         p[r:r + step] = Abuf[r:r + step, :n] @ w
     pn2 = allreduce((p * p).sum().reshape(1))
     pn = float(pn2.sqrt())
+    # residual direction, drawn per GLOBAL chunk (like G) so b is the same for any row partition
     z = torch.empty(ml, dtype=f64, device=dev)
-    for r in range(row_begin, row_end, step):
-        r1 = min(row_end, r + step)
+    for c in range(row_begin // chunk, (row_end - 1) // chunk + 1):
         g = torch.Generator(device=dev)
-        g.manual_seed(seed * 13 + 3 + r)
-        z[r - row_begin:r1 - row_begin] = torch.rand(r1 - r, dtype=f64, device=dev, generator=g) * 2 - 1
+        g.manual_seed(seed * 13 + 3 + c)
+        blk = torch.rand(chunk, dtype=f64, device=dev, generator=g) * 2 - 1
+        a, b_ = max(row_begin, c * chunk), min(row_end, (c + 1) * chunk)
+        z[a - row_begin:b_ - row_begin] = blk[a - c * chunk:b_ - c * chunk]
     for _ in range(2):
         c = allreduce(U.T @ z)
         z -= U @ c
@@ -201,7 +203,8 @@ def make_problem(torch, m, n, cond, rho, row_begin, row_end, dev, dist=None, see
     Abuf[:, n] = p * (range_norm / pn) + z * (rho / zn)
     x_star = (w * (range_norm / pn)).cpu().numpy()
     del U, z, p
-    torch.cuda.synchronize()
+    if dev.type == "cuda":
+        torch.cuda.synchronize()
     return Abuf, ld, x_star
 
 
