@@ -173,6 +173,64 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
             const int rows = static_cast<int>(min(static_cast<int64_t>(a.R), a.m - row0));
             // rows of this tile owned by this warp: (k*R + i) % 8 == warp
             int i = first_row(k);
+            if (NP <= 2) {
+                // short rows (ld <= 128): four of the warp's rows per step, their
+                // dot products reduced together (a 4-way transpose reduction: 6
+                // double shuffles instead of 20, four independent chains)
+                for (int t = 0; i < rows; i += 4 * kConsumerWarps, t += 4) {
+                    double2 vr4[4][NP];
+                    double acc[4];
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        const int ig = i + g * kConsumerWarps;
+                        const double* row = tile + static_cast<int64_t>(ig < rows ? ig : 0) * ld;
+                        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                        for (int q = 0; q < NP; ++q) {
+                            const int64_t j = 2 * lane + 64 * q;
+                            vr4[g][q] = (j < ld && ig < rows) ? *reinterpret_cast<const double2*>(row + j)
+                                                              : make_double2(0.0, 0.0);
+                            a0 = fma(vr4[g][q].x, j < ld ? pr[2 * q] : 0.0, a0);
+                            a1 = fma(vr4[g][q].y, j < ld ? pr[2 * q + 1] : 0.0, a1);
+                        }
+                        acc[g] = a0 + a1;
+                    }
+                    const bool h16 = lane & 16, h8 = lane & 8;
+                    double k0 = h16 ? acc[2] : acc[0], k1 = h16 ? acc[3] : acc[1];
+                    k0 += __shfl_xor_sync(0xffffffffu, h16 ? acc[0] : acc[2], 16);
+                    k1 += __shfl_xor_sync(0xffffffffu, h16 ? acc[1] : acc[3], 16);
+                    double kk = h8 ? k1 : k0;
+                    kk += __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
+                    kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+                    kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+                    kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+                    // lane group gq = lane >> 3 now holds row (h16 ? 2 : 0) + (h8 ? 1 : 0)
+                    const int gq = (h16 ? 2 : 0) + (h8 ? 1 : 0);
+                    const int ig = i + gq * kConsumerWarps;
+                    double u = 0.0;
+                    if (upre) u = __shfl_sync(0xffffffffu, ucur, (t + gq) & 31);
+                    else if (ig < rows) u = a.u_in ? a.u_in[row0 + ig] : tile[static_cast<int64_t>(ig) * ld + a.n];
+                    const double uh = __dadd_rn(kk, __dmul_rn(c, u));
+                    if ((lane & 7) == 0 && ig < rows) {
+                        if (a.u_out) a.u_out[row0 + ig] = uh;
+                        ssq = fma(uh, uh, ssq);
+                    }
+                    if (a.want_z) {
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+                            const int gl = (g & 2 ? 16 : 0) + (g & 1 ? 8 : 0);
+                            const double ug = __shfl_sync(0xffffffffu, uh, gl);
+                            if (i + g * kConsumerWarps < rows) {
+#pragma unroll
+                                for (int q = 0; q < NP; ++q) {
+                                    z[2 * q] = fma(vr4[g][q].x, ug, z[2 * q]);
+                                    z[2 * q + 1] = fma(vr4[g][q].y, ug, z[2 * q + 1]);
+                                }
+                            }
+                        }
+                    }
+                }
+            } else
             for (int t = 0; i < rows; i += kConsumerWarps, ++t) {
                 const double* row = tile + static_cast<int64_t>(i) * ld;
                 const double u = upre ? __shfl_sync(0xffffffffu, ucur, t & 31)  // upre is CTA-uniform
@@ -219,6 +277,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
                     red[warp * ld + j + 1] = z[2 * q + 1];
                 }
             }
+        }
+        if (NP <= 2) {  // quad path: lanes 0, 8, 16, 24 hold the partial sums of their row groups
+            ssq += __shfl_xor_sync(0xffffffffu, ssq, 8);
+            ssq += __shfl_xor_sync(0xffffffffu, ssq, 16);
         }
         if (lane == 0) red[kConsumerWarps * ld + warp] = ssq;
     }
