@@ -36,7 +36,6 @@ struct PassOp {
     virtual void pass(slq_ctx* ctx, const PassCall& c) const = 0;
     virtual std::vector<uint64_t> key() const = 0;  // identity for the graph cache
     virtual double pass_bytes() const = 0;          // algorithmic bytes of one pass
-    virtual double moved_bytes() const { return pass_bytes(); }  // bytes actually streamed (>= algorithmic)
     // make the main stream wait for data the operator prepares asynchronously
     // (called by every routine before its first pass)
     virtual void ready(slq_ctx*) const {}

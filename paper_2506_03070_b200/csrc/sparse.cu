@@ -1119,13 +1119,6 @@ public:
     }
     // algorithmic bytes: one read of the CSR (the operator's data) + u in, u_hat out
     double pass_bytes() const override { return 12.0 * A_->nnz + 8.0 * (m + 1) + 16.0 * m; }
-    // bytes the two-pass operator actually streams: CSR values + u16 columns +
-    // row pointers + u in, u_hat out; then the blocked CSC (u16 row + value),
-    // u_hat again and the per-block column starts
-    double moved_bytes() const override {
-        return two_ ? 10.0 * A_->nnz + 8.0 * (m + 1) + 16.0 * m + 10.0 * A_->nnz + 8.0 * m + 4.0 * nblk_ * (n + 1)
-                    : pass_bytes();
-    }
 
 private:
     const slq_sparse* A_;
