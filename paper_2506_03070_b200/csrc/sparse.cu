@@ -1115,7 +1115,7 @@ public:
                 reinterpret_cast<uint64_t>(A_->vals), reinterpret_cast<uint64_t>(A_->b), static_cast<uint64_t>(m),
                 static_cast<uint64_t>(n), static_cast<uint64_t>(W_), static_cast<uint64_t>(grid_),
                 reinterpret_cast<uint64_t>(crow_), reinterpret_cast<uint64_t>(cval_), reinterpret_cast<uint64_t>(blkcol_),
-                reinterpret_cast<uint64_t>(us_)};
+                reinterpret_cast<uint64_t>(us_), reinterpret_cast<uint64_t>(col16_)};
     }
     // algorithmic bytes: one read of the CSR (the operator's data) + u in, u_hat out
     double pass_bytes() const override { return 12.0 * A_->nnz + 8.0 * (m + 1) + 16.0 * m; }
