@@ -181,3 +181,22 @@ def test_sparse_two_pass_multiblock(monkeypatch):
     xgo, _ = C.gd_hbm_csc(m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, M, b, x0, P.alpha, P.beta,
                           eps=0.0, maxit=6)
     assert np.linalg.norm(xg - xgo) <= 1e-10 * np.linalg.norm(xgo)
+
+
+@pytest.mark.parametrize("m,n,dens", [(100, 12, 0.3), (37, 1, 0.6), (300, 24, 0.02)])
+def test_sparse_two_pass_small_shapes(m, n, dens):
+    """The two-pass operator at shapes below one 128-row chunk / one 16384-row
+    block, with empty rows (and n = 1): LSQR against the oracle's CSC LSQR.
+    For n <= maxit the Krylov space is exhausted: whether beta / alpha land on
+    an exact zero (Breakdown) or on a rounding-level value depends on the
+    summation order, so only x is compared there."""
+    Acsc, A = rand_csc(m, n, dens, m + 7 * n, empty_rows=3)
+    b = np.random.default_rng(m).standard_normal(m)
+    M = np.triu(np.random.default_rng(n).standard_normal((n, n))) + 3.0 * np.eye(n)
+    x0 = np.zeros(n)
+    xo, repo = C.lsqr_csc(m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, M, b, x0, eps=0.0, maxit=4,
+                          one_sync=True)
+    x, rep = slq.lsqr_one_sync(Acsc, M, b, x0, slq.SolveOptions(eps=0.0, maxit=4))
+    if n > 4:
+        assert rep.iterations == repo.iterations
+    assert np.linalg.norm(x - xo) <= 1e-10 * max(np.linalg.norm(xo), 1e-300)
