@@ -86,6 +86,7 @@ struct PassArgs {
     const int* skip;       // nonzero -> no-op
     int R, S;              // rows per tile, stages
     int keep_l2;           // A small enough to stay L2-resident across passes: evict_last, else evict_first
+    int upre_rows;         // tiles of >= this many rows prefetch u one tile ahead
 };
 
 template <int NP, bool P_SMEM>
@@ -148,12 +149,12 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
             }
         }
         const double c = a.coef ? *a.coef : a.c_fixed;
-        // Short rows (many rows per warp per tile): u of this warp's rows is
+        // Short rows (tiles of >= upre_rows rows): u of this warp's rows is
         // loaded one tile ahead, lane l holding the l-th row the warp owns
         // (R <= 7 * 32), so no row waits on a global load.  Long rows hide the
         // per-row load behind the row itself (and the prefetch measurably
         // raises the sustained power draw at C3): per-row loads there.
-        const bool upre = a.u_in && a.R >= 4 * kConsumerWarps;
+        const bool upre = a.u_in && a.R >= a.upre_rows;
         auto first_row = [&](int64_t k) {
             return static_cast<int>(((warp - (k * a.R) % kConsumerWarps) + kConsumerWarps) % kConsumerWarps);
         };
@@ -948,17 +949,18 @@ public:
         double keep_mb = 96.0;
         if (const char* e = std::getenv("SLQ_L2_KEEP_MB")) keep_mb = std::atof(e);
         keep_l2_ = 8.0 * static_cast<double>(A->m) * static_cast<double>(A->ld) <= keep_mb * 1048576.0 ? 1 : 0;
+        if (const char* e = std::getenv("SLQ_UPRE_ROWS")) upre_rows_ = std::atoi(e);
     }
     int grid() const override { return pp_.grid; }
     void pass(slq_ctx* ctx, const PassCall& c) const override {
         PassArgs a{A_->A, A_->ld, m, n, c.p, c.u_in, c.u_out, c.coef, c.c_fixed, c.part, c.want_z, c.skip, 0, 0,
-                   keep_l2_};
+                   keep_l2_, upre_rows_};
         launch_pass(ctx, pp_, a);
     }
     std::vector<uint64_t> key() const override {
         return {1, reinterpret_cast<uint64_t>(A_->A), static_cast<uint64_t>(m), static_cast<uint64_t>(n),
                 static_cast<uint64_t>(A_->ld), static_cast<uint64_t>(pp_.grid), static_cast<uint64_t>(pp_.R),
-                static_cast<uint64_t>(pp_.S), static_cast<uint64_t>(keep_l2_)};
+                static_cast<uint64_t>(pp_.S), static_cast<uint64_t>(keep_l2_), static_cast<uint64_t>(upre_rows_)};
     }
     double pass_bytes() const override { return 8.0 * m * n + 16.0 * m; }
 
@@ -966,6 +968,10 @@ private:
     const slq_dense* A_;
     PassPlan pp_;
     int keep_l2_ = 0;
+    // u is prefetched one tile ahead for tiles of >= 16 rows (rows <= 4 KB:
+    // C2's 16-row tiles 0.82 -> 0.68 ms per iteration); C3's 8-row tiles load
+    // u per row, hidden behind the 8 KB row (SLQ_UPRE_ROWS overrides, diagnostics)
+    int upre_rows_ = 16;
 };
 
 struct LsqrBufs {
