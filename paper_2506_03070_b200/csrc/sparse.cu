@@ -821,6 +821,7 @@ __global__ void __launch_bounds__(1024, 1) sparse_tpass_kernel(TPassArgs a) {
     const int64_t n = a.n;
     double* u_s = reinterpret_cast<double*>(tsm);
     double* z_s = u_s + kTbRows;
+    uint32_t* bc_s = reinterpret_cast<uint32_t*>(z_s + ((n + 1) & ~int64_t(1)));  // the block's column starts
     for (int64_t j = tid; j < n; j += blockDim.x) z_s[j] = 0.0;
     if (tid == 0) {
         mbar_init(&ubar, 1);
@@ -833,13 +834,17 @@ __global__ void __launch_bounds__(1024, 1) sparse_tpass_kernel(TPassArgs a) {
         const int64_t r0 = b * kTbRows, rows = min(static_cast<int64_t>(kTbRows), a.m - r0);
         if (tid == 0) {
             const unsigned bytes = static_cast<unsigned>((rows * 8 + 15) & ~int64_t(15));
-            mbar_expect_tx(&ubar, bytes);
+            // column starts: 16-byte aligned superset of [b (n+1), (b+1)(n+1))
+            const int64_t c0 = (b * (n + 1)) & ~int64_t(3);
+            const unsigned cbytes = static_cast<unsigned>((((b + 1) * (n + 1) - c0) * 4 + 15) & ~int64_t(15));
+            mbar_expect_tx(&ubar, bytes + cbytes);
             bulk_g2s(u_s, a.uhat + r0, bytes, &ubar);
+            bulk_g2s(bc_s, a.blkcol + c0, cbytes, &ubar);
         }
         mbar_wait(&ubar, phase);
         phase ^= 1u;
         const int64_t e0 = a.rowptr[r0];
-        const uint32_t* bc = a.blkcol + b * (n + 1);
+        const uint32_t* bc = bc_s + (b * (n + 1) - ((b * (n + 1)) & ~int64_t(3)));
         const uint16_t* cr = a.crow + e0;
         const double* cv = a.cval + e0;
         for (int64_t j = warp; j < n; j += W) {
@@ -950,7 +955,7 @@ void prepare_two_pass(slq_ctx* ctx, slq_sparse* A, bool async) {
     const int64_t m = A->m, n = A->n, nnz = A->nnz;
     if (!A->t_crow) {  // sizes are fixed for the handle's lifetime
         A->t_nblk = ceil_div(std::max<int64_t>(m, 1), static_cast<int64_t>(kTbRows));
-        SLQ_CUDA_CHECK(cudaMalloc(&A->t_blkcol, sizeof(uint32_t) * A->t_nblk * (n + 1)));
+        SLQ_CUDA_CHECK(cudaMalloc(&A->t_blkcol, sizeof(uint32_t) * (A->t_nblk * (n + 1) + 16)));  // + bulk-copy slack
         SLQ_CUDA_CHECK(cudaMalloc(&A->t_crow, sizeof(uint16_t) * (nnz + 64)));
         SLQ_CUDA_CHECK(cudaMalloc(&A->t_cval, sizeof(double) * (nnz + 64)));
         SLQ_CUDA_CHECK(cudaMalloc(&A->t_uscr, sizeof(double) * (m + kSparseRowPad)));
@@ -1056,7 +1061,8 @@ public:
         // and the block's u_hat + z in shared memory); else p + one z copy per
         // warp in shared memory
         two_ = two_pass && slq_env_flag("SLQ_SPARSE_ONEPASS") == false &&
-               static_cast<int64_t>(kTbRows) * 8 + zrow <= budget && static_cast<int64_t>(UpG::kStage) * UpG::kStages + zrow <= 227 * 1024 &&
+               static_cast<int64_t>(kTbRows) * 8 + zrow + 4 * (n + 8) + 8 <= 227 * 1024 &&
+               static_cast<int64_t>(UpG::kStage) * UpG::kStages + zrow <= 227 * 1024 &&
                n < 65536 &&
                m > 0 && A->nnz > 0;
         if (two_) {
@@ -1071,7 +1077,7 @@ public:
             grid_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, ceil_div(m, UpG::kRows))));
             SLQ_CUDA_CHECK(cudaFuncSetAttribute(sparse_upass_kernel<UpG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 static_cast<int>(smem_)));
-            tsmem_ = static_cast<size_t>(kTbRows) * 8 + static_cast<size_t>(zrow);
+            tsmem_ = static_cast<size_t>(kTbRows) * 8 + static_cast<size_t>(zrow) + 8 + static_cast<size_t>(n + 8) * 4;
             SLQ_CUDA_CHECK(cudaFuncSetAttribute(sparse_tpass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 static_cast<int>(tsmem_)));
             return;
