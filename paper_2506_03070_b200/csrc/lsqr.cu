@@ -237,15 +237,20 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
                 const double u = upre ? __shfl_sync(0xffffffffu, ucur, t & 31)  // upre is CTA-uniform
                                       : (a.u_in ? a.u_in[row0 + i] : row[a.n]);
                 double acc0 = 0.0, acc1 = 0.0;
-                double2 vr[NP];  // the row stays in registers for the z update: one shared-memory read
+                // the row stays in registers for the z update (one shared-memory
+                // read) -- except at NP = 32, where row + z (256 registers) would
+                // spill: the z loop reads the row from shared memory again
+                constexpr bool kKeepRow = NP < 32;
+                double2 vr[kKeepRow ? NP : 1];
 #pragma unroll
                 for (int q = 0; q < NP; ++q) {
                     const int64_t j = 2 * lane + 64 * q;
-                    vr[q] = j < ld ? *reinterpret_cast<const double2*>(row + j) : make_double2(0.0, 0.0);
+                    const double2 v2 = j < ld ? *reinterpret_cast<const double2*>(row + j) : make_double2(0.0, 0.0);
+                    if (kKeepRow) vr[kKeepRow ? q : 0] = v2;
                     const double p0 = j < ld ? (P_SMEM ? p_s[j] : pr[2 * q]) : 0.0;
                     const double p1 = j < ld ? (P_SMEM ? p_s[j + 1] : pr[2 * q + 1]) : 0.0;
-                    acc0 = fma(vr[q].x, p0, acc0);
-                    acc1 = fma(vr[q].y, p1, acc1);
+                    acc0 = fma(v2.x, p0, acc0);
+                    acc1 = fma(v2.y, p1, acc1);
                 }
                 const double y = warp_sum(acc0 + acc1);
                 const double uh = __dadd_rn(y, __dmul_rn(c, u));
@@ -254,8 +259,12 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
                 if (a.want_z) {
 #pragma unroll
                     for (int q = 0; q < NP; ++q) {
-                        z[2 * q] = fma(vr[q].x, uh, z[2 * q]);
-                        z[2 * q + 1] = fma(vr[q].y, uh, z[2 * q + 1]);
+                        const int64_t j = 2 * lane + 64 * q;
+                        const double2 v2 = kKeepRow ? vr[kKeepRow ? q : 0]
+                                                    : (j < ld ? *reinterpret_cast<const double2*>(row + j)
+                                                              : make_double2(0.0, 0.0));
+                        z[2 * q] = fma(v2.x, uh, z[2 * q]);
+                        z[2 * q + 1] = fma(v2.y, uh, z[2 * q + 1]);
                     }
                 }
             }
