@@ -71,6 +71,10 @@ __device__ __forceinline__ double warp_sum(double v) {
 // --------------------------------------------------------------- K4 pass
 
 constexpr int kConsumerWarps = 7;  // + 1 producer warp = 256 threads (255-register budget)
+#ifndef SLQ_QUAD_NP
+#define SLQ_QUAD_NP 4
+#endif
+constexpr int kQuadNP = SLQ_QUAD_NP;  // rows of <= 64 * kQuadNP columns: four rows per warp step
 constexpr int kPassThreads = (kConsumerWarps + 1) * 32;
 
 struct PassArgs {
@@ -174,7 +178,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
             const int rows = static_cast<int>(min(static_cast<int64_t>(a.R), a.m - row0));
             // rows of this tile owned by this warp: (k*R + i) % 8 == warp
             int i = first_row(k);
-            if (NP <= 2) {
+            if (NP <= kQuadNP) {
                 // short rows (ld <= 128): four of the warp's rows per step, their
                 // dot products reduced together (a 4-way transpose reduction: 6
                 // double shuffles instead of 20, four independent chains)
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
                 }
             }
         }
-        if (NP <= 2) {  // quad path: lanes 0, 8, 16, 24 hold the partial sums of their row groups
+        if (NP <= kQuadNP) {  // quad path: lanes 0, 8, 16, 24 hold the partial sums of their row groups
             ssq += __shfl_xor_sync(0xffffffffu, ssq, 8);
             ssq += __shfl_xor_sync(0xffffffffu, ssq, 16);
         }
