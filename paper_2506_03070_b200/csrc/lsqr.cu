@@ -242,9 +242,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) fused_pass_kernel(PassArgs a)
                                       : (a.u_in ? a.u_in[row0 + i] : row[a.n]);
                 double acc0 = 0.0, acc1 = 0.0;
                 // the row stays in registers for the z update (one shared-memory
-                // read) -- except at NP = 32, where row + z (256 registers) would
-                // spill: the z loop reads the row from shared memory again
-                constexpr bool kKeepRow = NP < 32;
+                // read) -- except at NP >= 24, where row + z (192-256 registers)
+                // would spill: the z loop reads the row from shared memory again
+                constexpr bool kKeepRow = NP <= 16;
                 double2 vr[kKeepRow ? NP : 1];
 #pragma unroll
                 for (int q = 0; q < NP; ++q) {
@@ -892,9 +892,17 @@ PassPlan plan_pass(slq_ctx* ctx, const slq_dense* A) {
         pp.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, ntiles)));
         return pp;
     }
-    pp.NP = 1;
-    while (64 * pp.NP < ld) pp.NP <<= 1;
-    pp.p_smem = pp.NP >= 32;
+    // slots of 64 columns per lane pair: the smallest instantiated count that
+    // covers the row (12 and 24 keep rows of 700 / 1100 columns from running
+    // a third / half of their slots empty)
+    static const int kNPs[] = {1, 2, 4, 8, 12, 16, 24, 32};
+    pp.NP = 32;
+    for (int np : kNPs)
+        if (64 * np >= ld) {
+            pp.NP = np;
+            break;
+        }
+    pp.p_smem = pp.NP >= 24;
     const int64_t row_bytes = ld * static_cast<int64_t>(sizeof(double));
     int64_t R = (64 * 1024) / row_bytes;
     if (R >= 8) R = (R / 8) * 8;
@@ -946,7 +954,9 @@ void launch_pass(slq_ctx* ctx, const PassPlan& pp, PassArgs a) {
         case 2: launch_pass_t<2, false>(ctx, pp, a); break;
         case 4: launch_pass_t<4, false>(ctx, pp, a); break;
         case 8: launch_pass_t<8, false>(ctx, pp, a); break;
+        case 12: launch_pass_t<12, false>(ctx, pp, a); break;
         case 16: launch_pass_t<16, false>(ctx, pp, a); break;
+        case 24: launch_pass_t<24, true>(ctx, pp, a); break;
         default: launch_pass_t<32, true>(ctx, pp, a); break;
     }
 }

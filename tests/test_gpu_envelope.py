@@ -21,10 +21,13 @@ def _eta(A, b, x):
     return np.linalg.norm(A.T @ r) / (np.linalg.norm(A, 2) * np.linalg.norm(r))
 
 
-@pytest.mark.parametrize("m,n", [(6000, 2100), (5000, 3000), (6000, 4500), (8500, 8000)])
+@pytest.mark.parametrize("m,n", [(6000, 2100), (5000, 3000), (6000, 4500), (8500, 8000),
+                                 (3000, 150), (4000, 700), (5000, 1100), (5000, 1500), (4000, 2000)])
 def test_wide_pass_lsqr_vs_oracle(m, n):
-    """K4 wide rows (ld > 2048, NQ = 6 / 9 / 12 / 18): LSQR iterates against
-    the oracle's lsqr_one_sync at a fixed T from the same M and x0."""
+    """K4 at every slot count: wide rows (ld > 2048, NQ = 6 / 9 / 12 / 18) and
+    the one-warp-per-row pass at NP = 4 (quad path), 12, 24 (row re-read for
+    the z update), 32: LSQR iterates against the oracle's lsqr_one_sync at a
+    fixed T from the same M and x0."""
     rng = np.random.default_rng(n)
     A = np.asfortranarray(rng.standard_normal((m, n)) * np.logspace(0, -2, n))
     b = rng.standard_normal(m)
