@@ -1385,10 +1385,12 @@ namespace {
 // one TSQR level (and the levels above it); tol = rank tolerance of the original Y
 void qr_tsqr(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t ncols, int64_t ldy, double* R, double* qtb,
              double* sign_out, const double* tol) {
-    const int64_t leaf = std::min<int64_t>(kLeafRows, d);
+    // leaves of >= 2n rows (so every level halves the stack), at most what one
+    // panel cluster factors
+    const int64_t leaf = std::min<int64_t>(std::min<int64_t>(std::max<int64_t>(kLeafRows, 2 * n), kMaxPanelRows), d);
     const int64_t nblk = ceil_div(d, leaf);
     if (ceil_div(d, nblk) < 2 * n)
-        fail(SLQ_UNSUPPORTED, "householder_qr: d > 12400 needs n <= 4096 (TSQR leaves of >= 2n rows)");
+        fail(SLQ_UNSUPPORTED, "householder_qr: d > 12400 needs n <= 6200 (TSQR leaves of >= 2n rows)");
     DevBuf zero, leafbuf, stackbuf, rk;
     double* z0 = static_cast<double*>(zero.ensure(sizeof(double)));
     SLQ_CUDA_CHECK(cudaMemsetAsync(z0, 0, sizeof(double), ctx->stream));

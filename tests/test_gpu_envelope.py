@@ -62,6 +62,19 @@ def test_tsqr_tall_sketch_vs_oracle(d, n):
     assert np.abs(W.T @ W - np.eye(n)).max() <= max(10 * np.abs((Y @ Mo).T @ (Y @ Mo) - np.eye(n)).max(), 1e-12)
 
 
+def test_tsqr_wide_leaves():
+    """n > 4096 with d > 12400: TSQR leaves of 2n rows (here 2 leaves of 8400),
+    R against LAPACK's (numpy) QR with the diagonal made nonnegative."""
+    d, n = 16800, 4200
+    rng = np.random.default_rng(7)
+    Y = np.asfortranarray(rng.standard_normal((d, n)) * np.logspace(0, -3, n))
+    P, _ = slq.build_preconditioner(Y, Sb=rng.standard_normal(d), want_q=False)
+    Rn = np.linalg.qr(Y, mode="r")
+    Rn *= np.sign(np.diag(Rn))[:, None]
+    Rg = np.linalg.inv(P.M)
+    assert np.linalg.norm(Rg - Rn) / np.linalg.norm(Rn) <= 1e-12 * np.linalg.cond(Rn)
+
+
 def test_tsqr_rank_deficient_detected():
     rng = np.random.default_rng(2)
     Y = np.asfortranarray(rng.standard_normal((20000, 10)))
