@@ -7,4 +7,4 @@ timeout 600 python bench.py --m 100000 --n 100 --cond 1e3 --steps 20 --warmup 5 
 timeout 600 python bench.py --m 1048576 --n 500 --steps 10 --warmup 5 --no-cpu > gpurun_out/bench_c2.jsonl 2> gpurun_out/bench_c2.err
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_c3.jsonl 2> gpurun_out/bench_c3.err
 timeout 900 python bench.py --config c4 --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_c4.jsonl 2> gpurun_out/bench_c4.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches_c3.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --iters 30 > gpurun_out/ncu_c3_launches.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:slq:: -c 2000 --csv --log-file gpurun_out/launches_c3.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --iters 30 > gpurun_out/ncu_c3_launches.log 2>&1
