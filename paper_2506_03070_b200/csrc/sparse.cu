@@ -807,6 +807,7 @@ struct TPassArgs {
     double* part;         // [grid][n + 1]: z partials in [0, n)
     int want_z;
     const int* skip;
+    int z_smem;           // z accumulated in shared memory (else in part directly)
 };
 
 // grid CTAs split the row blocks evenly; per block: u_hat of the block ->
@@ -820,9 +821,13 @@ __global__ void __launch_bounds__(1024, 1) sparse_tpass_kernel(TPassArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = blockDim.x >> 5;
     const int64_t n = a.n;
     double* u_s = reinterpret_cast<double*>(tsm);
-    double* z_s = u_s + kTbRows;
-    uint32_t* bc_s = reinterpret_cast<uint32_t*>(z_s + ((n + 1) & ~int64_t(1)));  // the block's column starts
-    for (int64_t j = tid; j < n; j += blockDim.x) z_s[j] = 0.0;
+    uint32_t* bc_s = reinterpret_cast<uint32_t*>(u_s + kTbRows);  // the block's column starts
+    // z accumulates in shared memory when it fits, else in this CTA's partial
+    // row (column j is owned by warp j % W in every block: no races, fixed
+    // order); part[.][n] holds the u_hat pass's ||u_hat||^2
+    double* outp = a.part + static_cast<int64_t>(blockIdx.x) * (n + 1);
+    double* zp = a.z_smem ? reinterpret_cast<double*>(bc_s + ((n + 8) & ~int64_t(3))) : outp;
+    for (int64_t j = tid; j < n; j += blockDim.x) zp[j] = 0.0;
     if (tid == 0) {
         mbar_init(&ubar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -868,12 +873,12 @@ __global__ void __launch_bounds__(1024, 1) sparse_tpass_kernel(TPassArgs a) {
             double s = (sp[0] + sp[1]) + (sp[2] + sp[3]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) z_s[j] += s;
+            if (lane == 0) zp[j] += s;
         }
         __syncthreads();  // u_s is overwritten by the next block
     }
-    double* outp = a.part + static_cast<int64_t>(blockIdx.x) * (n + 1);
-    for (int64_t j = tid; j < n; j += blockDim.x) outp[j] = z_s[j];
+    if (a.z_smem)
+        for (int64_t j = tid; j < n; j += blockDim.x) outp[j] = zp[j];
 }
 
 }  // namespace
@@ -1060,11 +1065,15 @@ public:
         // two-pass: z from the row-blocked CSC copy (needs u16 row offsets
         // and the block's u_hat + z in shared memory); else p + one z copy per
         // warp in shared memory
+        // shared memory: the u_hat pass holds its ring + p, the A^T u_hat pass a
+        // block's u_hat + column starts (1 KB left for static shared memory)
+        const int64_t smax = 226 * 1024;
+        big_ring_ = static_cast<int64_t>(UpG::kStage) * UpG::kStages + zrow <= smax;
+        const int64_t ring = big_ring_ ? static_cast<int64_t>(UpG::kStage) * UpG::kStages
+                                       : static_cast<int64_t>(UpS::kStage) * UpS::kStages;
         two_ = two_pass && slq_env_flag("SLQ_SPARSE_ONEPASS") == false &&
-               static_cast<int64_t>(kTbRows) * 8 + zrow + 4 * (n + 8) + 8 <= 227 * 1024 &&
-               static_cast<int64_t>(UpG::kStage) * UpG::kStages + zrow <= 227 * 1024 &&
-               n < 65536 &&
-               m > 0 && A->nnz > 0;
+               static_cast<int64_t>(kTbRows) * 8 + 4 * (n + 8) <= smax && ring + zrow <= smax && n < 65536 && m > 0 &&
+               A->nnz > 0;
         if (two_) {
             prepare_two_pass(ctx, const_cast<slq_sparse*>(A), true);
             nblk_ = A->t_nblk;
@@ -1073,11 +1082,17 @@ public:
             cval_ = A->t_cval;
             us_ = A->t_uscr;
             col16_ = A->t_col16;
-            smem_ = UpG::kStage * UpG::kStages + static_cast<size_t>(zrow);
-            grid_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, ceil_div(m, UpG::kRows))));
-            SLQ_CUDA_CHECK(cudaFuncSetAttribute(sparse_upass_kernel<UpG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                static_cast<int>(smem_)));
-            tsmem_ = static_cast<size_t>(kTbRows) * 8 + static_cast<size_t>(zrow) + 8 + static_cast<size_t>(n + 8) * 4;
+            smem_ = static_cast<size_t>(ring + zrow);
+            grid_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, ceil_div(m, UpS::kRows))));
+            if (big_ring_)
+                SLQ_CUDA_CHECK(cudaFuncSetAttribute(sparse_upass_kernel<UpG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    static_cast<int>(smem_)));
+            else
+                SLQ_CUDA_CHECK(cudaFuncSetAttribute(sparse_upass_kernel<UpS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    static_cast<int>(smem_)));
+            tsmem_ = static_cast<size_t>(kTbRows) * 8 + static_cast<size_t>(n + 8) * 4;
+            z_smem_ = static_cast<int64_t>(tsmem_) + zrow + 32 <= smax;
+            if (z_smem_) tsmem_ += static_cast<size_t>(zrow) + 32;
             SLQ_CUDA_CHECK(cudaFuncSetAttribute(sparse_tpass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 static_cast<int>(tsmem_)));
             return;
@@ -1109,10 +1124,11 @@ public:
             return;
         }
         UPassArgs ua{A_->rowptr, col16_, A_->vals, A_->b, m, n, c.p, c.u_in, uo, c.coef, c.c_fixed, c.part, c.skip};
-        sparse_upass_kernel<UpG><<<grid_, 32 * (kUpConsumers + 1), smem_, ctx->stream>>>(ua);
+        if (big_ring_) sparse_upass_kernel<UpG><<<grid_, 32 * (kUpConsumers + 1), smem_, ctx->stream>>>(ua);
+        else sparse_upass_kernel<UpS><<<grid_, 32 * (kUpConsumers + 1), smem_, ctx->stream>>>(ua);
         SLQ_LAUNCH_CHECK(ctx);
         (void)a;
-        TPassArgs t{A_->rowptr, blkcol_, crow_, cval_, uo, m, n, nblk_, c.part, c.want_z, c.skip};
+        TPassArgs t{A_->rowptr, blkcol_, crow_, cval_, uo, m, n, nblk_, c.part, c.want_z, c.skip, z_smem_ ? 1 : 0};
         sparse_tpass_kernel<<<grid_, 1024, tsmem_, ctx->stream>>>(t);
         SLQ_LAUNCH_CHECK(ctx);
     }
@@ -1137,6 +1153,9 @@ private:
     // 128-row chunks, two 84 KB stages: measured against 64 x 4, 96 x 3 and
     // 160 x 2 at C4 (1.6 ms vs 2.05 / 1.9 / 1.7 ms for the u_hat pass)
     using UpG = UpGeom<128, 8192, 2>;
+    using UpS = UpGeom<64, 4096, 2>;  // wide p (n > ~7900): a smaller ring
+    bool big_ring_ = true;
+    bool z_smem_ = true;
     uint32_t* blkcol_ = nullptr;
     uint16_t* crow_ = nullptr;
     double* cval_ = nullptr;

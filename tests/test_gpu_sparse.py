@@ -200,3 +200,22 @@ def test_sparse_two_pass_small_shapes(m, n, dens):
     if n > 4:
         assert rep.iterations == repo.iterations
     assert np.linalg.norm(x - xo) <= 1e-10 * max(np.linalg.norm(xo), 1e-300)
+
+
+@pytest.mark.parametrize("m,n,dens", [(40_000, 9000, 0.002), (20_000, 3000, 0.005)])
+def test_sparse_two_pass_wide_n(m, n, dens):
+    """Wide sparse rows: at n = 9000 the u_hat pass runs its smaller ring (p
+    takes 72 KB of shared memory) and the A^T u_hat pass accumulates z in the
+    global partials; at n = 3000 both keep their shared-memory layouts."""
+    Acsc, A = rand_csc(m, n, dens, n, empty_rows=2)
+    b = np.random.default_rng(n).standard_normal(m)
+    rng = np.random.default_rng(1)
+    M = np.asfortranarray(np.diag(1.0 / np.maximum(np.sqrt(np.asarray(A.multiply(A).sum(axis=0)).ravel()), 1e-3))
+                          + np.triu(rng.standard_normal((n, n)), 1) * (1e-3 / np.sqrt(n)))
+    x0 = np.zeros(n)
+    xo, repo = C.lsqr_csc(m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, M, b, x0, eps=0.0, maxit=5,
+                          one_sync=True)
+    x, rep = slq.lsqr_one_sync(Acsc, M, b, x0, slq.SolveOptions(eps=0.0, maxit=5))
+    assert rep.iterations == repo.iterations == 5
+    assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
+    assert np.allclose(rep.residual_estimate, repo.residual_estimate, rtol=1e-9)
