@@ -676,7 +676,7 @@ struct UPassArgs {
     const int* skip;
 };
 
-template <class G>
+template <class G, int LPR>
 __global__ void __launch_bounds__(32 * (kUpConsumers + 1), 1) sparse_upass_kernel(UPassArgs a) {
     constexpr int kUpRows = G::kRows, kUpStages = G::kStages;
     constexpr unsigned kUpVBytes = G::kV, kUpCBytes = G::kC, kUpPBytes = G::kP, kUpStage = G::kStage;
@@ -737,9 +737,11 @@ __global__ void __launch_bounds__(32 * (kUpConsumers + 1), 1) sparse_upass_kerne
         }
         return;
     }
-    // ---------------- consumers: lane group g = lane >> 3 (8 lanes per row)
+    // ---------------- consumers: lane groups of LPR lanes, one row each
+    // (LPR = 4 for rows of <= 100 entries on average: twice the rows per warp step; else 8)
+    constexpr int kGroups = 32 / LPR;
     const double c = a.coef ? *a.coef : a.c_fixed;
-    const int g = lane >> 3, gl = lane & 7;
+    const int g = lane / LPR, gl = lane % LPR;
     double ssq = 0.0;
     for (int64_t k = 0; k < nk; ++k) {
         const int s = static_cast<int>(k % kUpStages);
@@ -754,7 +756,7 @@ __global__ void __launch_bounds__(32 * (kUpConsumers + 1), 1) sparse_upass_kerne
         const int64_t e0 = P[r0 - pa];
         const int64_t va = e0 & ~int64_t(1), ca = e0 & ~int64_t(7);
         const bool dir = direct[s] != 0;
-        for (int64_t i = r0 + warp * 4 + g; i - g < r1; i += 4 * kUpConsumers) {
+        for (int64_t i = r0 + warp * kGroups + g; i - g < r1; i += kGroups * kUpConsumers) {
             double acc = 0.0;
             if (i < r1) {
                 const int64_t lo = P[i - pa], hi = P[i + 1 - pa];
@@ -762,21 +764,20 @@ __global__ void __launch_bounds__(32 * (kUpConsumers + 1), 1) sparse_upass_kerne
                     // two independent chains per lane, loads of both issued first
                     double a1 = 0.0;
                     int64_t e = lo + gl;
-                    for (; e + 8 < hi; e += 16) {
-                        const int c0 = Cc[e - ca], c1 = Cc[e + 8 - ca];
-                        const double v0 = V[e - va], v1 = V[e + 8 - va];
+                    for (; e + LPR < hi; e += 2 * LPR) {
+                        const int c0 = Cc[e - ca], c1 = Cc[e + LPR - ca];
+                        const double v0 = V[e - va], v1 = V[e + LPR - va];
                         acc = fma(v0, p_s[c0], acc);
                         a1 = fma(v1, p_s[c1], a1);
                     }
                     if (e < hi) acc = fma(V[e - va], p_s[Cc[e - ca]], acc);
                     acc += a1;
                 } else {
-                    for (int64_t e = lo + gl; e < hi; e += 8) acc = fma(a.vals[e], p_s[a.col16[e]], acc);
+                    for (int64_t e = lo + gl; e < hi; e += LPR) acc = fma(a.vals[e], p_s[a.col16[e]], acc);
                 }
             }
-            acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+#pragma unroll
+            for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if (gl == 0 && i < r1) {
                 const double uh = __dadd_rn(acc, __dmul_rn(c, U[i - pa]));
                 if (a.u_out) a.u_out[i] = uh;
@@ -786,8 +787,8 @@ __global__ void __launch_bounds__(32 * (kUpConsumers + 1), 1) sparse_upass_kerne
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }
-    ssq += __shfl_xor_sync(0xffffffffu, ssq, 8);
-    ssq += __shfl_xor_sync(0xffffffffu, ssq, 16);
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
     if (lane == 0) red[warp] = ssq;
     asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kUpConsumers));  // consumers only (the producer has returned)
     if (tid == 0) {
@@ -1084,12 +1085,15 @@ public:
             col16_ = A->t_col16;
             smem_ = static_cast<size_t>(ring + zrow);
             grid_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms, ceil_div(m, UpS::kRows))));
-            if (big_ring_)
-                SLQ_CUDA_CHECK(cudaFuncSetAttribute(sparse_upass_kernel<UpG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    static_cast<int>(smem_)));
-            else
-                SLQ_CUDA_CHECK(cudaFuncSetAttribute(sparse_upass_kernel<UpS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    static_cast<int>(smem_)));
+            // rows of <= 100 entries on average: 4 lanes per row (C4's 50: 2.97 -> 2.84 ms;
+            // 200 entries: 2.80 vs 2.97 ms with 8 lanes)
+            short_rows_ = A->nnz <= 100 * m;
+            if (const char* e = std::getenv("SLQ_UPASS_LPR")) short_rows_ = std::atoi(e) == 4;  // diagnostics
+            const void* kfn = big_ring_ ? (short_rows_ ? reinterpret_cast<const void*>(sparse_upass_kernel<UpG, 4>)
+                                                       : reinterpret_cast<const void*>(sparse_upass_kernel<UpG, 8>))
+                                        : (short_rows_ ? reinterpret_cast<const void*>(sparse_upass_kernel<UpS, 4>)
+                                                       : reinterpret_cast<const void*>(sparse_upass_kernel<UpS, 8>));
+            SLQ_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
             tsmem_ = static_cast<size_t>(kTbRows) * 8 + static_cast<size_t>(n + 8) * 4;
             z_smem_ = static_cast<int64_t>(tsmem_) + zrow + 32 <= smax;
             if (z_smem_) tsmem_ += static_cast<size_t>(zrow) + 32;
@@ -1124,8 +1128,14 @@ public:
             return;
         }
         UPassArgs ua{A_->rowptr, col16_, A_->vals, A_->b, m, n, c.p, c.u_in, uo, c.coef, c.c_fixed, c.part, c.skip};
-        if (big_ring_) sparse_upass_kernel<UpG><<<grid_, 32 * (kUpConsumers + 1), smem_, ctx->stream>>>(ua);
-        else sparse_upass_kernel<UpS><<<grid_, 32 * (kUpConsumers + 1), smem_, ctx->stream>>>(ua);
+        const dim3 ub(32 * (kUpConsumers + 1));
+        if (big_ring_) {
+            if (short_rows_) sparse_upass_kernel<UpG, 4><<<grid_, ub, smem_, ctx->stream>>>(ua);
+            else sparse_upass_kernel<UpG, 8><<<grid_, ub, smem_, ctx->stream>>>(ua);
+        } else {
+            if (short_rows_) sparse_upass_kernel<UpS, 4><<<grid_, ub, smem_, ctx->stream>>>(ua);
+            else sparse_upass_kernel<UpS, 8><<<grid_, ub, smem_, ctx->stream>>>(ua);
+        }
         SLQ_LAUNCH_CHECK(ctx);
         (void)a;
         TPassArgs t{A_->rowptr, blkcol_, crow_, cval_, uo, m, n, nblk_, c.part, c.want_z, c.skip, z_smem_ ? 1 : 0};
@@ -1156,6 +1166,7 @@ private:
     using UpS = UpGeom<64, 4096, 2>;  // wide p (n > ~7900): a smaller ring
     bool big_ring_ = true;
     bool z_smem_ = true;
+    bool short_rows_ = false;
     uint32_t* blkcol_ = nullptr;
     uint16_t* crow_ = nullptr;
     double* cval_ = nullptr;
