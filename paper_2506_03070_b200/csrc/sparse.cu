@@ -1063,11 +1063,10 @@ public:
         n = A->n;
         const int64_t zrow = n * static_cast<int64_t>(sizeof(double));
         const int64_t budget = 220 * 1024;
-        // two-pass: z from the row-blocked CSC copy (needs u16 row offsets
-        // and the block's u_hat + z in shared memory); else p + one z copy per
-        // warp in shared memory
-        // shared memory: the u_hat pass holds its ring + p, the A^T u_hat pass a
-        // block's u_hat + column starts (1 KB left for static shared memory)
+        // two-pass (u16 columns / row offsets): the u_hat pass holds its ring +
+        // p in shared memory, the A^T u_hat pass a block's u_hat + column starts
+        // (+ z when it fits; 1 KB left for static shared memory); else the single
+        // fused pass with p + one z copy per warp in shared memory
         const int64_t smax = 226 * 1024;
         big_ring_ = static_cast<int64_t>(UpG::kStage) * UpG::kStages + zrow <= smax;
         const int64_t ring = big_ring_ ? static_cast<int64_t>(UpG::kStage) * UpG::kStages
@@ -1118,15 +1117,15 @@ public:
     }
     void pass(slq_ctx* ctx, const PassCall& c) const override {
         if (!c.u_in && !A_->b) fail(SLQ_INVALID_ARG, "sparse lsqr: no right-hand side");
-        // the z pass reads u_hat back: callers that do not keep it get a scratch vector
-        double* uo = (two_ && !c.u_out) ? us_ : c.u_out;
-        SPassArgs a{A_->rowptr, A_->colidx, A_->vals, A_->b, m, n, c.p, c.u_in, uo, c.coef, c.c_fixed,
-                    c.part, c.want_z, c.skip};
         if (!two_) {
+            SPassArgs a{A_->rowptr, A_->colidx, A_->vals, A_->b, m, n, c.p, c.u_in, c.u_out, c.coef, c.c_fixed,
+                        c.part, c.want_z, c.skip};
             sparse_pass_kernel<true><<<grid_, 32 * W_, smem_, ctx->stream>>>(a);
             SLQ_LAUNCH_CHECK(ctx);
             return;
         }
+        // the z pass reads u_hat back: callers that do not keep it get a scratch vector
+        double* uo = c.u_out ? c.u_out : us_;
         UPassArgs ua{A_->rowptr, col16_, A_->vals, A_->b, m, n, c.p, c.u_in, uo, c.coef, c.c_fixed, c.part, c.skip};
         const dim3 ub(32 * (kUpConsumers + 1));
         if (big_ring_) {
@@ -1137,7 +1136,6 @@ public:
             else sparse_upass_kernel<UpS, 8><<<grid_, ub, smem_, ctx->stream>>>(ua);
         }
         SLQ_LAUNCH_CHECK(ctx);
-        (void)a;
         TPassArgs t{A_->rowptr, blkcol_, crow_, cval_, uo, m, n, nblk_, c.part, c.want_z, c.skip, z_smem_ ? 1 : 0};
         sparse_tpass_kernel<<<grid_, 1024, tsmem_, ctx->stream>>>(t);
         SLQ_LAUNCH_CHECK(ctx);
@@ -1147,7 +1145,9 @@ public:
                 reinterpret_cast<uint64_t>(A_->vals), reinterpret_cast<uint64_t>(A_->b), static_cast<uint64_t>(m),
                 static_cast<uint64_t>(n), static_cast<uint64_t>(W_), static_cast<uint64_t>(grid_),
                 reinterpret_cast<uint64_t>(crow_), reinterpret_cast<uint64_t>(cval_), reinterpret_cast<uint64_t>(blkcol_),
-                reinterpret_cast<uint64_t>(us_), reinterpret_cast<uint64_t>(col16_)};
+                reinterpret_cast<uint64_t>(us_), reinterpret_cast<uint64_t>(col16_),
+                static_cast<uint64_t>(two_) | static_cast<uint64_t>(big_ring_) << 1 | static_cast<uint64_t>(short_rows_) << 2 |
+                    static_cast<uint64_t>(z_smem_) << 3};
     }
     // algorithmic bytes: one read of the CSR (the operator's data) + u in, u_hat out
     double pass_bytes() const override { return 12.0 * A_->nnz + 8.0 * (m + 1) + 16.0 * m; }
