@@ -622,6 +622,10 @@ def main():
                 "peak_source": peak_src,
                 "lsqr_iteration_gbs": iter_bytes / ph["lsqr_per_iteration"] / 1e9 if ph["lsqr_per_iteration"] else None,
                 "sketch_seconds": float(kt[1]), "sketch_gbs": (8.0 * ml * (ld) + 4.0 * ml * zeta) / kt[1] / 1e9,
+                # SURVEY 8(d)'s second bound for S.[A b]: 16 zeta m n B of shared-memory read-modify-write at the
+                # 37.2 TB/s aggregate shared-memory rate (the scatter formulation; HBM alone would allow 4.98 ms at C3)
+                "sketch_smem_bound_seconds": 16.0 * zeta * ml * (n + 1) / 37.2e12,
+                "sketch_frac_of_smem_bound": (16.0 * zeta * ml * (n + 1) / 37.2e12) / float(kt[1]) if kt[1] else None,
                 "precond_seconds": float(kt[3])}
 
     # e2e through the C-ABI from pinned host buffers (column-major A as the reference's DenseMatrix)
