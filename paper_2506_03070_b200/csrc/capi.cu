@@ -1069,6 +1069,7 @@ int slq_sparse_fill_random(slq_sparse* A, int64_t nnz_per_row, uint64_t seed, co
         slq::generate_sparse_rows_dev(ctx, A->n, nnz_per_row, seed, A->row_begin, A->m, dsc, A->rowptr, A->colidx,
                                       A->vals);
         A->t_valid = false;
+        A->s_valid = false;
     });
 }
 

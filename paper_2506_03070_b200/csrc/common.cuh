@@ -193,6 +193,11 @@ struct slq_sparse {
     bool t_valid = false;
     bool t_pending = false;        // built on a side stream; nobody has waited for it yet
     cudaEvent_t t_ready = nullptr; // recorded after the side-stream build
+    // per-row column-slab segments for the sparse sketch gather ([m][s_S],
+    // sparse.cu slab_ptr_kernel), built on first use, invalidated with the above
+    uint64_t* s_ptr = nullptr;
+    int s_S = 0, s_w = 0;
+    bool s_valid = false;
 };
 
 namespace slq {

@@ -21,7 +21,10 @@
 //        memory (column indices within a row are distinct: no races, no
 //        atomics); the copies are summed in a fixed order at the end.
 #include <algorithm>
+#include <climits>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "lsqr.cuh"
@@ -234,15 +237,19 @@ __global__ void __launch_bounds__(512) sparse_gather_kernel(SGatherArgs g) {
         for (int64_t e = e0; e < e1; e += kSgB) {
             const int nb = (e1 - e < kSgB) ? static_cast<int>(e1 - e) : kSgB;
             // round 1: entries; round 2: row pointers and b (lane q: row q)
-            const uint32_t my_en = lane < nb ? g.sent[e + lane] : 0u;
+            // (lanes >= nb repeat entry nb - 1: their loads are unconditional too)
+            const uint32_t my_en = g.sent[e + (lane < nb ? lane : nb - 1)];
             const int64_t my_k = my_en & 0x7fffffffu;
-            const int64_t my_rb = lane < nb ? g.rowptr[my_k] : 0;
-            const int64_t my_re = lane < nb ? g.rowptr[my_k + 1] : 0;
-            const double my_b = (g.b && lane < nb) ? g.b[my_k] : 0.0;
+            const int64_t my_rb = g.rowptr[my_k];
+            const int64_t my_re = g.rowptr[my_k + 1];
+            const double my_b = g.b ? g.b[my_k] : 0.0;
             // round 3: every row's (column, value) pairs
+            // unconditional loads (slots past a row's end read its first entry, or
+            // entry 0): a predicated load + default move would wait for the load
             int32_t cc[kSgB][2];
             double vv[kSgB][2];
             int64_t rb[kSgB], re[kSgB];
+            unsigned live = 0;
 #pragma unroll
             for (int q = 0; q < kSgB; ++q) {
                 rb[q] = __shfl_sync(0xffffffffu, my_rb, q);
@@ -251,8 +258,10 @@ __global__ void __launch_bounds__(512) sparse_gather_kernel(SGatherArgs g) {
                 for (int h = 0; h < 2; ++h) {
                     const int64_t t = rb[q] + lane + 32 * h;
                     const bool ok = t < re[q];
-                    cc[q][h] = ok ? g.colidx[t] : -1;
-                    vv[q][h] = ok ? g.vals[t] : 0.0;
+                    const int64_t at = ok ? t : rb[q];
+                    cc[q][h] = g.colidx[at];
+                    vv[q][h] = g.vals[at];
+                    live |= static_cast<unsigned>(ok) << (2 * q + h);
                 }
             }
 #pragma unroll
@@ -264,7 +273,7 @@ __global__ void __launch_bounds__(512) sparse_gather_kernel(SGatherArgs g) {
                 // csc_matrix.hpp:133: yj[row] += S_val * akj (two roundings)
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
-                    if (cc[q][h] >= 0) y[cc[q][h]] = __dadd_rn(y[cc[q][h]], __dmul_rn(sv, vv[q][h]));
+                    if (live >> (2 * q + h) & 1u) y[cc[q][h]] = __dadd_rn(y[cc[q][h]], __dmul_rn(sv, vv[q][h]));
                 for (int64_t t = rb[q] + 64 + lane; t < re[q]; t += 32) {  // rows longer than 64
                     const int32_t c = g.colidx[t];
                     y[c] = __dadd_rn(y[c], __dmul_rn(sv, g.vals[t]));
@@ -274,6 +283,247 @@ __global__ void __launch_bounds__(512) sparse_gather_kernel(SGatherArgs g) {
             }
         }
         for (int64_t j = lane; j < n1; j += 32) g.Y[j * g.d + r] = y[j];
+    }
+}
+
+// ------------------------------------------------- K2s column-slab gather
+//
+// The row gather above re-reads each A row from DRAM for most of its zeta
+// target rows: only ~1/4 of the d Y rows fit in shared memory at once, and
+// the resident warps drift apart in k.  Here every Y row is resident at once
+// by splitting Y into S column slabs: CTA c owns Y rows [c d/G, (c+1) d/G)
+// and keeps their slab (w columns) in shared memory; slab q's pass streams
+// the slab's part of each A row -- a contiguous segment of the row, since
+// CSR rows are sorted by column, located by the per-row slab table P (built
+// once per matrix).  The grid walks k in windows of kwin A rows with a soft
+// barrier (a CTA may run `lag` windows ahead of the slowest), so an A row
+// segment comes from DRAM once and from L2 for its other target rows.
+//
+// Same per-element order as the row gather (for Y[r, j]: ascending k), so the
+// same bits.  A warp serves four Y rows at once (8-lane groups), each group
+// walks its row's entries in ascending k in batches of 8 (lane l holds entry
+// l): entries two batches ahead, table lookups one batch ahead, the segment
+// loads of a batch issued before the previous batch is added.
+constexpr int kSlW = 16;      // warps per CTA
+constexpr int kSlB = 8;       // entries per group batch
+
+struct SlabArgs {
+    const uint64_t* P;        // [m][S]: row k's slab-q segment, start | length << 40 (slab_ptr_kernel)
+    const int32_t* colidx;
+    const double* vals;
+    const double* b;          // may be null
+    int64_t n, d, m;
+    int S, w, rmax;           // slab q = columns [q w, min((q + 1) w, n + 1)); column n is b
+    const int64_t* srow_ptr;
+    const uint32_t* sent;
+    double val;
+    double* Y;                // d x (n + 1) column-major
+    int64_t kwin;             // A rows per window
+    int nwin, lag;
+    unsigned* sync;           // zeroed before the launch; one count per warp and window
+};
+
+constexpr int kSlLenShift = 40;
+constexpr uint64_t kSlLoMask = (uint64_t(1) << kSlLenShift) - 1;
+
+// P[k][q]: the entries of row k with columns in slab q (start | length << 40;
+// n < 2^24 and nnz < 2^40, host-checked).  A row whose columns are not
+// ascending gets the whole row for every slab, and the gather filters its
+// entries by column (it always does).  Warp per row.
+__global__ void slab_ptr_kernel(const int64_t* rowptr, const int32_t* colidx, int64_t m, int S, int w, uint64_t* P) {
+    const int lane = threadIdx.x & 31;
+    const int64_t k = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (k >= m) return;
+    const int64_t lo = rowptr[k], hi = rowptr[k + 1];
+    int cnt = 0;           // lane q (1 <= q <= S): entries with column < q w
+    bool sorted = true;
+    int prev = INT_MIN;
+    for (int64_t e0 = lo; e0 < hi; e0 += 32) {
+        const int64_t e = e0 + lane;
+        const int c = e < hi ? colidx[e] : INT_MAX;
+        const int cp = __shfl_up_sync(0xffffffffu, c, 1);
+        const int before = lane == 0 ? prev : cp;
+        if (e < hi && c < before) sorted = false;
+        prev = __shfl_sync(0xffffffffu, c, 31);
+        for (int q = 1; q < S; ++q) {
+            const int t = __popc(__ballot_sync(0xffffffffu, c < q * w));
+            if (lane == q) cnt += t;
+        }
+    }
+    sorted = __all_sync(0xffffffffu, sorted);
+    if (lane == S) cnt = static_cast<int>(hi - lo);
+    const int nxt = __shfl_down_sync(0xffffffffu, cnt, 1);  // lane q: boundary q + 1 (S < 31, host)
+    if (lane < S) {
+        const int64_t b0 = sorted ? lo + cnt : lo, len = sorted ? nxt - cnt : hi - lo;
+        P[k * S + lane] = static_cast<uint64_t>(b0) | static_cast<uint64_t>(len) << kSlLenShift;
+    }
+}
+
+struct SlMeta {         // lane l of a group: entry l of the group's batch
+    uint32_t en;
+    uint64_t pw;          // its slab segment (P word)
+    double b;
+};
+
+struct SlPairs {
+    int32_t c[kSlB][2];
+    double v[kSlB][2];
+    unsigned live;        // bit 2 t + h: slot (t, h) holds an entry of the segment
+};
+
+__device__ __forceinline__ void sl_rows(const SlabArgs& a, int q, bool ok, SlMeta& M) {
+    M.pw = 0;
+    M.b = 0.0;
+    if (ok) {
+        const int64_t k = M.en & 0x7fffffffu;
+        M.pw = a.P[k * a.S + q];
+        if (a.b && q == a.S - 1) M.b = a.b[k];
+    }
+}
+
+// The loads are unconditional (slots past the segment's end read its first
+// entry, or entry 0 -- always allocated) so that nothing here waits on them: a
+// predicated load followed by a default-value move would make the move wait
+// for the load, and predicating the loads alone measured 2x slower.  Liveness
+// goes into a bit mask, applied at use.
+__device__ __forceinline__ void sl_issue(const SlabArgs& a, const SlMeta& M, int g, int gl, SlPairs& B) {
+    B.live = 0;
+#pragma unroll
+    for (int t = 0; t < kSlB; ++t) {
+        const uint64_t pw = __shfl_sync(0xffffffffu, M.pw, g * 8 + t);
+        const int64_t lo = static_cast<int64_t>(pw & kSlLoMask);
+        const int len = static_cast<int>(pw >> kSlLenShift);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int i = gl + 8 * h;
+            const bool ok = i < len;
+            const int64_t at = ok ? lo + i : lo;
+            // plain loads: the segment is re-read from L2 by the row's other target rows
+            B.c[t][h] = a.colidx[at];
+            B.v[t][h] = a.vals[at];
+            B.live |= static_cast<unsigned>(ok) << (2 * t + h);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(32 * kSlW, 1) sparse_gather_slab_kernel(SlabArgs a) {
+    extern __shared__ __align__(16) double ysl[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 3, gl = lane & 7;
+    const int64_t n1 = a.n + 1;
+    const int64_t r0 = blockIdx.x * a.d / gridDim.x, R = (blockIdx.x + 1) * a.d / gridDim.x - r0;
+    int64_t* cur = reinterpret_cast<int64_t*>(ysl + static_cast<int64_t>(a.rmax) * a.w);
+    int64_t* cend = cur + a.rmax;
+    const unsigned WG = gridDim.x * kSlW;  // warps in the grid: each signals every window
+    unsigned t_win = 0;  // global window index (slab-major)
+    for (int q = 0; q < a.S; ++q) {
+        const int64_t c0 = static_cast<int64_t>(q) * a.w, c1 = min(n1, c0 + a.w);
+        const unsigned wq = static_cast<unsigned>(c1 - c0);
+        const bool lastq = q == a.S - 1 && a.b != nullptr;
+        for (int64_t i = tid; i < R * wq; i += blockDim.x) ysl[i] = 0.0;
+        for (int64_t i = tid; i < R; i += blockDim.x) {
+            cur[i] = a.srow_ptr[r0 + i];
+            cend[i] = a.srow_ptr[r0 + i + 1];
+        }
+        __syncthreads();
+        if (warp * 4 >= R) {  // no rows here: count this slab's windows as done
+            if (lane == 0) atomicAdd(a.sync, static_cast<unsigned>(a.nwin));
+            t_win += a.nwin;
+        }
+        for (int win = 0; warp * 4 < R && win < a.nwin; ++win, ++t_win) {
+            if (t_win >= static_cast<unsigned>(a.lag)) {  // soft barrier: every warp done with window t_win - lag
+                if (lane == 0) {
+                    const unsigned target = WG * (t_win - a.lag + 1);
+                    while (*reinterpret_cast<volatile unsigned*>(a.sync) < target) __nanosleep(256);
+                }
+                __syncwarp();
+            }
+            const int64_t kend = min(a.m, (win + 1) * a.kwin);
+            for (int64_t base = warp * 4; base < R; base += kSlW * 4) {
+                const int64_t i = base + g;
+                const bool has = i < R;
+                int64_t e = has ? cur[i] : 0;
+                const int64_t eend = has ? cend[i] : 0;
+                const unsigned ys_row = ptx::smem_u32(ysl) + static_cast<unsigned>((has ? i : 0) * wq) * 8u;
+                const unsigned gmask = 0xffu << (8 * g);
+                // prologue: batch at e (rows + pairs), entries of the batch at e + 8
+                SlMeta Mc, Mn;
+                Mc.en = e + gl < eend ? a.sent[e + gl] : 0u;
+                Mn.en = e + 8 + gl < eend ? a.sent[e + 8 + gl] : 0u;
+                const bool okc = e + gl < eend && (Mc.en & 0x7fffffffu) < kend;
+                int nbc = __popc(__ballot_sync(0xffffffffu, okc) & gmask);
+                sl_rows(a, q, okc, Mc);
+                SlPairs P;
+                sl_issue(a, Mc, g, gl, P);
+                while (__any_sync(0xffffffffu, nbc > 0)) {
+                    // next batch's table lookups (only if this batch is full), entries two ahead
+                    const bool okn = nbc == kSlB && e + 8 + gl < eend && (Mn.en & 0x7fffffffu) < kend;
+                    const int nbn = __popc(__ballot_sync(0xffffffffu, okn) & gmask);
+                    sl_rows(a, q, okn, Mn);
+                    const uint32_t en_nn = nbn == kSlB && e + 16 + gl < eend ? a.sent[e + 16 + gl] : 0u;
+                    const unsigned longm = __ballot_sync(0xffffffffu, (Mc.pw >> kSlLenShift) > 16);
+                    // add this batch in entry order (csc_matrix.hpp:133: yj[row] += S_val * akj);
+                    // branch-free per entry (groups past their batch's end are masked off)
+                    const unsigned actm = P.live & ((1u << (2 * nbc)) - 1u);
+#pragma unroll
+                    for (int t = 0; t < kSlB; ++t) {
+                        const uint32_t en = __shfl_sync(0xffffffffu, Mc.en, g * 8 + t);
+                        const double sv = (en >> 31) ? -a.val : a.val;
+                        {   // the entry's two slots hold distinct columns: both loads before both stores
+                            const unsigned cu0 = static_cast<unsigned>(P.c[t][0] - static_cast<int>(c0));
+                            const unsigned cu1 = static_cast<unsigned>(P.c[t][1] - static_cast<int>(c0));
+                            const bool a0 = (actm >> (2 * t) & 1u) && cu0 < wq;
+                            const bool a1 = (actm >> (2 * t + 1) & 1u) && cu1 < wq;
+                            const unsigned ad0 = ys_row + 8u * cu0, ad1 = ys_row + 8u * cu1;
+                            double y0 = 0.0, y1 = 0.0;
+                            if (a0) y0 = ptx::lds_f64(ad0);
+                            if (a1) y1 = ptx::lds_f64(ad1);
+                            if (a0) ptx::sts_f64(ad0, __dadd_rn(y0, __dmul_rn(sv, P.v[t][0])));
+                            if (a1) ptx::sts_f64(ad1, __dadd_rn(y1, __dmul_rn(sv, P.v[t][1])));
+                        }
+                        if (longm & (0x01010101u << t)) {  // some group's entry t is longer than 16 (warp-uniform)
+                            int len = 0;
+                            int64_t lo = 0;
+                            if ((longm >> (g * 8 + t) & 1u) && t < nbc) {
+                                const uint64_t pw = a.P[static_cast<int64_t>(en & 0x7fffffffu) * a.S + q];
+                                lo = static_cast<int64_t>(pw & kSlLoMask);
+                                len = static_cast<int>(pw >> kSlLenShift);
+                            }
+                            for (int x = 16 + gl; x < len; x += 8) {
+                                const unsigned cu = static_cast<unsigned>(a.colidx[lo + x] - static_cast<int>(c0));
+                                if (cu < wq) {
+                                    const unsigned ad = ys_row + 8u * cu;
+                                    ptx::sts_f64(ad, __dadd_rn(ptx::lds_f64(ad), __dmul_rn(sv, a.vals[lo + x])));
+                                }
+                            }
+                        }
+                        if (lastq) {
+                            const double bt = __shfl_sync(0xffffffffu, Mc.b, g * 8 + t);
+                            if (gl == 0 && t < nbc && bt != 0.0) {
+                                const unsigned ad = ys_row + 8u * static_cast<unsigned>(a.n - c0);
+                                ptx::sts_f64(ad, __dadd_rn(ptx::lds_f64(ad), __dmul_rn(sv, bt)));
+                            }
+                        }
+                        __syncwarp();
+                    }
+                    e += nbc;
+                    sl_issue(a, Mn, g, gl, P);
+                    Mc = Mn;
+                    nbc = nbn;
+                    Mn.en = en_nn;
+                }
+                if (has && gl == 0) cur[i] = e;
+            }
+            __syncwarp();
+            if (lane == 0) atomicAdd(a.sync, 1u);
+        }
+        __syncthreads();
+        // slab -> Y (column-major; consecutive threads take consecutive rows)
+        for (int64_t x = tid; x < R * wq; x += blockDim.x) {
+            const int64_t i = x % R, j = x / R;
+            a.Y[(c0 + j) * a.d + r0 + i] = ysl[i * wq + j];
+        }
+        __syncthreads();
     }
 }
 
@@ -946,6 +1196,9 @@ void sparse_free(slq_sparse* A) {
     cudaFree(A->t_cval);
     cudaFree(A->t_uscr);
     cudaFree(A->t_col16);
+    cudaFree(A->s_ptr);
+    A->s_ptr = nullptr;
+    A->s_valid = false;
     if (A->t_ready) cudaEventDestroy(A->t_ready);
     A->t_ready = nullptr;
     A->t_col16 = nullptr;
@@ -1042,7 +1295,64 @@ void sketch_apply_sparse_compact_dev(slq_ctx* ctx, const slq_sparse* A, int64_t 
                                               cc.plan.K, d, srow_ptr, sent);
     SLQ_LAUNCH_CHECK(ctx);
     check_chunk_csr(ctx, cc);
-    // gather: one warp per Y row, rows of n+1 doubles in shared memory
+    // column-slab gather (every Y row resident) unless the geometry rules it out
+    const int G = ctx->num_sms;
+    const int64_t rmax = ceil_div(d, static_cast<int64_t>(G));
+    const int64_t budget = 200 * 1024 - 16 * rmax;
+    int64_t w = budget > 0 ? budget / (8 * rmax) : 0;
+    int S = w > 0 ? static_cast<int>(ceil_div(n + 1, w)) : 0;
+    // diagnostics / tests: SLQ_K2S=row selects the row gather, SLQ_K2S_W caps the
+    // slab width (more slabs at small sizes), SLQ_K2S_KWIN / SLQ_K2S_LAG the pacing
+    const char* mode = std::getenv("SLQ_K2S");
+    if (const char* e = std::getenv("SLQ_K2S_W")) {
+        w = std::min<int64_t>(w, std::max<int64_t>(32, std::atoll(e)));
+        S = w > 0 ? static_cast<int>(ceil_div(n + 1, w)) : 0;
+    }
+    if (w >= 32 && S >= 1 && S < 31 && n < (int64_t(1) << 24) && A->nnz < (int64_t(1) << kSlLenShift) &&
+        !(mode && std::string(mode) == "row")) {
+        w = ceil_div(n + 1, static_cast<int64_t>(S));  // balanced slabs
+        slq_sparse* Am = const_cast<slq_sparse*>(A);     // the slab table is a cached derived layout
+        if (!Am->s_valid || Am->s_S != S || Am->s_w != w) {
+            if (!Am->s_ptr || Am->s_S != S) {
+                if (Am->s_ptr) SLQ_CUDA_CHECK(cudaFree(Am->s_ptr));
+                Am->s_ptr = nullptr;
+                SLQ_CUDA_CHECK(cudaMalloc(&Am->s_ptr, sizeof(uint64_t) * m * S));
+            }
+            slab_ptr_kernel<<<static_cast<unsigned>(ceil_div(m * 32, 256)), 256, 0, ctx->stream>>>(
+                A->rowptr, A->colidx, m, S, static_cast<int>(w), Am->s_ptr);
+            SLQ_LAUNCH_CHECK(ctx);
+            Am->s_S = S;
+            Am->s_w = static_cast<int>(w);
+            Am->s_valid = true;
+        }
+        const int64_t kwin_env = std::getenv("SLQ_K2S_KWIN") ? std::atoll(std::getenv("SLQ_K2S_KWIN")) : 0;
+        const int lag_env = std::getenv("SLQ_K2S_LAG") ? std::atoi(std::getenv("SLQ_K2S_LAG")) : 0;
+        const int64_t kwin = kwin_env > 0 ? kwin_env : (int64_t(1) << 18);
+        const int nwin = static_cast<int>(ceil_div(m, kwin));
+        const int lag = lag_env > 0 ? lag_env : 2;
+        unsigned* sync = static_cast<unsigned*>(ws.flags.ensure(4096)) + 32;  // [32]: this kernel's counter
+        SLQ_CUDA_CHECK(cudaMemsetAsync(sync, 0, sizeof(unsigned), ctx->stream));
+        const size_t smem = sizeof(double) * rmax * w + 2 * sizeof(int64_t) * rmax;
+        SLQ_CUDA_CHECK(cudaFuncSetAttribute(sparse_gather_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smem)));
+        SlabArgs sa{A->s_ptr, A->colidx, A->vals, A->b, n, d, m, S, static_cast<int>(w), static_cast<int>(rmax),
+                    srow_ptr, sent, val, Y, kwin, nwin, lag, sync};
+        void* args[] = {&sa};
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(G));
+        cfg.blockDim = dim3(32 * kSlW);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;  // the soft barrier needs every CTA resident
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        SLQ_CUDA_CHECK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(sparse_gather_slab_kernel), args));
+        SLQ_LAUNCH_CHECK(ctx);
+        return;
+    }
+    // row gather: one warp per Y row, rows of n+1 doubles in shared memory
     const int64_t row_bytes = (n + 1) * static_cast<int64_t>(sizeof(double));
     int warps = static_cast<int>(std::min<int64_t>(16, (200 * 1024) / row_bytes));
     if (warps < 1) fail(SLQ_UNSUPPORTED, "sparse sketch_apply: n too large for a shared-memory row");

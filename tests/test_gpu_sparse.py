@@ -219,3 +219,84 @@ def test_sparse_two_pass_wide_n(m, n, dens):
     assert rep.iterations == repo.iterations == 5
     assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
     assert np.allclose(rep.residual_estimate, repo.residual_estimate, rtol=1e-9)
+
+
+# ----------------------------------------------- K2s column-slab gather
+
+
+def _sketch_vs_oracle(Acsc, b, d, zeta, seed):
+    Yo, Sbo = C.sketch_apply_csc(d, zeta, seed, Acsc.rows, Acsc.cols, Acsc.row_indices, Acsc.values,
+                                 Acsc.col_pointers, b)
+    dm = slq.SparseDeviceMatrix.from_csc(Acsc, b)
+    Yd, Sbd = dm.sketch(d, zeta, seed)
+    dm.free()
+    return np.array_equal(Yd, Yo) and np.array_equal(Sbd, Sbo)
+
+
+@pytest.mark.parametrize("wcap,kwin,lag", [(None, None, None), ("32", None, None), ("48", "512", "1"),
+                                           ("100", "700", "3"), ("32", "64", "1")])
+def test_sparse_apply_slab_gather(monkeypatch, wcap, kwin, lag):
+    """S [A b] through the column-slab gather (every Y row resident, A walked in
+    k windows under a soft grid barrier): bit-exact against the oracle's
+    spmm(csc, csc) for slab widths down to 32 columns (segments longer than one
+    group pass come from the long rows), several windows and lags, and the row
+    gather (SLQ_K2S=row) on the same matrix."""
+    for k, v in (("SLQ_K2S_W", wcap), ("SLQ_K2S_KWIN", kwin), ("SLQ_K2S_LAG", lag)):
+        if v is not None:
+            monkeypatch.setenv(k, v)
+    Acsc, A = rand_csc(5000, 150, 0.1, 21, long_rows=4, empty_rows=3)
+    b = np.random.default_rng(3).standard_normal(5000)
+    assert _sketch_vs_oracle(Acsc, b, 600, 8, 19)
+    monkeypatch.setenv("SLQ_K2S", "row")
+    assert _sketch_vs_oracle(Acsc, b, 600, 8, 19)
+
+
+def test_sparse_apply_slab_gather_two_slabs_natural():
+    """d large enough that the Y rows of one CTA fill its shared memory: the
+    slab count comes out > 1 without any override (d = 9000 on 148 SMs ->
+    61 rows per CTA, ~417-column slabs for n + 1 = 601)."""
+    Acsc, A = rand_csc(30_000, 600, 0.015, 8, long_rows=2, empty_rows=1)
+    b = np.random.default_rng(5).standard_normal(30_000)
+    assert _sketch_vs_oracle(Acsc, b, 9000, 4, 23)
+
+
+def _cudart():
+    import ctypes as ct
+    import os
+
+    import nvidia.cuda_runtime as cr
+    lib = ct.CDLL(os.path.join(list(cr.__path__)[0], "lib", "libcudart.so.12"))
+    lib.cudaMemcpy.argtypes = [ct.c_void_p, ct.c_void_p, ct.c_size_t, ct.c_int]
+    return lib
+
+
+def test_sparse_apply_slab_gather_unsorted_rows(monkeypatch):
+    """A CSR written in place (slq_sparse_create_csr) whose rows are NOT sorted by
+    column: the slab table marks those rows and the gather filters their
+    entries by column -- still bit-exact (the per-element order is ascending
+    k, whatever the order inside a row)."""
+    m, n, d, zeta = 3000, 120, 500, 8
+    Acsc, A = rand_csc(m, n, 0.08, 41, long_rows=2)
+    R = A.tocsr()
+    rng = np.random.default_rng(9)
+    cols, vals = R.indices.astype(np.int32).copy(), R.data.copy()
+    for r in range(0, m, 3):  # every third row shuffled
+        lo, hi = R.indptr[r], R.indptr[r + 1]
+        p = rng.permutation(hi - lo)
+        cols[lo:hi], vals[lo:hi] = cols[lo:hi][p], vals[lo:hi][p]
+    b = rng.standard_normal(m)
+    dm, (rp, ci, vl, bp) = slq.SparseDeviceMatrix.create_csr(m, n, R.nnz)
+    cu = _cudart()
+    H2D = 1
+    rowptr = R.indptr.astype(np.int64)
+    for dst, src in ((rp, rowptr), (ci, cols), (vl, vals), (bp, b)):
+        assert cu.cudaMemcpy(dst, src.ctypes.data, src.nbytes, H2D) == 0
+    Yo, Sbo = C.sketch_apply_csc(d, zeta, 13, m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, b)
+    for wcap in ("32", "64", None):
+        if wcap:
+            monkeypatch.setenv("SLQ_K2S_W", wcap)
+        else:
+            monkeypatch.delenv("SLQ_K2S_W", raising=False)
+        Yd, Sbd = dm.sketch(d, zeta, 13)
+        assert np.array_equal(Yd, Yo) and np.array_equal(Sbd, Sbo)
+    dm.free()

@@ -1,0 +1,14 @@
+#!/bin/bash
+mkdir -p gpurun_out
+run() {  # tag, env...
+  local tag=$1; shift
+  env "$@" timeout 300 python bench.py --config c4 --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/k2s_$tag.jsonl 2>gpurun_out/k2s_$tag.err
+  python -c "
+import json; d=json.loads(open('gpurun_out/k2s_$tag.jsonl').read().strip().splitlines()[-1]); print('$tag', round(d['value'],4), 'apply', round(d['phases_s']['apply']*1e3,2), 'ms', d['clocks']['reasons'])" || tail -3 gpurun_out/k2s_$tag.err
+}
+run slab
+run kw16 SLQ_K2S_KWIN=65536
+run kw15 SLQ_K2S_KWIN=32768
+run nolag SLQ_K2S_LAG=100000
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"sparse_gather_slab" -c 1 -o gpurun_out/k2slab2_full python bench.py --config c4 --steps 1 --warmup 3 --no-cpu --no-e2e --iters 4 > gpurun_out/ncu_k2slab2.log 2>&1
+ncu -i gpurun_out/k2slab2_full.ncu-rep --page raw --csv > gpurun_out/k2slab2_raw.csv 2>&1
