@@ -1378,9 +1378,14 @@ public:
         // (+ z when it fits; 1 KB left for static shared memory); else the single
         // fused pass with p + one z copy per warp in shared memory
         const int64_t smax = 226 * 1024;
-        big_ring_ = static_cast<int64_t>(UpG::kStage) * UpG::kStages + zrow <= smax;
-        const int64_t ring = big_ring_ ? static_cast<int64_t>(UpG::kStage) * UpG::kStages
-                                       : static_cast<int64_t>(UpS::kStage) * UpS::kStages;
+        // ring: 2 = three tight 128-row stages (rows of <= 50 entries on average:
+        // a third chunk in flight), 1 = two 128-row stages, 0 = two 64-row stages (wide p)
+        const int64_t ringT = static_cast<int64_t>(UpT::kStage) * UpT::kStages;
+        const int64_t ringG = static_cast<int64_t>(UpG::kStage) * UpG::kStages;
+        const int64_t ringS = static_cast<int64_t>(UpS::kStage) * UpS::kStages;
+        ring_ = ringT + zrow <= smax && A->nnz <= 50 * m ? 2 : ringG + zrow <= smax ? 1 : 0;
+        if (const char* e = std::getenv("SLQ_UPASS_GEOM")) ring_ = std::min(ring_, std::atoi(e));  // diagnostics
+        const int64_t ring = ring_ == 2 ? ringT : ring_ == 1 ? ringG : ringS;
         two_ = two_pass && slq_env_flag("SLQ_SPARSE_ONEPASS") == false &&
                static_cast<int64_t>(kTbRows) * 8 + 4 * (n + 8) <= smax && ring + zrow <= smax && n < 65536 && m > 0 &&
                A->nnz > 0;
@@ -1398,10 +1403,12 @@ public:
             // 200 entries: 2.80 vs 2.97 ms with 8 lanes)
             short_rows_ = A->nnz <= 100 * m;
             if (const char* e = std::getenv("SLQ_UPASS_LPR")) short_rows_ = std::atoi(e) == 4;  // diagnostics
-            const void* kfn = big_ring_ ? (short_rows_ ? reinterpret_cast<const void*>(sparse_upass_kernel<UpG, 4>)
-                                                       : reinterpret_cast<const void*>(sparse_upass_kernel<UpG, 8>))
-                                        : (short_rows_ ? reinterpret_cast<const void*>(sparse_upass_kernel<UpS, 4>)
-                                                       : reinterpret_cast<const void*>(sparse_upass_kernel<UpS, 8>));
+            const void* kfn = ring_ == 2 ? (short_rows_ ? reinterpret_cast<const void*>(sparse_upass_kernel<UpT, 4>)
+                                                        : reinterpret_cast<const void*>(sparse_upass_kernel<UpT, 8>))
+                              : ring_ == 1 ? (short_rows_ ? reinterpret_cast<const void*>(sparse_upass_kernel<UpG, 4>)
+                                                          : reinterpret_cast<const void*>(sparse_upass_kernel<UpG, 8>))
+                                           : (short_rows_ ? reinterpret_cast<const void*>(sparse_upass_kernel<UpS, 4>)
+                                                          : reinterpret_cast<const void*>(sparse_upass_kernel<UpS, 8>));
             SLQ_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
             tsmem_ = static_cast<size_t>(kTbRows) * 8 + static_cast<size_t>(n + 8) * 4;
             z_smem_ = static_cast<int64_t>(tsmem_) + zrow + 32 <= smax;
@@ -1438,7 +1445,10 @@ public:
         double* uo = c.u_out ? c.u_out : us_;
         UPassArgs ua{A_->rowptr, col16_, A_->vals, A_->b, m, n, c.p, c.u_in, uo, c.coef, c.c_fixed, c.part, c.skip};
         const dim3 ub(32 * (kUpConsumers + 1));
-        if (big_ring_) {
+        if (ring_ == 2) {
+            if (short_rows_) sparse_upass_kernel<UpT, 4><<<grid_, ub, smem_, ctx->stream>>>(ua);
+            else sparse_upass_kernel<UpT, 8><<<grid_, ub, smem_, ctx->stream>>>(ua);
+        } else if (ring_ == 1) {
             if (short_rows_) sparse_upass_kernel<UpG, 4><<<grid_, ub, smem_, ctx->stream>>>(ua);
             else sparse_upass_kernel<UpG, 8><<<grid_, ub, smem_, ctx->stream>>>(ua);
         } else {
@@ -1456,8 +1466,8 @@ public:
                 static_cast<uint64_t>(n), static_cast<uint64_t>(W_), static_cast<uint64_t>(grid_),
                 reinterpret_cast<uint64_t>(crow_), reinterpret_cast<uint64_t>(cval_), reinterpret_cast<uint64_t>(blkcol_),
                 reinterpret_cast<uint64_t>(us_), reinterpret_cast<uint64_t>(col16_),
-                static_cast<uint64_t>(two_) | static_cast<uint64_t>(big_ring_) << 1 | static_cast<uint64_t>(short_rows_) << 2 |
-                    static_cast<uint64_t>(z_smem_) << 3};
+                static_cast<uint64_t>(two_) | static_cast<uint64_t>(ring_) << 1 | static_cast<uint64_t>(short_rows_) << 3 |
+                    static_cast<uint64_t>(z_smem_) << 4};
     }
     // algorithmic bytes: one read of the CSR (the operator's data) + u in, u_hat out
     double pass_bytes() const override { return 12.0 * A_->nnz + 8.0 * (m + 1) + 16.0 * m; }
@@ -1473,8 +1483,9 @@ private:
     // 128-row chunks, two 84 KB stages: measured against 64 x 4, 96 x 3 and
     // 160 x 2 at C4 (1.6 ms vs 2.05 / 1.9 / 1.7 ms for the u_hat pass)
     using UpG = UpGeom<128, 8192, 2>;
+    using UpT = UpGeom<128, 6656, 3>;  // <= 52 entries per row fit a stage
     using UpS = UpGeom<64, 4096, 2>;  // wide p (n > ~7900): a smaller ring
-    bool big_ring_ = true;
+    int ring_ = 1;
     bool z_smem_ = true;
     bool short_rows_ = false;
     uint32_t* blkcol_ = nullptr;
