@@ -557,14 +557,6 @@ struct UpdArgs {
     int transT;              // 1: C -= V T^T V^T C (apply H_{kb-1}..H_0); 0: C -= V T V^T C
 };
 
-// V(r, a) with the implicit unit diagonal / zero upper part.
-__device__ __forceinline__ double vget(const UpdArgs& u, int64_t r, int a) {
-    if (a >= u.kb || r >= u.r_end) return 0.0;
-    const int64_t g = u.k0 + a;
-    if (r < g) return 0.0;
-    if (r == g) return 1.0;
-    return u.V[(u.k0 + a) * u.ldv + r];
-}
 
 // Tiles of the trailing update: RB rows x CB columns per CTA.  Two kernels
 // per panel: U1 forms per-row-block partials of W = V^T C, U2 sums them (fixed
@@ -575,20 +567,38 @@ constexpr int kCB = 32;
 constexpr int kLdT = kRB + 4;  // smem leading dimension (doubles): conflict-free fragments
 constexpr int kWChunks = 1;    // row blocks per update_w CTA (more serialises the narrow update)
 
-// Stage V rows [r0, r0+kRB) (implicit unit diagonal / zero upper part) as Vs[a][i]
-__device__ __forceinline__ void stage_v(const UpdArgs& u, int64_t r0, double* Vs) {
-    for (int e = threadIdx.x; e < kNbMax * kRB; e += blockDim.x) {
-        const int a = e / kRB, i = e % kRB;
-        Vs[a * kLdT + i] = vget(u, r0 + i, a);
-    }
-}
-
-// Stage C rows [r0, r0+kRB) x columns [c0, c0+kCB) as Cs[c][i]
-__device__ __forceinline__ void stage_c(const UpdArgs& u, int64_t r0, int64_t c0, double* Cs) {
-    for (int e = threadIdx.x; e < kCB * kRB; e += blockDim.x) {
-        const int c = e / kRB, i = e % kRB;
-        const int64_t r = r0 + i, cc = c0 + c;
-        Cs[c * kLdT + i] = (r < u.r_end && cc < u.c_end) ? u.C[cc * u.ldc + r] : 0.0;
+// Stage V rows [r0, r0 + RB) (implicit unit diagonal / zero upper part) as
+// Vs[a][i] and C rows [r0, r0 + RB) x columns [c0, c0 + kCB) as Cs[c][i] (row
+// stride LD), rows >= rend as zeros.  Every thread issues all of its loads
+// (clamped to valid addresses) before the first store, so a stage costs one
+// memory latency instead of one per element; validity is applied afterwards.
+template <int RB, int LD, int NT, int ROUNDS = 1>
+__device__ __forceinline__ void stage_vc(const UpdArgs& u, int64_t r0, int64_t rend, int64_t c0, double* Vs,
+                                         double* Cs) {
+    static_assert(kNbMax == kCB && (kNbMax * RB) % (NT * ROUNDS) == 0, "tile shape");
+    constexpr int kPer = kNbMax * RB / (NT * ROUNDS);     // loads of each kind in flight per thread
+    const int tid = threadIdx.x;
+    const int64_t rlast = rend - 1;                        // callers stage only when rend > r0
+    const int acl = u.kb - 1;                              // clamp for panel columns past kb
+    const int64_t ccl = u.c_end - 1;
+#pragma unroll
+    for (int rd = 0; rd < ROUNDS; ++rd) {
+        double rv[kPer], rc[kPer];
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+            const int e = tid + (rd * kPer + t) * NT, a = e / RB, i = e % RB;
+            const int64_t r = min(r0 + i, rlast);
+            rv[t] = u.V[(u.k0 + min(a, acl)) * u.ldv + r];
+            rc[t] = ccl >= c0 ? u.C[min(c0 + a, ccl) * u.ldc + r] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+            const int e = tid + (rd * kPer + t) * NT, a = e / RB, i = e % RB;
+            const int64_t r = r0 + i, g = u.k0 + a;
+            const bool in = r < rend;
+            Vs[a * LD + i] = (!in || a >= u.kb || r < g) ? 0.0 : r == g ? 1.0 : rv[t];
+            Cs[a * LD + i] = (in && c0 + a <= ccl) ? rc[t] : 0.0;
+        }
     }
 }
 
@@ -610,8 +620,7 @@ __global__ void __launch_bounds__(256) update_w_kernel(UpdArgs u, double* Wpart,
         const int64_t r0 = u.k0 + (static_cast<int64_t>(blockIdx.y) * kWChunks + ch) * kRB;
         if (r0 >= u.r_end) break;
         if (ch) __syncthreads();
-        stage_v(u, r0, Vs);
-        stage_c(u, r0, c0, Cs);
+        stage_vc<kRB, kLdT, 256>(u, r0, u.r_end, c0, Vs, Cs);
         __syncthreads();
 #pragma unroll 8
         for (int ks = 0; ks < kRB / 4; ++ks) {
@@ -687,8 +696,7 @@ __global__ void __launch_bounds__(256) update_apply_kernel(UpdArgs u, const doub
     const int64_t c0 = u.c_begin + static_cast<int64_t>(blockIdx.x) * kCB;
     const double* w2 = W2g + static_cast<int64_t>(blockIdx.x) * (kNbMax * kCB);
     for (int e = tid; e < kNbMax * kCB; e += 256) W2[(e / kCB) * (kCB + 1) + e % kCB] = w2[e];
-    stage_v(u, r0, Vs);
-    stage_c(u, r0, c0, Cs);
+    stage_vc<kRB, kLdT, 256>(u, r0, u.r_end, c0, Vs, Cs);
     __syncthreads();
     // output tiles: (kRB/8) x (kCB/8) = 16 x 4 = 64; warp w owns 8 (two row tiles x four c tiles)
 #pragma unroll
@@ -750,19 +758,7 @@ __global__ void __launch_bounds__(kNThreads) narrow_update_kernel(UpdArgs u, int
     const int64_t nrows = rend > rbeg ? rend - rbeg : 0;
     const int nch = static_cast<int>((nrows + kNRB - 1) / kNRB);
     const int64_t c0 = u.c_begin;
-    auto stage = [&](int64_t r0) {
-        for (int e = tid; e < kNbMax * kNRB; e += kNThreads) {
-            const int a = e / kNRB, i = e % kNRB;
-            const int64_t r = r0 + i;
-            double v = 0.0, c = 0.0;
-            if (r < rend) {
-                v = vget(u, r, a);
-                if (c0 + a < u.c_end) c = u.C[(c0 + a) * u.ldc + r];
-            }
-            Vs[a * kNLd + i] = v;
-            Cs[a * kNLd + i] = c;
-        }
-    };
+    auto stage = [&](int64_t r0) { stage_vc<kNRB, kNLd, kNThreads, 2>(u, r0, rend, c0, Vs, Cs); };
     for (int e = tid; e < kNbMax * kNbMax; e += kNThreads) Ts[(e % kNbMax) * (kNbMax + 1) + e / kNbMax] = u.T[e];
     // phase 1: Wp = V^T C over this CTA's rows (16 8x8 tiles, one per warp)
     double acc0 = 0.0, acc1 = 0.0;
