@@ -116,6 +116,7 @@ struct Workspace {
     DevBuf xbuf;         // solution vector
     DevBuf tmp;
     DevBuf host_A;       // device copy of A for slq_solve_host (kept across calls)
+    DevBuf st_ptr, st_cnt, st_scan;  // sparse sketch: S^T row pointers, counts, scan scratch
 };
 
 }  // namespace slq

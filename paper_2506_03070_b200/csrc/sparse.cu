@@ -1276,25 +1276,28 @@ void sketch_apply_sparse_compact_dev(slq_ctx* ctx, const slq_sparse* A, int64_t 
         SLQ_CUDA_CHECK(cudaMemsetAsync(Y, 0, sizeof(double) * d * (n + 1), ctx->stream));
         return;
     }
-    ChunkCsr cc = build_chunk_csr(ctx, compact, colptr_dev, zeta_max, m, d, 0);
     // S^T rows (entries of each Y row in ascending k)
-    DevBuf srp, scan_tmp;
-    int64_t* srow_ptr = static_cast<int64_t*>(srp.ensure(sizeof(int64_t) * (d + 1)));
-    const unsigned wgrid = static_cast<unsigned>(ceil_div(d * 32, 256));
-    srow_count<<<wgrid, 256, 0, ctx->stream>>>(cc.ptr, cc.plan.ptr_stride, cc.plan.nchunks, d, srow_ptr);
-    SLQ_LAUNCH_CHECK(ctx);
-    DevBuf cnt_copy;
-    int64_t* cnt = static_cast<int64_t*>(cnt_copy.ensure(sizeof(int64_t) * (d + 1)));
-    SLQ_CUDA_CHECK(cudaMemcpyAsync(cnt, srow_ptr, sizeof(int64_t) * d, cudaMemcpyDeviceToDevice, ctx->stream));
-    exclusive_scan(ctx, cnt, d, srow_ptr, scan_tmp);
-    set_total_kernel<<<1, 32, 0, ctx->stream>>>(cnt, d, srow_ptr);
-    SLQ_LAUNCH_CHECK(ctx);
-    const int64_t nnz_s = static_cast<int64_t>(cc.plan.ent_stride) * cc.plan.nchunks;  // >= entries of S
-    uint32_t* sent = static_cast<uint32_t*>(ws.ypart.ensure(sizeof(uint32_t) * nnz_s));
-    srow_fill<<<wgrid, 256, 0, ctx->stream>>>(cc.ptr, cc.ent, cc.plan.ptr_stride, cc.plan.ent_stride, cc.plan.nchunks,
-                                              cc.plan.K, d, srow_ptr, sent);
-    SLQ_LAUNCH_CHECK(ctx);
-    check_chunk_csr(ctx, cc);
+    // workspace buffers (grow-only): a local DevBuf's cudaFree would wait for the device
+    DevBuf& scan_tmp = ws.st_scan;
+    int64_t* srow_ptr = static_cast<int64_t*>(ws.st_ptr.ensure(sizeof(int64_t) * (d + 1)));
+    int64_t* cnt = static_cast<int64_t*>(ws.st_cnt.ensure(sizeof(int64_t) * (d + 1)));
+    uint32_t* sent = nullptr;
+    {
+        ChunkCsr cc = build_chunk_csr(ctx, compact, colptr_dev, zeta_max, m, d, 0);
+        const unsigned wgrid = static_cast<unsigned>(ceil_div(d * 32, 256));
+        srow_count<<<wgrid, 256, 0, ctx->stream>>>(cc.ptr, cc.plan.ptr_stride, cc.plan.nchunks, d, srow_ptr);
+        SLQ_LAUNCH_CHECK(ctx);
+        SLQ_CUDA_CHECK(cudaMemcpyAsync(cnt, srow_ptr, sizeof(int64_t) * d, cudaMemcpyDeviceToDevice, ctx->stream));
+        exclusive_scan(ctx, cnt, d, srow_ptr, scan_tmp);
+        set_total_kernel<<<1, 32, 0, ctx->stream>>>(cnt, d, srow_ptr);
+        SLQ_LAUNCH_CHECK(ctx);
+        const int64_t nnz_s = static_cast<int64_t>(cc.plan.ent_stride) * cc.plan.nchunks;  // >= entries of S
+        sent = static_cast<uint32_t*>(ws.ypart.ensure(sizeof(uint32_t) * nnz_s));
+        srow_fill<<<wgrid, 256, 0, ctx->stream>>>(cc.ptr, cc.ent, cc.plan.ptr_stride, cc.plan.ent_stride,
+                                                  cc.plan.nchunks, cc.plan.K, d, srow_ptr, sent);
+        SLQ_LAUNCH_CHECK(ctx);
+        check_chunk_csr(ctx, cc);
+    }
     // column-slab gather (every Y row resident) unless the geometry rules it out
     const int G = ctx->num_sms;
     const int64_t rmax = ceil_div(d, static_cast<int64_t>(G));

@@ -300,3 +300,14 @@ def test_sparse_apply_slab_gather_unsorted_rows(monkeypatch):
         Yd, Sbd = dm.sketch(d, zeta, 13)
         assert np.array_equal(Yd, Yo) and np.array_equal(Sbd, Sbo)
     dm.free()
+
+
+@pytest.mark.parametrize("d,zeta", [(600, 8), (20_000, 3), (64, 1)])
+def test_sparse_apply_wide_and_narrow_sketches(d, zeta):
+    """S [A b] bit-exact against the oracle for a sketch far taller than one
+    CTA's shared memory holds per row set (d = 20000: 136 rows per CTA, slabs
+    of ~180 columns) and for zeta = 1."""
+    m = 25_000 if d > 1000 else 5000
+    Acsc, A = rand_csc(m, 90, 0.05, d + zeta, long_rows=2, empty_rows=2)
+    b = np.random.default_rng(d).standard_normal(m)
+    assert _sketch_vs_oracle(Acsc, b, d, zeta, 31)
