@@ -1080,6 +1080,7 @@ int slq_sparse_prepare(slq_ctx* ctx, slq_sparse* A) {
         if (A->t_pending) SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, A->t_ready, 0));
         A->t_pending = false;
         A->t_valid = false;
+        A->s_valid = false;  // slab tables of the sketch gather: rebuilt on next use
         slq::prepare_two_pass(ctx, A);
         SLQ_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     });

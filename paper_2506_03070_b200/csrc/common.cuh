@@ -194,10 +194,19 @@ struct slq_sparse {
     bool t_valid = false;
     bool t_pending = false;        // built on a side stream; nobody has waited for it yet
     cudaEvent_t t_ready = nullptr; // recorded after the side-stream build
-    // per-row column-slab segments for the sparse sketch gather ([m][s_S],
-    // sparse.cu slab_ptr_kernel), built on first use, invalidated with the above
-    uint64_t* s_ptr = nullptr;
-    int s_S = 0, s_w = 0;
+    // per-row column-slab segments for the sparse sketch gather ([m][S] per
+    // slab geometry (S slabs of w columns), sparse.cu slab_ptr_kernel): built on
+    // first use of a geometry and then immutable (a sketch of another d on
+    // another stream gets its own table; `ready` orders the build before every
+    // use); dropped when the CSR is rewritten (s_valid = false)
+    struct SlabTable {
+        uint64_t* p = nullptr;
+        int S = 0, w = 0;
+        cudaEvent_t ready = nullptr;
+    };
+    static constexpr int kSlabTables = 4;
+    SlabTable s_tab[kSlabTables];
+    int s_ntab = 0;
     bool s_valid = false;
 };
 

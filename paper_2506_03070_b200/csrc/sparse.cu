@@ -1184,6 +1184,16 @@ void sparse_alloc(slq_ctx* ctx, slq_sparse* A, bool with_b) {
     }
 }
 
+void drop_slab_tables(slq_sparse* A) {
+    for (int i = 0; i < A->s_ntab; ++i) {
+        cudaFree(A->s_tab[i].p);
+        if (A->s_tab[i].ready) cudaEventDestroy(A->s_tab[i].ready);
+        A->s_tab[i] = slq_sparse::SlabTable{};
+    }
+    A->s_ntab = 0;
+    A->s_valid = false;
+}
+
 void sparse_free(slq_sparse* A) {
     if (A->owned) {
         cudaFree(A->rowptr);
@@ -1196,9 +1206,7 @@ void sparse_free(slq_sparse* A) {
     cudaFree(A->t_cval);
     cudaFree(A->t_uscr);
     cudaFree(A->t_col16);
-    cudaFree(A->s_ptr);
-    A->s_ptr = nullptr;
-    A->s_valid = false;
+    drop_slab_tables(A);
     if (A->t_ready) cudaEventDestroy(A->t_ready);
     A->t_ready = nullptr;
     A->t_col16 = nullptr;
@@ -1315,19 +1323,36 @@ void sketch_apply_sparse_compact_dev(slq_ctx* ctx, const slq_sparse* A, int64_t 
         !(mode && std::string(mode) == "row")) {
         w = ceil_div(n + 1, static_cast<int64_t>(S));  // balanced slabs
         slq_sparse* Am = const_cast<slq_sparse*>(A);     // the slab table is a cached derived layout
-        if (!Am->s_valid || Am->s_S != S || Am->s_w != w) {
-            if (!Am->s_ptr || Am->s_S != S) {
-                if (Am->s_ptr) SLQ_CUDA_CHECK(cudaFree(Am->s_ptr));
-                Am->s_ptr = nullptr;
-                SLQ_CUDA_CHECK(cudaMalloc(&Am->s_ptr, sizeof(uint64_t) * m * S));
+        if (!Am->s_valid) {  // the CSR was (re)written: every table is stale
+            if (Am->s_ntab) {
+                SLQ_CUDA_CHECK(cudaDeviceSynchronize());
+                drop_slab_tables(Am);
             }
-            slab_ptr_kernel<<<static_cast<unsigned>(ceil_div(m * 32, 256)), 256, 0, ctx->stream>>>(
-                A->rowptr, A->colidx, m, S, static_cast<int>(w), Am->s_ptr);
-            SLQ_LAUNCH_CHECK(ctx);
-            Am->s_S = S;
-            Am->s_w = static_cast<int>(w);
             Am->s_valid = true;
         }
+        slq_sparse::SlabTable* tab = nullptr;
+        for (int i = 0; i < Am->s_ntab; ++i)
+            if (Am->s_tab[i].S == S && Am->s_tab[i].w == w) tab = &Am->s_tab[i];
+        if (!tab) {
+            if (Am->s_ntab == slq_sparse::kSlabTables) {  // rare: retire the oldest geometry
+                SLQ_CUDA_CHECK(cudaDeviceSynchronize());
+                cudaFree(Am->s_tab[0].p);
+                cudaEventDestroy(Am->s_tab[0].ready);
+                for (int i = 1; i < Am->s_ntab; ++i) Am->s_tab[i - 1] = Am->s_tab[i];
+                Am->s_tab[--Am->s_ntab] = slq_sparse::SlabTable{};
+            }
+            tab = &Am->s_tab[Am->s_ntab];
+            SLQ_CUDA_CHECK(cudaMalloc(&tab->p, sizeof(uint64_t) * m * S));
+            SLQ_CUDA_CHECK(cudaEventCreateWithFlags(&tab->ready, cudaEventDisableTiming));
+            slab_ptr_kernel<<<static_cast<unsigned>(ceil_div(m * 32, 256)), 256, 0, ctx->stream>>>(
+                A->rowptr, A->colidx, m, S, static_cast<int>(w), tab->p);
+            SLQ_LAUNCH_CHECK(ctx);
+            SLQ_CUDA_CHECK(cudaEventRecord(tab->ready, ctx->stream));
+            tab->S = S;
+            tab->w = static_cast<int>(w);
+            ++Am->s_ntab;
+        }
+        SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, tab->ready, 0));  // built on another stream, maybe
         const int64_t kwin_env = std::getenv("SLQ_K2S_KWIN") ? std::atoll(std::getenv("SLQ_K2S_KWIN")) : 0;
         const int lag_env = std::getenv("SLQ_K2S_LAG") ? std::atoi(std::getenv("SLQ_K2S_LAG")) : 0;
         const int64_t kwin = kwin_env > 0 ? kwin_env : (int64_t(1) << 18);
@@ -1338,7 +1363,7 @@ void sketch_apply_sparse_compact_dev(slq_ctx* ctx, const slq_sparse* A, int64_t 
         const size_t smem = sizeof(double) * rmax * w + 2 * sizeof(int64_t) * rmax;
         SLQ_CUDA_CHECK(cudaFuncSetAttribute(sparse_gather_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem)));
-        SlabArgs sa{A->s_ptr, A->colidx, A->vals, A->b, n, d, m, S, static_cast<int>(w), static_cast<int>(rmax),
+        SlabArgs sa{tab->p, A->colidx, A->vals, A->b, n, d, m, S, static_cast<int>(w), static_cast<int>(rmax),
                     srow_ptr, sent, val, Y, kwin, nwin, lag, sync};
         void* args[] = {&sa};
         cudaLaunchConfig_t cfg = {};

@@ -311,3 +311,28 @@ def test_sparse_apply_wide_and_narrow_sketches(d, zeta):
     Acsc, A = rand_csc(m, 90, 0.05, d + zeta, long_rows=2, empty_rows=2)
     b = np.random.default_rng(d).standard_normal(m)
     assert _sketch_vs_oracle(Acsc, b, d, zeta, 31)
+
+
+def test_sparse_apply_slab_tables_per_geometry(monkeypatch):
+    """One matrix sketched under six slab geometries (the per-matrix cache holds
+    four: the oldest is retired), then again after its right-hand side changed
+    and after prepare() (tables dropped and rebuilt): bit-exact every time."""
+    m, n, d, zeta = 4000, 130, 500, 8
+    Acsc, A = rand_csc(m, n, 0.06, 77, long_rows=1)
+    b = np.random.default_rng(7).standard_normal(m)
+    Yo, Sbo = C.sketch_apply_csc(d, zeta, 9, m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, b)
+    dm = slq.SparseDeviceMatrix.from_csc(Acsc, b)
+    for wcap in ("32", "40", "48", "64", "100", None, "32"):
+        if wcap:
+            monkeypatch.setenv("SLQ_K2S_W", wcap)
+        else:
+            monkeypatch.delenv("SLQ_K2S_W", raising=False)
+        Yd, Sbd = dm.sketch(d, zeta, 9)
+        assert np.array_equal(Yd, Yo) and np.array_equal(Sbd, Sbo)
+    b2 = np.random.default_rng(8).standard_normal(m)
+    dm.set_rhs(b2)
+    dm.prepare()
+    Yo2, Sbo2 = C.sketch_apply_csc(d, zeta, 9, m, n, Acsc.row_indices, Acsc.values, Acsc.col_pointers, b2)
+    Yd, Sbd = dm.sketch(d, zeta, 9)
+    assert np.array_equal(Yd, Yo2) and np.array_equal(Sbd, Sbo2)
+    dm.free()
