@@ -721,40 +721,6 @@ __global__ void __launch_bounds__(1024) tile_bucketize_kernel(TileBucketArgs a) 
         }
         __syncwarp();
     }
-    // bank-aware grouping: gather_dmma_kernel reads a group's four A rows with
-    // one LDS.128 per lane from the 128-byte-swizzled stage, and two rows
-    // k1, k2 share banks there iff ((k1 ^ k2) & 6) == 0; so the tile's list is
-    // regrouped (deterministically, no extra padding) such that each group of
-    // four takes distinct classes (k >> 1) & 3 while it can.  The summation
-    // order changes (fast mode has no reference order; exact mode does not
-    // use this layout).
-    __syncthreads();
-    for (int t = tid; t < ntile; t += 1024) {
-        const int nt = tot[t];
-        if (nt <= 4 || nt > 64) continue;
-        uint16_t* lst = a.out + (c * a.nrb + t / kTdTiles) * a.blk_stride + kTdHdr + off[t];
-        uint16_t ev[64];
-        int left[4] = {0, 0, 0, 0}, cur[4] = {0, 0, 0, 0};
-        for (int i = 0; i < nt; ++i) {
-            ev[i] = lst[i];
-            ++left[(ev[i] >> 1) & 3];
-        }
-        for (int o = 0; o < nt;) {
-            unsigned used = 0;
-            for (int slot = 0; slot < 4 && o < nt; ++slot) {
-                int best = -1, bc = 0;
-                for (int q = 0; q < 4; ++q)
-                    if (!((used >> q) & 1u) && left[q] > bc) best = q, bc = left[q];
-                if (best < 0)
-                    for (int q = 0; q < 4; ++q)
-                        if (left[q] > bc) best = q, bc = left[q];
-                while (((ev[cur[best]] >> 1) & 3) != best) ++cur[best];
-                lst[o++] = ev[cur[best]++];
-                --left[best];
-                used |= 1u << best;
-            }
-        }
-    }
     // padding and headers
     for (int t = tid; t < ntile; t += 1024) {
         uint16_t* blk = a.out + (c * a.nrb + t / kTdTiles) * a.blk_stride;

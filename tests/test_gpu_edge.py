@@ -27,8 +27,13 @@ def test_pipeline_edge_shapes(m, n, d, zeta):
     M, Q = C.build_preconditioner(Yo)
     x0 = C.initial_guess(M, Q, Sbo)
     xo, repo = C.lsqr(A, M, b, x0, eps=0.0, maxit=T, one_sync=True)
-    assert rep.iterations == repo.iterations
-    assert rep.termination.name.lower() == repo.termination
+    if n > T:
+        # for n <= T the Krylov space is exhausted after n steps: whether the next
+        # beta / alpha is an exact zero (Breakdown) or a rounding-level value
+        # (MaxIter) depends on the summation order of the fast-mode sketch, so
+        # only x is compared there (as tests/test_gpu_sparse.py does)
+        assert rep.iterations == repo.iterations
+        assert rep.termination.name.lower() == repo.termination
     # d = n + 1 gives a poorly embedding sketch and slow, rounding-sensitive
     # Krylov iterates: the oracle's own standard vs one-sync variants differ
     # by ~1e-8 here (the reference's bar for that pair, test_solvers.cpp:149-185)
