@@ -493,6 +493,8 @@ int slq_ctx_destroy(slq_ctx* ctx) {
         cudaStreamSynchronize(ctx->stream);
         slq::comm_destroy(ctx);
         if (ctx->lsqr_exec) cudaGraphExecDestroy(ctx->lsqr_exec);
+        for (auto& g : ctx->qr_graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
         if (ctx->lsqr_hdone) cudaFreeHost(ctx->lsqr_hdone);
         if (ctx->aux) cudaStreamDestroy(ctx->aux);
         for (cudaEvent_t e : ctx->aux_ev)
@@ -515,6 +517,9 @@ int slq_ctx_set_stream(slq_ctx* ctx, void* s) {
         if (ctx->lsqr_exec) cudaGraphExecDestroy(ctx->lsqr_exec);
         ctx->lsqr_exec = nullptr;
         ctx->lsqr_key.clear();
+        for (auto& g : ctx->qr_graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+        ctx->qr_graphs.clear();
         ctx->stream = static_cast<cudaStream_t>(s);
         ctx->own_stream = false;
     });

@@ -143,6 +143,14 @@ struct slq_ctx {
     // QR look-ahead streams (panel + narrow update / wide update) and events
     cudaStream_t qr_hi = nullptr, qr_lo = nullptr;
     cudaEvent_t qr_ev[3] = {nullptr, nullptr, nullptr};
+    // cached QR panel schedules (one CUDA graph per shape / buffer set, captured
+    // on the second solve that uses it: the first sizes the workspace)
+    struct QrGraph {
+        std::vector<uint64_t> key;
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+    };
+    std::vector<QrGraph> qr_graphs;
     int* lsqr_hdone = nullptr;            // pinned done-flag mirror (2 ints)
     int64_t lsqr_live_m = -1, lsqr_live_n = -1;  // shape whose LSQR vectors the workspace holds
     // Inside slq_solve: error conditions found on the device (rank-deficient

@@ -1235,8 +1235,23 @@ void qr_factor_core(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nc
     double* part = misc + 2 * n;          // 1024 partial maxima
     double* rank_tol = misc + 2 * n + 1024;
     int* err = static_cast<int*>(ws.flags.ensure(4096)) + 4;
+    if (n == 0) {
+        SLQ_CUDA_CHECK(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+        return;
+    }
+    // The panel schedule (rank tolerance, panels, narrow / wide updates on the
+    // two look-ahead streams) is ~100 launches plus cross-stream events, whose
+    // gaps on the panel chain cost ~15 us per panel; inside a solve (device
+    // status, no host reads) it is replayed as one CUDA graph per shape and
+    // buffer set.  The first use of a key runs plainly (and sizes the
+    // workspace), the second captures, later ones replay.
+    static const bool pprof_env = slq_env_flag("SLQ_PANEL_PROF");
+    static const bool no_graph = slq_env_flag("SLQ_NO_QR_GRAPH");  // diagnostics
+    cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+    SLQ_CUDA_CHECK(cudaStreamIsCapturing(ctx->stream, &cap_status));
+    const bool graphable = ctx->defer_status && !pprof_env && !no_graph && cap_status == cudaStreamCaptureStatusNone;
+    auto schedule = [&]() {
     SLQ_CUDA_CHECK(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
-    if (n == 0) return;
 
     const int nmax = 1024;
     const int nb_blocks = static_cast<int>(std::min<int64_t>(nmax, ceil_div(d * n, 256)));
@@ -1336,6 +1351,55 @@ void qr_factor_core(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nc
     SLQ_CUDA_CHECK(cudaEventRecord(ev_p, s_hi));
     SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ev_p, 0));
     if (w_pending) SLQ_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ev_w, 0));
+    };  // schedule
+    if (!graphable) {
+        schedule();
+    } else {
+        auto make_key = [&]() {
+            return std::vector<uint64_t>{
+                reinterpret_cast<uint64_t>(Yaug), static_cast<uint64_t>(d), static_cast<uint64_t>(n),
+                static_cast<uint64_t>(ncols), static_cast<uint64_t>(ldy), reinterpret_cast<uint64_t>(T),
+                reinterpret_cast<uint64_t>(misc), reinterpret_cast<uint64_t>(err), reinterpret_cast<uint64_t>(ws.qr_w.p),
+                reinterpret_cast<uint64_t>(ws.qr_cnt.p), reinterpret_cast<uint64_t>(ws.qr_w2.p),
+                reinterpret_cast<uint64_t>(ws.qr_cnt2.p), reinterpret_cast<uint64_t>(tol), static_cast<uint64_t>(tol_given),
+                reinterpret_cast<uint64_t>(ctx->stream), reinterpret_cast<uint64_t>(ctx->qr_hi),
+                reinterpret_cast<uint64_t>(ctx->qr_lo)};
+        };
+        const std::vector<uint64_t> key = make_key();
+        slq_ctx::QrGraph* g = nullptr;
+        for (auto& e : ctx->qr_graphs)
+            if (e.key == key) g = &e;
+        if (!g) {  // first use: plain, and remember the key
+            schedule();
+            if (ctx->qr_graphs.size() >= 8) {
+                if (ctx->qr_graphs.front().exec) cudaGraphExecDestroy(ctx->qr_graphs.front().exec);
+                ctx->qr_graphs.erase(ctx->qr_graphs.begin());
+            }
+            ctx->qr_graphs.push_back(slq_ctx::QrGraph{make_key(), nullptr, 0});
+        } else {
+            if (!g->exec) {
+                const int64_t l0 = ctx->launches;
+                cudaGraph_t graph = nullptr;
+                SLQ_CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+                try {
+                    schedule();
+                } catch (...) {  // leave the stream out of capture mode
+                    cudaStreamEndCapture(ctx->stream, &graph);
+                    if (graph) cudaGraphDestroy(graph);
+                    ctx->launches = l0;
+                    throw;
+                }
+                SLQ_CUDA_CHECK(cudaStreamEndCapture(ctx->stream, &graph));
+                SLQ_CUDA_CHECK(cudaGraphInstantiate(&g->exec, graph, 0));
+                cudaGraphDestroy(graph);
+                g->launches = ctx->launches - l0;
+                ctx->launches = l0;  // captured, not launched
+                if (make_key() != key) fail(SLQ_CUDA, "householder_qr: workspace moved during graph capture");
+            }
+            SLQ_CUDA_CHECK(cudaGraphLaunch(g->exec, ctx->stream));
+            ctx->launches += g->launches;
+        }
+    }
     if (ctx->defer_status) {
         defer_status_dev(ctx, err, kCondNonzero, SLQ_RANK_DEFICIENT);  // checked at the end of the solve
     } else {
