@@ -916,10 +916,14 @@ struct GemmBatch {
                     // 1: M12 = -M11 * T (A = M11; B = T)
 };
 
-// 64 x 64 output tile per CTA, 8 warps (each 32 x 16 = 4 x 2 DMMA tiles), K in steps of 16 via smem
+// 64 x 64 output tile per CTA, 8 warps (each 32 x 16 = 4 x 2 DMMA tiles), K in
+// steps of 16 through double-buffered shared memory: the next step's operands
+// are loaded into registers (unconditionally, clamped addresses; a predicated
+// load + default move would wait for the load) while the current step's DMMAs
+// run, so each step costs one barrier and no exposed load latency.
 __global__ void __launch_bounds__(256) merge_gemm_kernel(GemmBatch g) {
-    __shared__ double As[64][17];
-    __shared__ double Bs[16][65];
+    __shared__ double As[2][64][17];
+    __shared__ double Bs[2][16][65];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int lr = lane & 3, lg = lane >> 2;
     const int64_t a = g.base + static_cast<int64_t>(blockIdx.z) * g.step;  // merge start
@@ -941,37 +945,55 @@ __global__ void __launch_bounds__(256) merge_gemm_kernel(GemmBatch g) {
         Ab = g.A + a * g.ld + a;      // M[a:b, a:b]
         Bb = g.B + b * g.ld;          // T stored at rows [0, half), cols [b, e) of the scratch (ld)
     }
+    // this thread's 4 + 4 staging elements: A (i = t % 64, k = t / 64), B (k = t % 16, j = t / 16)
+    double ra[4], rb[4];
+    auto load = [&](int64_t k0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = tid + 256 * q;
+            const int64_t gi = min(r0 + t % 64, P - 1), gka = min(k0 + t / 64, K - 1);
+            ra[q] = Ab[gka * g.ld + gi];
+            const int64_t gkb = min(k0 + t % 16, K - 1), gj = min(c0 + t / 16, Qn - 1);
+            rb[q] = Bb[gj * g.ld + gkb];
+        }
+    };
+    auto store = [&](int64_t k0, int buf) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = tid + 256 * q;
+            const int i = t % 64, ka = t / 64, kb2 = t % 16, j = t / 16;
+            As[buf][i][ka] = (r0 + i < P && k0 + ka < K) ? ra[q] : 0.0;
+            Bs[buf][kb2][j] = (k0 + kb2 < K && c0 + j < Qn) ? rb[q] : 0.0;
+        }
+    };
     double acc[4][2][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const int wr = (warp >> 2) * 32, wc = (warp & 3) * 16;
+    load(0);
+    store(0, 0);
+    __syncthreads();
+    int buf = 0;
     for (int64_t k0 = 0; k0 < K; k0 += 16) {
-        for (int t = tid; t < 64 * 16; t += 256) {
-            const int i = t % 64, k = t / 64;
-            const int64_t gi = r0 + i, gk = k0 + k;
-            As[i][k] = (gi < P && gk < K) ? Ab[gk * g.ld + gi] : 0.0;
-        }
-        for (int t = tid; t < 16 * 64; t += 256) {
-            const int k = t % 16, j = t / 16;
-            const int64_t gk = k0 + k, gj = c0 + j;
-            Bs[k][j] = (gk < K && gj < Qn) ? Bb[gj * g.ld + gk] : 0.0;
-        }
-        __syncthreads();
+        const bool more = k0 + 16 < K;
+        if (more) load(k0 + 16);
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const double af = As[wr + i * 8 + lg][ks * 4 + lr];
+                const double af = As[buf][wr + i * 8 + lg][ks * 4 + lr];
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
-                    const double bf = Bs[ks * 4 + lr][wc + j * 8 + lg];
+                    const double bf = Bs[buf][ks * 4 + lr][wc + j * 8 + lg];
                     dmma(acc[i][j][0], acc[i][j][1], af, bf);
                 }
             }
         }
+        if (more) store(k0 + 16, buf ^ 1);
         __syncthreads();
+        buf ^= 1;
     }
     double* Cb = (g.mode == 0) ? g.C + b * g.ld : g.C + b * g.ld + a;  // mode 0: scratch T rows [0,half); mode 1: M[a:b, b:e]
 #pragma unroll
