@@ -23,6 +23,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -1245,6 +1246,19 @@ __global__ void rank_tol_copy_kernel(const double* src, double* dst) {
 // tol (device, may be null): rank tolerance to use instead of 1e-12 max|Y| --
 // TSQR leaves pass 0 (only an exactly zero column fails there) and the top of
 // the tree the tolerance of the ORIGINAL Y.
+namespace {
+bool profiler_injected() {
+    std::FILE* f = std::fopen("/proc/self/maps", "r");
+    if (!f) return false;
+    char line[4096];
+    bool hit = false;
+    while (!hit && std::fgets(line, sizeof line, f))
+        hit = std::strstr(line, "libcuda-injection") != nullptr || std::strstr(line, "InjectionTarget") != nullptr;
+    std::fclose(f);
+    return hit;
+}
+}  // namespace
+
 void qr_factor_core(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t ncols, int64_t ldy, double* R,
                     double* qtb, double* Q, double* sign_out, const double* tol, bool tol_given) {
     if (d < n) fail(SLQ_DIMENSION_MISMATCH, "householder_qr: need rows >= cols");
@@ -1268,7 +1282,12 @@ void qr_factor_core(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nc
     // buffer set.  The first use of a key runs plainly (and sizes the
     // workspace), the second captures, later ones replay.
     static const bool pprof_env = slq_env_flag("SLQ_PANEL_PROF");
-    static const bool no_graph = slq_env_flag("SLQ_NO_QR_GRAPH");  // diagnostics
+    // SLQ_NO_QR_GRAPH=1: diagnostics.  Under a CUDA tools injection (Nsight
+    // Compute maps libcuda-injection.so into the process) the schedule runs
+    // plainly: ncu's per-node replay of the captured cluster launches fails
+    // (LaunchFailed; its --graph-profiling graph mode works), and plain launches
+    // give the per-kernel launch lists the profiles are made of.
+    static const bool no_graph = slq_env_flag("SLQ_NO_QR_GRAPH") || profiler_injected();
     cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
     SLQ_CUDA_CHECK(cudaStreamIsCapturing(ctx->stream, &cap_status));
     const bool graphable = ctx->defer_status && !pprof_env && !no_graph && cap_status == cudaStreamCaptureStatusNone;

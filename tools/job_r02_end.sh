@@ -15,3 +15,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-n
 for f in default reference c1 c2 c4; do python -c "
 import json; d=json.loads(open('gpurun_out/bench_end_$f.jsonl').read().strip().splitlines()[-1]); print('$f', d.get('value'), d.get('e2e',{}).get('value') if isinstance(d.get('e2e'),dict) else None, d.get('roofline',{}).get('frac') if isinstance(d.get('roofline'),dict) else None, d.get('clocks'))" 2>&1 | tail -1; done
 cat gpurun_out/bench_end_walltime.txt
+SLQ_GUARD=1 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/gputests_end_guard.log 2>&1; echo "guard suite rc=$?" >> gpurun_out/gputests_end_guard.log; tail -2 gpurun_out/gputests_end_guard.log
