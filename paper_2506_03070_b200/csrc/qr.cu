@@ -1290,7 +1290,9 @@ void qr_factor_core(slq_ctx* ctx, double* Yaug, int64_t d, int64_t n, int64_t nc
     static const bool no_graph = slq_env_flag("SLQ_NO_QR_GRAPH") || profiler_injected();
     cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
     SLQ_CUDA_CHECK(cudaStreamIsCapturing(ctx->stream, &cap_status));
-    const bool graphable = ctx->defer_status && !pprof_env && !no_graph && cap_status == cudaStreamCaptureStatusNone;
+    // (the legacy default stream cannot be captured)
+    const bool graphable = ctx->stream != nullptr && ctx->defer_status && !pprof_env && !no_graph &&
+                           cap_status == cudaStreamCaptureStatusNone;
     auto schedule = [&]() {
     SLQ_CUDA_CHECK(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
 

@@ -85,3 +85,30 @@ def test_wrap_zeroes_nonfinite_padding():
     assert np.all(np.isfinite(x))
     xr, _, _ = slq.solve(np.asfortranarray(A), 24, 4, 7, slq.SolveOptions(eps=0.0, maxit=10), b=b)
     assert np.linalg.norm(x - xr) <= 1e-12 * np.linalg.norm(xr)
+
+
+def test_solve_on_legacy_and_user_streams():
+    """The same solve on a context bound to the legacy default stream (which
+    cannot be captured: no CUDA graphs there), on a caller's stream and on the
+    library's own stream, three times each (first use, graph capture, graph
+    replay): bit-identical solutions."""
+    import torch
+
+    m, n, d, zeta = 20000, 70, 280, 8
+    A = C.gen_dense(m, n, 1e3, 5)
+    b, _ = C.gen_rhs(A, 0.5, 6)
+    opts = slq.SolveOptions(eps=0.0, maxit=12)
+    dm0 = slq.DeviceMatrix.from_numpy(A, b)
+    ref, _, _ = slq.solve(dm0, d, zeta, 3, opts)
+    dm0.free()
+    user = torch.cuda.Stream()
+    for ptr in (0, user.cuda_stream, None):
+        ctx = slq.Context(0)
+        if ptr is not None:
+            ctx.set_stream(ptr)
+        dm = slq.DeviceMatrix.from_numpy(A, b, ctx=ctx)
+        for _ in range(3):
+            x, rep, _ = slq.solve(dm, d, zeta, 3, opts, ctx=ctx)
+            assert rep.iterations == 12
+            assert np.array_equal(x, ref)
+        dm.free()
