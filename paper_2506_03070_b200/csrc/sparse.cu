@@ -296,14 +296,17 @@ __global__ void __launch_bounds__(512) sparse_gather_kernel(SGatherArgs g) {
 // the slab's part of each A row -- a contiguous segment of the row, since
 // CSR rows are sorted by column, located by the per-row slab table P (built
 // once per matrix).  The grid walks k in windows of kwin A rows with a soft
-// barrier (a CTA may run `lag` windows ahead of the slowest), so an A row
-// segment comes from DRAM once and from L2 for its other target rows.
+// barrier (per-warp counters; a warp may run `lag` windows ahead of the
+// slowest), so an A row segment mostly comes from L2 for its other target rows
+// (measured: 36.5 GB of DRAM reads at C4 vs 113 GB for the row gather).
 //
 // Same per-element order as the row gather (for Y[r, j]: ascending k), so the
 // same bits.  A warp serves four Y rows at once (8-lane groups), each group
 // walks its row's entries in ascending k in batches of 8 (lane l holds entry
-// l): entries two batches ahead, table lookups one batch ahead, the segment
-// loads of a batch issued before the previous batch is added.
+// l): entries two batches ahead, the next batch's table words loaded before
+// the current batch is added, its segment loads issued right after; the adds
+// are branch-free shared-memory read-modify-writes (both slots of an entry
+// loaded before either is stored).  L1/LSU-bound (84 % at C4).
 constexpr int kSlW = 16;      // warps per CTA
 constexpr int kSlB = 8;       // entries per group batch
 
