@@ -323,7 +323,6 @@ __global__ void __launch_bounds__(kRegPanelThreads, 1) panel_reg_kernel(PanelArg
     extern __shared__ __align__(16) double w[];  // [rpc][kWs] staging for the coalesced load / store
     __shared__ double red[2][kRegWarps][32];  // warp partials, double-buffered by column parity
     __shared__ double rrow[2][32];
-    __shared__ __align__(16) double mine[2][64];  // this CTA's (G_j, R_j) pairs (bulk-copied to peers)
     __shared__ __align__(16) double tot[2][64];   // cluster sums, broadcast to the CTA's warps
     __shared__ __align__(16) double inbox[2][16][64];
     __shared__ double Ts[kNbMax][kNbMax + 1];
@@ -388,24 +387,23 @@ __global__ void __launch_bounds__(kRegPanelThreads, 1) panel_reg_kernel(PanelArg
                 t2 += red[p][q + 2][lane];
                 t3 += red[p][q + 3][lane];
             }
-            *reinterpret_cast<double2*>(&mine[p][2 * lane]) = make_double2((t0 + t1) + (t2 + t3), r0 ? rrow[p][lane] : 0.0);
+            const double2 mv = make_double2((t0 + t1) + (t2 + t3), r0 ? rrow[p][lane] : 0.0);
             if (lane == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
                              "r"(static_cast<unsigned>(nr * 64 * sizeof(double)))
                              : "memory");
-        }
-        __syncthreads();
-        if (wid < static_cast<int>(nr)) {
-            // warp q pushes the vector to CTA q (DSMEM store completing bytes on
-            // the peer's mbarrier): the 16 pushes leave in parallel
-            const double2 mv = *reinterpret_cast<const double2*>(&mine[p][2 * lane]);
+            // warp 0 pushes the vector to every CTA (DSMEM stores completing
+            // bytes on the peers' mbarriers) straight from registers: no block
+            // barrier between the sum and the pushes
             const unsigned slot = static_cast<unsigned>(__cvta_generic_to_shared(&inbox[p][rank][2 * lane]));
-            unsigned rslot, rbar;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rslot) : "r"(slot), "r"(wid));
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rbar) : "r"(bar), "r"(wid));
-            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(rslot),
-                         "d"(mv.x), "d"(mv.y), "r"(rbar)
-                         : "memory");
+            for (unsigned q = 0; q < nr; ++q) {
+                unsigned rslot, rbar;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rslot) : "r"(slot), "r"(q));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rbar) : "r"(bar), "r"(q));
+                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(rslot),
+                             "d"(mv.x), "d"(mv.y), "r"(rbar)
+                             : "memory");
+            }
         }
         if (prof) prof[kk * 8 + 2] = clock64();
         if (wid == 0) {
