@@ -327,6 +327,10 @@ __global__ void __launch_bounds__(kRegPanelThreads, 1) panel_reg_kernel(PanelArg
     __shared__ __align__(16) double inbox[2][16][64];
     __shared__ double Ts[kNbMax][kNbMax + 1];
     __shared__ uint64_t mbar[2];
+    // the pivot column's values of each warp's rows, by column parity: written
+    // by the column's owner lane, read by all 32 lanes (broadcast loads,
+    // 16 bytes per access) instead of two 64-bit shuffles per row per column
+    __shared__ __align__(16) double piv[2][kRegWarps][RS];
     cg::cluster_group cl = cg::this_cluster();
     if (threadIdx.x == 0) {
         for (int q = 0; q < 2; ++q) {
@@ -359,12 +363,20 @@ __global__ void __launch_bounds__(kRegPanelThreads, 1) panel_reg_kernel(PanelArg
     const double rank_tol = *a.rank_tol;
 
     // partial G for column 0 (rows strictly below the panel's first diagonal row)
+    if (lane == 0)
+#pragma unroll
+        for (int s = 0; s < RS; s += 2)
+            *reinterpret_cast<double2*>(&piv[0][wid][s]) = make_double2(v[s], v[s + 1]);
+    __syncwarp();
     double g = 0.0;
 #pragma unroll
-    for (int s = 0; s < RS; ++s) {
-        const int il = wid + kRegWarps * s;
-        const double vk = __shfl_sync(0xffffffffu, v[s], 0);
-        if (il < nrows && (!r0 || il > 0)) g = fma(v[s], vk, g);
+    for (int s = 0; s < RS; s += 2) {
+        const double2 vk = *reinterpret_cast<const double2*>(&piv[0][wid][s]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int il = wid + kRegWarps * (s + h);
+            if (il < nrows && (!r0 || il > 0)) g = fma(v[s + h], h ? vk.y : vk.x, g);
+        }
     }
 
     long long* prof = (a.prof && tid == 0) ? a.prof + static_cast<int64_t>(rank) * 32 * 8 : nullptr;
@@ -473,20 +485,37 @@ __global__ void __launch_bounds__(kRegPanelThreads, 1) panel_reg_kernel(PanelArg
         g = 0.0;
         const int kn = kk + 1 < 32 ? kk + 1 : 31;
         const bool isk = lane == kk;
+        bool accs[RS];
+        // this column's pivot values (stored by lane kk at the end of the previous column)
 #pragma unroll
-        for (int s = 0; s < RS; ++s) {
-            const int il = wid + kRegWarps * s;
-            const double wk = __shfl_sync(0xffffffffu, v[s], kk);
-            double nv = isk ? wk * rv0 : fma(-cj, wk, v[s]);
-            bool acc = true;
-            if (s < 2 && r0) {
-                if (il < kk) nv = v[s];
-                else if (il == kk) nv = isk ? beta : v[s] - sj;
-                acc = il > kk + 1;
+        for (int s = 0; s < RS; s += 2) {
+            const double2 wk2 = *reinterpret_cast<const double2*>(&piv[p][wid][s]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int ss = s + h, il = wid + kRegWarps * ss;
+                const double wk = h ? wk2.y : wk2.x;
+                double nv = isk ? wk * rv0 : fma(-cj, wk, v[ss]);
+                bool acc = true;
+                if (ss < 2 && r0) {
+                    if (il < kk) nv = v[ss];
+                    else if (il == kk) nv = isk ? beta : v[ss] - sj;
+                    acc = il > kk + 1;
+                }
+                v[ss] = nv;
+                accs[ss] = acc;
             }
-            v[s] = nv;
-            const double wn = __shfl_sync(0xffffffffu, nv, kn);
-            if (acc) g = fma(nv, wn, g);
+        }
+        // the next column's pivot values: lane kn's updated rows (the other parity's buffer)
+        if (lane == kn)
+#pragma unroll
+            for (int s = 0; s < RS; s += 2)
+                *reinterpret_cast<double2*>(&piv[p ^ 1][wid][s]) = make_double2(v[s], v[s + 1]);
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < RS; s += 2) {
+            const double2 wn2 = *reinterpret_cast<const double2*>(&piv[p ^ 1][wid][s]);
+            if (accs[s]) g = fma(v[s], wn2.x, g);
+            if (accs[s + 1]) g = fma(v[s + 1], wn2.y, g);
         }
         if (prof) prof[kk * 8 + 5] = clock64();
     }
